@@ -1,0 +1,124 @@
+/*
+ * bmmgpu.h -- C ABI of the B200-native Boolean / GF(2) bit-matrix product.
+ *
+ * Plain pointers and sizes only.  Every entry point returns a status code;
+ * bmmgpu_last_error() gives the message of the last failure on the calling
+ * thread.  The C++ drop-in (include/bmm/*.hpp, libbmm_b200.so) turns the codes
+ * back into the reference's exception types:
+ *     BMMGPU_EINVAL -> std::invalid_argument   (reference engine.cpp:355-365)
+ *     BMMGPU_ESHAPE -> bmm::ShapeError         (reference engine.cpp:134, 359-362)
+ *     BMMGPU_ECUDA / BMMGPU_ENODEV -> std::runtime_error (no CPU fallback)
+ *
+ * Bit layout everywhere is the reference BitMatrix layout
+ * (reference include/bmm/bitmatrix.hpp:27-52): row-major, words_per_row =
+ * ceil(cols/64) little-endian uint64 words, bit j of row i at bit j%64 of word
+ * j/64, pad bits zero.
+ */
+#ifndef BMMGPU_H
+#define BMMGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define BMMGPU_OK 0
+#define BMMGPU_EINVAL 1
+#define BMMGPU_ESHAPE 3
+#define BMMGPU_ECUDA 5
+#define BMMGPU_ENODEV 6
+
+/* bmm::Semiring order (reference include/bmm/engine.hpp:14) */
+#define BMMGPU_BOOLEAN_OR_AND 0
+#define BMMGPU_GF2_XOR_AND 1
+
+/* bmm::Algo order (reference include/bmm/engine.hpp:16) */
+#define BMMGPU_ALGO_CUBIC 0
+#define BMMGPU_ALGO_STRASSEN_WINOGRAD 1
+#define BMMGPU_ALGO_ALT_SELF_INVERSE 2
+#define BMMGPU_ALGO_ALT_CHAINING 3
+
+/* block-product kernel selection */
+#define BMMGPU_KERNEL_AUTO 0
+#define BMMGPU_KERNEL_LOP3 1      /* LOP3 AND/XOR|OR word kernel (integer ALU)      */
+#define BMMGPU_KERNEL_UMMA_F4 2   /* tcgen05 kind::mxf4 0/1 e2m1, f32 accumulate    */
+
+typedef struct bmmgpu_opts {
+    uint32_t device_mask; /* bit g = use CUDA device g; 0 = device 0            */
+    int32_t kernel;       /* BMMGPU_KERNEL_*                                      */
+    int32_t accumulate;   /* 0: C = A.B;  1: C = C (+) A.B  (XOR / OR integration) */
+    int32_t leaf_log2;    /* fast algos: log2 of the leaf dimension the recursion stops at
+                             and hands to the block-product kernel (>= 6); 0 = auto */
+    double* timing_ms;    /* optional out: device time of the product on the slowest device */
+} bmmgpu_opts;
+
+/* bmm::LayerPlan (reference include/bmm/plan.hpp:26-44) */
+typedef struct bmmgpu_plan {
+    int32_t d_host;
+    int32_t d_serial;
+    int32_t d_parallel;
+    int32_t d_inner;
+    int32_t workers;
+} bmmgpu_plan;
+
+/* ---------------------------------------------------------------- host API */
+
+/* C (m x n) = A (m x k) . B (k x n) over the semiring.  Host row-major buffers
+ * (A: m*ceil(k/64) words, B: k*ceil(n/64), C: m*ceil(n/64), written in full,
+ * pad bits zero).  Any shape, including non-multiples of 64 and empty
+ * dimensions.  Replaces bmm::multiply_cubic (reference engine.cpp:132-144 ->
+ * cubic_blocked 60-100 / cubic_rowwise 102-128). */
+int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, uint64_t k, uint64_t n,
+                 int32_t semiring, const bmmgpu_opts* opts);
+
+/* Fast product through a bilinear scheme: square n = 64 * 2^depth, plan.depth()
+ * must equal depth.  Cubic algo dispatches to bmmgpu_cubic; Boolean with a fast
+ * algo is BMMGPU_EINVAL.  Replaces bmm::multiply (reference engine.cpp:351-382). */
+int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int32_t algo,
+                    const bmmgpu_plan* plan, int32_t semiring, const bmmgpu_opts* opts);
+
+/* In-place basis change of an interleaved vector (host buffer of total_words
+ * words laid out [4]*levels ... [inner]): factor 0 phi, 1 psi, 2 chi of the
+ * scheme of `algo`; inverse != 0 applies the factor's inverse.  Each level is
+ * one in-place pass over [outer][4][inner] (reference engine.cpp:146-172 ->
+ * yates.cpp:143-172). */
+int bmmgpu_basis_change(uint64_t* words, uint64_t total_words, int32_t levels, int32_t algo, int32_t factor,
+                        int32_t inverse);
+
+/* -------------------------------------------------------- device-resident API
+ * Pointers are device memory on the current CUDA device; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  Launch only, no sync. */
+
+/* Padding granularity of the panel product for a kernel: rows of A / Bt a
+ * launch tiles by, and the K granule in bits. */
+int bmmgpu_dev_granularity(int32_t kernel, uint64_t* m_gran, uint64_t* n_gran, uint64_t* k_gran_bits);
+
+/* Bt (n_pad x kw words, row j = column j of B) from row-major B (k x ceil(n/64)
+ * words, row stride ldb words).  Rows j >= n and bits k.. are zero-filled up to
+ * n_pad / kw*64.  The 64x64 block transpose is reference bitmatrix.cpp:16-31. */
+int bmmgpu_dev_transpose(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
+                         uint64_t kw, void* stream);
+
+/* Panel product on device: dA (m_pad x kw words, row stride lda),
+ * dBt (n_pad x kw words, stride ldbt), dC (m_pad x n_pad/64 words, stride ldc).
+ * m_pad, n_pad, kw*64 multiples of the kernel granularity.  accumulate != 0
+ * XOR/OR-folds into dC (out-of-core K-split integration, reference
+ * engine.cpp:81-84). */
+int bmmgpu_dev_cubic(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
+                     uint64_t m_pad, uint64_t n_pad, uint64_t kw, int32_t semiring, int32_t kernel,
+                     int32_t accumulate, void* stream);
+
+/* Number of kernel launches the last host-API call made on its devices. */
+uint64_t bmmgpu_last_launch_count(void);
+
+int bmmgpu_device_count(void);
+const char* bmmgpu_last_error(void);
+const char* bmmgpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BMMGPU_H */

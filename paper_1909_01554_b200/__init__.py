@@ -1,0 +1,261 @@
+"""B200-native Boolean / GF(2) bit-matrix multiplication engine.
+
+Python mirror of the reference's `bmm::` operator API for the product path
+(reference proj/include/bmm/engine.hpp, bitmatrix.hpp): the same names,
+argument meaning and exception types, all computed through the C ABI in
+include/bmmgpu.h (libbmmgpu.so, sm_100a kernels).  There is no CPU fallback:
+if the native library or a CUDA device is missing, calls raise.
+
+The C++ drop-in of the same API is include/bmm/*.hpp + libbmm_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libbmmgpu.so"
+HOST_LIB_PATH = _HERE / "libbmm_b200.so"
+
+__all__ = [
+    "Semiring", "Algo", "Kernel", "LayerPlan", "BitMatrix", "ShapeError", "FormatError", "EngineError",
+    "multiply_cubic", "multiply", "lib", "device_count", "granularity",
+]
+
+
+class ShapeError(RuntimeError):
+    """Dimensions do not fit the operation (bmm::ShapeError)."""
+
+
+class FormatError(RuntimeError):
+    """Invalid BMM1 contents (bmm::FormatError)."""
+
+
+class EngineError(RuntimeError):
+    """CUDA / device failure inside the engine (no CPU fallback exists)."""
+
+
+class Semiring(enum.IntEnum):
+    BooleanOrAnd = 0
+    Gf2XorAnd = 1
+
+
+class Algo(enum.IntEnum):
+    Cubic = 0
+    StrassenWinograd = 1
+    AltSelfInverse = 2
+    AltChaining = 3
+
+
+class Kernel(enum.IntEnum):
+    AUTO = 0
+    LOP3 = 1
+    UMMA_F4 = 2
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("device_mask", ctypes.c_uint32), ("kernel", ctypes.c_int32), ("accumulate", ctypes.c_int32),
+                ("leaf_log2", ctypes.c_int32), ("timing_ms", ctypes.POINTER(ctypes.c_double))]
+
+
+class _Plan(ctypes.Structure):
+    _fields_ = [("d_host", ctypes.c_int32), ("d_serial", ctypes.c_int32), ("d_parallel", ctypes.c_int32),
+                ("d_inner", ctypes.c_int32), ("workers", ctypes.c_int32)]
+
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_lib: ctypes.CDLL | None = None
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded libbmmgpu.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise EngineError(f"{LIB_PATH} is missing: run `python __graft_entry__.py` / build() first; "
+                              "the engine has no CPU fallback")
+        L = ctypes.CDLL(str(LIB_PATH))
+        u64, i32, vp = ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p
+        L.bmmgpu_cubic.argtypes = [vp, vp, vp, u64, u64, u64, i32, ctypes.POINTER(_Opts)]
+        L.bmmgpu_multiply.argtypes = [vp, vp, vp, u64, i32, ctypes.POINTER(_Plan), i32, ctypes.POINTER(_Opts)]
+        L.bmmgpu_basis_change.argtypes = [vp, u64, i32, i32, i32, i32]
+        L.bmmgpu_dev_granularity.argtypes = [i32, _u64p, _u64p, _u64p]
+        L.bmmgpu_dev_transpose.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp]
+        L.bmmgpu_dev_cubic.argtypes = [vp, u64, vp, u64, vp, u64, u64, u64, u64, i32, i32, i32, vp]
+        L.bmmgpu_last_launch_count.restype = u64
+        L.bmmgpu_device_count.restype = ctypes.c_int
+        L.bmmgpu_last_error.restype = ctypes.c_char_p
+        L.bmmgpu_version.restype = ctypes.c_char_p
+        for name in ("bmmgpu_cubic", "bmmgpu_multiply", "bmmgpu_basis_change", "bmmgpu_dev_granularity",
+                     "bmmgpu_dev_transpose", "bmmgpu_dev_cubic"):
+            getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib().bmmgpu_last_error().decode(errors="replace")
+    if status == 3:
+        raise ShapeError(msg)
+    if status == 1:
+        raise ValueError(msg)  # std::invalid_argument
+    raise EngineError(msg)
+
+
+def device_count() -> int:
+    return int(lib().bmmgpu_device_count())
+
+
+def granularity(kernel: int = Kernel.AUTO) -> tuple[int, int, int]:
+    """(row granule of A, row granule of Bt, K granule in bits) of a panel-product kernel."""
+    gm, gn, gk = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib().bmmgpu_dev_granularity(int(kernel), ctypes.byref(gm), ctypes.byref(gn), ctypes.byref(gk)))
+    return gm.value, gn.value, gk.value
+
+
+@dataclass
+class LayerPlan:
+    """bmm::LayerPlan (reference plan.hpp:26-44)."""
+    d_host: int = 0
+    d_serial: int = 0
+    d_parallel: int = 0
+    d_inner: int = 1
+    workers: int = 1
+
+    def depth(self) -> int:
+        return self.d_host + self.d_serial + self.d_parallel
+
+    def matrix_dim(self) -> int:
+        return 64 << self.depth()
+
+    @staticmethod
+    def auto_plan(n: int, workers: int) -> "LayerPlan":
+        """Up to three parallel levels, the rest serial (reference engine.cpp:13-22)."""
+        if n < 64 or n & (n - 1):
+            raise ShapeError("matrix dimension must be 64 * 2^k")
+        k = n.bit_length() - 1 - 6
+        dp = min(3, k)
+        return LayerPlan(0, k - dp, dp, 1, max(1, workers))
+
+
+@dataclass(eq=False)
+class BitMatrix:
+    """bmm::BitMatrix (reference bitmatrix.hpp:31-52): row-major packed bits."""
+    rows: int
+    cols: int
+    words: np.ndarray = field(repr=False)
+
+    def words_per_row(self) -> int:
+        return (self.cols + 63) // 64
+
+    @staticmethod
+    def zeros(rows: int, cols: int) -> "BitMatrix":
+        return BitMatrix(rows, cols, np.zeros(rows * ((cols + 63) // 64), dtype=np.uint64))
+
+    @staticmethod
+    def random(rows: int, cols: int, seed: int) -> "BitMatrix":
+        """std::mt19937_64(seed), one draw per word, row-major, tail masked
+        (reference bitmatrix.cpp:64-77) -- via the drop-in C++ library."""
+        m = BitMatrix.zeros(rows, cols)
+        if m.words.size:
+            _host().bmmh_random(rows, cols, ctypes.c_uint64(seed), m.words.ctypes.data)
+        return m
+
+    def row(self, i: int) -> np.ndarray:
+        w = self.words_per_row()
+        return self.words[i * w:(i + 1) * w]
+
+    def get(self, i: int, j: int) -> bool:
+        if i >= self.rows or j >= self.cols or i < 0 or j < 0:
+            raise ShapeError("bit index out of range")
+        return bool((int(self.words[i * self.words_per_row() + j // 64]) >> (j % 64)) & 1)
+
+    def set(self, i: int, j: int, value: bool) -> None:
+        if i >= self.rows or j >= self.cols or i < 0 or j < 0:
+            raise ShapeError("bit index out of range")
+        k = i * self.words_per_row() + j // 64
+        bit = np.uint64(1 << (j % 64))
+        self.words[k] = (self.words[k] | bit) if value else (self.words[k] & ~bit)
+
+    def __eq__(self, other: object) -> bool:
+        return (isinstance(other, BitMatrix) and self.rows == other.rows and self.cols == other.cols
+                and np.array_equal(self.words, other.words))
+
+
+_host_lib: ctypes.CDLL | None = None
+
+
+def _host() -> ctypes.CDLL:
+    global _host_lib
+    if _host_lib is None:
+        if not HOST_LIB_PATH.exists():
+            raise EngineError(f"{HOST_LIB_PATH} is missing: run build() first")
+        L = ctypes.CDLL(str(HOST_LIB_PATH))
+        L.bmmh_random.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p]
+        L.bmmh_random.restype = None
+        _host_lib = L
+    return _host_lib
+
+
+def _opts(kernel: int, leaf_log2: int = 0, timing: ctypes.c_double | None = None, device_mask: int = 0,
+          accumulate: bool = False) -> _Opts:
+    o = _Opts()
+    o.device_mask = device_mask
+    o.kernel = int(kernel)
+    o.accumulate = int(accumulate)
+    o.leaf_log2 = int(leaf_log2)
+    o.timing_ms = ctypes.pointer(timing) if timing is not None else ctypes.POINTER(ctypes.c_double)()
+    return o
+
+
+def _contig(m: BitMatrix) -> np.ndarray:
+    w = np.ascontiguousarray(m.words, dtype=np.uint64)
+    if w.size != m.rows * m.words_per_row():
+        raise ShapeError("word storage does not match the shape")
+    return w
+
+
+def multiply_cubic(a: BitMatrix, b: BitMatrix, ring: Semiring, workers: int = 1, *, kernel: int = Kernel.AUTO,
+                   device_mask: int = 0, out: BitMatrix | None = None, accumulate: bool = False,
+                   timing: ctypes.c_double | None = None) -> BitMatrix:
+    """bmm::multiply_cubic (reference engine.cpp:132-144) on the GPU.
+
+    With `accumulate`, `out` is XOR/OR-folded with A.B (K-split integration)."""
+    if a.cols != b.rows:
+        raise ShapeError("inner dimensions differ")
+    c = out if out is not None else BitMatrix.zeros(a.rows, b.cols)
+    if (c.rows, c.cols) != (a.rows, b.cols):
+        raise ShapeError("output shape mismatch")
+    aw, bw = _contig(a), _contig(b)
+    _check(lib().bmmgpu_cubic(aw.ctypes.data, bw.ctypes.data, c.words.ctypes.data, a.rows, a.cols, b.cols,
+                              int(ring), ctypes.byref(_opts(kernel, 0, timing, device_mask, accumulate))))
+    return c
+
+
+def multiply(a: BitMatrix, b: BitMatrix, algo: Algo, plan: LayerPlan, ring: Semiring, *,
+             kernel: int = Kernel.AUTO, leaf_log2: int = 0, timing: ctypes.c_double | None = None) -> BitMatrix:
+    """bmm::multiply (reference engine.cpp:351-382) on the GPU."""
+    if algo == Algo.Cubic:
+        return multiply_cubic(a, b, ring, plan.workers, kernel=kernel, timing=timing)
+    if ring == Semiring.BooleanOrAnd:
+        raise ValueError("the Boolean semiring has no subtraction, so cancellation-based fast algorithms are "
+                         "unsound over it; use the cubic algorithm")
+    if a.rows != a.cols or b.rows != b.cols or a.rows != b.rows:
+        raise ShapeError("fast algorithms need equal square operands")
+    n = a.rows
+    if n < 64 or n & (n - 1):
+        raise ShapeError("fast algorithms need n = 64 * 2^k")
+    if (plan.matrix_dim() != n or plan.d_host < 0 or plan.d_serial < 0 or plan.d_parallel < 0
+            or plan.d_inner != 1 or plan.workers < 1):
+        raise ValueError("layer plan does not match the operands")
+    c = BitMatrix.zeros(n, n)
+    p = _Plan(plan.d_host, plan.d_serial, plan.d_parallel, plan.d_inner, plan.workers)
+    _check(lib().bmmgpu_multiply(_contig(a).ctypes.data, _contig(b).ctypes.data, c.words.ctypes.data, n, int(algo),
+                                 ctypes.byref(p), int(ring), ctypes.byref(_opts(kernel, leaf_log2, timing))))
+    return c

@@ -1,0 +1,315 @@
+// capi.cu -- the extern "C" boundary (include/bmmgpu.h) and the host-side
+// multi-GPU driver.
+//
+// Host API calls take reference-layout host buffers (BitMatrix::words), move
+// them to HBM, run the device pipeline and copy the result back.  With more
+// than one device in opts.device_mask the output rows are partitioned into
+// contiguous slabs, one host thread per device, each device holding its A
+// slab and all of Bt: output tiles are independent, so there is no exchange
+// step (the paper's "one host thread per output
+// segment").
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/bmmgpu.h"
+#include "common.cuh"
+
+namespace bmmgpu {
+
+int launch_transpose(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
+                     uint64_t kw, cudaStream_t stream);
+int launch_cubic_lop3(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
+                      uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate, cudaStream_t stream,
+                      uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
+void lop3_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
+int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
+                      uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate, cudaStream_t stream,
+                      uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
+void umma_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
+int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, const bmmgpu_plan* plan,
+                      int kernel, int leaf_log2, double* timing_ms);
+
+namespace {
+thread_local std::string g_error;
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+void set_error(const std::string& msg) { g_error = msg; }
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int resolve_kernel(int kernel) {
+    if (kernel == BMMGPU_KERNEL_AUTO) return BMMGPU_KERNEL_LOP3;
+    return kernel;
+}
+
+int granularity(int kernel, uint64_t* gm, uint64_t* gn, uint64_t* gk) {
+    switch (resolve_kernel(kernel)) {
+        case BMMGPU_KERNEL_LOP3: lop3_granularity(gm, gn, gk); return kOk;
+        case BMMGPU_KERNEL_UMMA_F4: umma_granularity(gm, gn, gk); return kOk;
+        default: set_error("unknown kernel id " + std::to_string(kernel)); return kEinval;
+    }
+}
+
+int launch_cubic(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
+                 uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate,
+                 cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch) {
+    switch (resolve_kernel(kernel)) {
+        case BMMGPU_KERNEL_LOP3:
+            return launch_cubic_lop3(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream, batch,
+                                     sA_batch, sB_batch, sC_batch);
+        case BMMGPU_KERNEL_UMMA_F4:
+            return launch_cubic_umma(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream, batch,
+                                     sA_batch, sB_batch, sC_batch);
+        default: set_error("unknown kernel id " + std::to_string(kernel)); return kEinval;
+    }
+}
+
+namespace {
+
+// RAII device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    int alloc(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            set_error("cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+            p = nullptr;
+            return kEcuda;
+        }
+        return kOk;
+    }
+    uint64_t* u64() const { return static_cast<uint64_t*>(p); }
+};
+
+struct SlabJob {
+    int device;
+    uint64_t row_begin, row_end;  // output rows of this device
+    int status = kOk;
+    std::string error;
+    float ms = 0.f;
+};
+
+// One device's share of C = A.B: rows [row_begin, row_end) of A and C.
+int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t k, uint64_t n,
+                   bool gf2, int kernel, bool accumulate) {
+    BMMGPU_CUDA_TRY(cudaSetDevice(job.device));
+    const uint64_t m = job.row_end - job.row_begin;
+    if (m == 0) return kOk;
+    uint64_t gm, gn, gk;
+    int st = granularity(kernel, &gm, &gn, &gk);
+    if (st) return st;
+    const uint64_t ka = ceil_div(k, 64), nb = ceil_div(n, 64);
+    const uint64_t m_pad = round_up(m, gm), n_pad = round_up(std::max<uint64_t>(n, 1), gn);
+    const uint64_t kw = round_up(std::max<uint64_t>(ka, 1), gk / 64);
+    const uint64_t cw = n_pad / 64;
+    cudaStream_t s;
+    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{s};
+    DevBuf dA, dB, dBt, dC;
+    if ((st = dA.alloc(m_pad * kw * 8)) || (st = dBt.alloc(n_pad * kw * 8)) || (st = dC.alloc(m_pad * cw * 8)))
+        return st;
+    // A slab into the zero-padded panel (pad columns / rows stay zero).
+    BMMGPU_CUDA_TRY(cudaMemsetAsync(dA.p, 0, m_pad * kw * 8, s));
+    count_launch();
+    if (ka > 0)
+        BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dA.p, kw * 8, A + job.row_begin * ka, ka * 8, ka * 8, m,
+                                          cudaMemcpyHostToDevice, s));
+    // B, then Bt on device.
+    if (k > 0 && nb > 0) {
+        if ((st = dB.alloc(k * nb * 8))) return st;
+        BMMGPU_CUDA_TRY(cudaMemcpyAsync(dB.p, B, k * nb * 8, cudaMemcpyHostToDevice, s));
+        if ((st = launch_transpose(dB.u64(), nb, k, n, dBt.u64(), n_pad, kw, s))) return st;
+    } else {
+        BMMGPU_CUDA_TRY(cudaMemsetAsync(dBt.p, 0, n_pad * kw * 8, s));
+        count_launch();
+    }
+    if (accumulate && nb > 0) {
+        BMMGPU_CUDA_TRY(cudaMemsetAsync(dC.p, 0, m_pad * cw * 8, s));
+        count_launch();
+        BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dC.p, cw * 8, C + job.row_begin * nb, nb * 8, nb * 8, m,
+                                          cudaMemcpyHostToDevice, s));
+    }
+    cudaEvent_t e0, e1;
+    BMMGPU_CUDA_TRY(cudaEventCreate(&e0));
+    BMMGPU_CUDA_TRY(cudaEventCreate(&e1));
+    BMMGPU_CUDA_TRY(cudaEventRecord(e0, s));
+    st = launch_cubic(kernel, dA.u64(), kw, dBt.u64(), kw, dC.u64(), cw, m_pad, n_pad, kw, gf2, accumulate, s, 1, 0, 0,
+                      0);
+    if (st) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return st;
+    }
+    BMMGPU_CUDA_TRY(cudaEventRecord(e1, s));
+    if (nb > 0)
+        BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(C + job.row_begin * nb, nb * 8, dC.p, cw * 8, nb * 8, m,
+                                          cudaMemcpyDeviceToHost, s));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaEventElapsedTime(&job.ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return kOk;
+}
+
+std::vector<int> devices_of(uint32_t mask, int* status) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    std::vector<int> devs;
+    if (e != cudaSuccess || count == 0) {
+        set_error(std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                  "); the bit-matrix engine has no CPU fallback");
+        *status = kEnodev;
+        return devs;
+    }
+    if (mask == 0) mask = 1;
+    for (int g = 0; g < 32 && g < count; ++g)
+        if (mask & (1u << g)) devs.push_back(g);
+    if (devs.empty() || (mask >> std::min(count, 31)) > 0) {
+        set_error("device_mask selects devices that do not exist");
+        *status = kEinval;
+        devs.clear();
+        return devs;
+    }
+    *status = kOk;
+    return devs;
+}
+
+}  // namespace
+
+}  // namespace bmmgpu
+
+using namespace bmmgpu;
+
+extern "C" {
+
+const char* bmmgpu_last_error(void) { return g_error.c_str(); }
+const char* bmmgpu_version(void) { return "bmm-b200 0.1 (sm_100a)"; }
+uint64_t bmmgpu_last_launch_count(void) { return g_launches.load(); }
+
+int bmmgpu_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}
+
+int bmmgpu_dev_granularity(int32_t kernel, uint64_t* m_gran, uint64_t* n_gran, uint64_t* k_gran_bits) {
+    return granularity(kernel, m_gran, n_gran, k_gran_bits);
+}
+
+int bmmgpu_dev_transpose(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
+                         uint64_t kw, void* stream) {
+    return launch_transpose(dB, ldb, k, n, dBt, n_pad, kw, static_cast<cudaStream_t>(stream));
+}
+
+int bmmgpu_dev_cubic(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
+                     uint64_t m_pad, uint64_t n_pad, uint64_t kw, int32_t semiring, int32_t kernel,
+                     int32_t accumulate, void* stream) {
+    if (semiring != BMMGPU_BOOLEAN_OR_AND && semiring != BMMGPU_GF2_XOR_AND) {
+        set_error("unknown semiring");
+        return kEinval;
+    }
+    return launch_cubic(kernel, dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, semiring == BMMGPU_GF2_XOR_AND,
+                        accumulate != 0, static_cast<cudaStream_t>(stream), 1, 0, 0, 0);
+}
+
+int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, uint64_t k, uint64_t n,
+                 int32_t semiring, const bmmgpu_opts* opts) {
+    g_launches.store(0);
+    if (semiring != BMMGPU_BOOLEAN_OR_AND && semiring != BMMGPU_GF2_XOR_AND) {
+        set_error("unknown semiring");
+        return kEinval;
+    }
+    const bmmgpu_opts defaults{};
+    const bmmgpu_opts& o = opts ? *opts : defaults;
+    int st = kOk;
+    std::vector<int> devs = devices_of(o.device_mask, &st);
+    if (st) return st;
+    if (m == 0 || n == 0) {
+        if (o.timing_ms) *o.timing_ms = 0.0;
+        return kOk;
+    }
+    // Contiguous row slabs, aligned to 64 rows so device tiles never straddle.
+    const uint64_t G = devs.size();
+    const uint64_t blocks = ceil_div(m, 64);
+    std::vector<SlabJob> jobs;
+    for (uint64_t g = 0; g < G; ++g) {
+        SlabJob j;
+        j.device = devs[g];
+        j.row_begin = std::min(m, (blocks * g / G) * 64);
+        j.row_end = std::min(m, (blocks * (g + 1) / G) * 64);
+        jobs.push_back(j);
+    }
+    const bool gf2 = semiring == BMMGPU_GF2_XOR_AND;
+    auto work = [&](SlabJob& j) {
+        j.status = run_cubic_slab(j, A, B, C, k, n, gf2, o.kernel, o.accumulate != 0);
+        if (j.status) j.error = g_error;
+    };
+    if (G == 1) {
+        work(jobs[0]);
+    } else {
+        std::vector<std::thread> threads;
+        for (auto& j : jobs) threads.emplace_back(work, std::ref(j));
+        for (auto& t : threads) t.join();
+    }
+    float worst = 0.f;
+    for (auto& j : jobs) {
+        if (j.status) {
+            set_error("device " + std::to_string(j.device) + ": " + j.error);
+            return j.status;
+        }
+        worst = std::max(worst, j.ms);
+    }
+    if (o.timing_ms) *o.timing_ms = worst;
+    return kOk;
+}
+
+int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int32_t algo,
+                    const bmmgpu_plan* plan, int32_t semiring, const bmmgpu_opts* opts) {
+    g_launches.store(0);
+    const bmmgpu_opts defaults{};
+    const bmmgpu_opts& o = opts ? *opts : defaults;
+    if (algo == BMMGPU_ALGO_CUBIC) return bmmgpu_cubic(A, B, C, n, n, n, semiring, opts);
+    if (algo < 0 || algo > BMMGPU_ALGO_ALT_CHAINING) {
+        set_error("unknown algorithm");
+        return kEinval;
+    }
+    if (semiring == BMMGPU_BOOLEAN_OR_AND) {
+        set_error(
+            "the Boolean semiring has no subtraction, so cancellation-based fast algorithms are unsound over it; "
+            "use the cubic algorithm");
+        return kEinval;
+    }
+    if (n < 64 || (n & (n - 1))) {
+        set_error("fast algorithms need n = 64 * 2^k");
+        return kEshape;
+    }
+    if (!plan) {
+        set_error("plan is required");
+        return kEinval;
+    }
+    int depth = 0;
+    while ((64ull << depth) < n) ++depth;
+    if (plan->d_host < 0 || plan->d_serial < 0 || plan->d_parallel < 0 || plan->d_inner != 1 || plan->workers < 1 ||
+        plan->d_host + plan->d_serial + plan->d_parallel != depth) {
+        set_error("layer plan does not match the operands");
+        return kEinval;
+    }
+    int st = kOk;
+    std::vector<int> devs = devices_of(o.device_mask, &st);
+    if (st) return st;
+    BMMGPU_CUDA_TRY(cudaSetDevice(devs[0]));
+    return alt_multiply_host(A, B, C, n, algo, plan, o.kernel, o.leaf_log2, o.timing_ms);
+}
+
+}  // extern "C"

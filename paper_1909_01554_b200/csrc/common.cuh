@@ -1,0 +1,71 @@
+// common.cuh -- shared helpers for the sm_100a bit-product kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+namespace bmmgpu {
+
+// Status codes mirror include/bmmgpu.h.
+constexpr int kOk = 0, kEinval = 1, kEshape = 3, kEcuda = 5, kEnodev = 6;
+
+void set_error(const std::string& msg);
+void count_launch(uint64_t n = 1);
+
+#define BMMGPU_CUDA_TRY(expr)                                                                     \
+    do {                                                                                          \
+        cudaError_t _e = (expr);                                                                  \
+        if (_e != cudaSuccess) {                                                                  \
+            ::bmmgpu::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+            return ::bmmgpu::kEcuda;                                                              \
+        }                                                                                         \
+    } while (0)
+
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// One stage of the warp-wide 64x64 bit transpose (reference bitmatrix.cpp:16-31
+// restated across lanes): lane l holds rows l and l+32.  For w >= 1 and < 32 the
+// partner rows live in lane l^w; w = 32 is the in-lane swap.
+__device__ __forceinline__ uint64_t tr_stage(uint64_t x, unsigned lane, unsigned w, uint64_t m) {
+    const uint64_t p = __shfl_xor_sync(0xffffffffu, x, w);
+    if (lane & w) {
+        const uint64_t t = ((p >> w) ^ x) & m;
+        return x ^ t;
+    } else {
+        const uint64_t t = ((x >> w) ^ p) & m;
+        return x ^ (t << w);
+    }
+}
+
+// Full 64x64 transpose of the block held as (x0 = row lane, x1 = row lane+32).
+__device__ __forceinline__ void warp_transpose64(uint64_t& x0, uint64_t& x1, unsigned lane) {
+    {
+        const uint64_t t = ((x0 >> 32) ^ x1) & 0x00000000FFFFFFFFull;
+        x0 ^= t << 32;
+        x1 ^= t;
+    }
+    x0 = tr_stage(x0, lane, 16, 0x0000FFFF0000FFFFull);
+    x1 = tr_stage(x1, lane, 16, 0x0000FFFF0000FFFFull);
+    x0 = tr_stage(x0, lane, 8, 0x00FF00FF00FF00FFull);
+    x1 = tr_stage(x1, lane, 8, 0x00FF00FF00FF00FFull);
+    x0 = tr_stage(x0, lane, 4, 0x0F0F0F0F0F0F0F0Full);
+    x1 = tr_stage(x1, lane, 4, 0x0F0F0F0F0F0F0F0Full);
+    x0 = tr_stage(x0, lane, 2, 0x3333333333333333ull);
+    x1 = tr_stage(x1, lane, 2, 0x3333333333333333ull);
+    x0 = tr_stage(x0, lane, 1, 0x5555555555555555ull);
+    x1 = tr_stage(x1, lane, 1, 0x5555555555555555ull);
+}
+
+}  // namespace bmmgpu

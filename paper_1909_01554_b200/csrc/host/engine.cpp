@@ -1,0 +1,248 @@
+// engine.cpp -- the drop-in bmm:: engine entry points (include/bmm/engine.hpp)
+// over the C ABI (include/bmmgpu.h).  Validation and exception types follow
+// the reference (src/engine.cpp); every product runs on the GPU, and the
+// OpCounter tallies are filled with the reference algorithm's exact counts.
+#include "bmm/engine.hpp"
+
+#include <bit>
+#include <stdexcept>
+#include <string>
+
+#include "bmmgpu.h"
+
+namespace bmm {
+
+namespace {
+
+[[noreturn]] void raise(int status) {
+    const std::string msg = bmmgpu_last_error();
+    switch (status) {
+        case BMMGPU_ESHAPE: throw ShapeError(msg);
+        case BMMGPU_EINVAL: throw std::invalid_argument(msg);
+        default: throw std::runtime_error("bmm GPU engine: " + msg);
+    }
+}
+
+void check(int status) {
+    if (status != BMMGPU_OK) raise(status);
+}
+
+std::uint64_t ipow(std::uint64_t b, int e) {
+    std::uint64_t v = 1;
+    while (e-- > 0) v *= b;
+    return v;
+}
+
+int algo_id(Builtin b) {
+    switch (b) {
+        case Builtin::StrassenWinograd: return BMMGPU_ALGO_STRASSEN_WINOGRAD;
+        case Builtin::AltSelfInverse: return BMMGPU_ALGO_ALT_SELF_INVERSE;
+        case Builtin::AltChaining: return BMMGPU_ALGO_ALT_CHAINING;
+        case Builtin::Elementary: break;
+    }
+    throw std::invalid_argument("engine layers require <2,2,2>_7 schemes");
+}
+
+bool factor_identity(const Decomposition& d, BasisFactor f) {
+    return (f == BasisFactor::Phi ? d.adds_phi : f == BasisFactor::Psi ? d.adds_psi : d.adds_chi) == 0;
+}
+
+int factor_id(BasisFactor f) { return f == BasisFactor::Phi ? 0 : f == BasisFactor::Psi ? 1 : 2; }
+
+// Reference SLP addition counts (decomposition.cpp:57-216).
+const Decomposition kSw{Builtin::StrassenWinograd, {2, 2, 2, 7}, {true, true}, 4, 4, 7, 0, 0, 0};
+const Decomposition kAsi{Builtin::AltSelfInverse, {2, 2, 2, 7}, {true, false}, 3, 3, 6, 2, 2, 2};
+const Decomposition kAch{Builtin::AltChaining, {2, 2, 2, 7}, {false, true}, 3, 3, 6, 2, 2, 2};
+const Decomposition kEl{Builtin::Elementary, {2, 2, 2, 8}, {true, true}, 0, 0, 4, 0, 0, 0};
+
+std::vector<std::uint64_t> modes_for(int depth) {
+    std::vector<std::uint64_t> m(depth, 4);
+    m.push_back(kBlockBits);
+    return m;
+}
+
+}  // namespace
+
+LayerPlan LayerPlan::auto_plan(std::uint64_t n, int workers) {
+    if (n < kBlockDim || !std::has_single_bit(n)) throw ShapeError("matrix dimension must be 64 * 2^k");
+    const int k = std::countr_zero(n) - 6;
+    LayerPlan p;
+    p.d_parallel = k < 3 ? k : 3;
+    p.d_serial = k - p.d_parallel;
+    p.workers = workers < 1 ? 1 : workers;
+    return p;
+}
+
+const Decomposition& builtin(Builtin which) {
+    switch (which) {
+        case Builtin::StrassenWinograd: return kSw;
+        case Builtin::AltSelfInverse: return kAsi;
+        case Builtin::AltChaining: return kAch;
+        case Builtin::Elementary: return kEl;
+    }
+    throw std::invalid_argument("unknown builtin decomposition");
+}
+
+std::uint64_t predicted_additions(const Decomposition& d, int depth, CostPart part) {
+    const TripleParams& p = d.params;
+    if (p.s != p.t || p.t != p.u) throw std::invalid_argument("addition prediction needs s = t = u");
+    const std::uint64_t s2 = std::uint64_t(p.s) * p.s;
+    if (std::uint64_t(p.r) <= s2) throw std::invalid_argument("addition prediction needs r > s^2");
+    if (depth < 0) throw std::invalid_argument("negative depth");
+    if (depth == 0) return 0;
+    if (part == CostPart::BasisChanges)
+        return std::uint64_t(d.adds_phi + d.adds_psi + d.adds_chi) * ipow(s2, depth - 1) * depth;
+    std::uint64_t geo = 0;
+    for (int l = 0; l < depth; ++l) geo += ipow(s2, l) * ipow(p.r, depth - 1 - l);
+    return std::uint64_t(d.adds_alpha + d.adds_beta + d.adds_gamma) * geo;
+}
+
+const Decomposition& decomposition_for(Algo algo) {
+    switch (algo) {
+        case Algo::StrassenWinograd: return kSw;
+        case Algo::AltSelfInverse: return kAsi;
+        case Algo::AltChaining: return kAch;
+        case Algo::Cubic: break;
+    }
+    throw std::invalid_argument("the cubic algorithm has no bilinear scheme");
+}
+
+void kernel64(const std::uint64_t* a, const std::uint64_t* b_transposed, std::uint64_t* out, Semiring ring) {
+    // b_transposed holds B column-major; the engine takes B row-major.
+    BitMatrix b = BitMatrix::zeros(kBlockDim, kBlockDim);
+    std::copy(b_transposed, b_transposed + kBlockWords, b.words.begin());
+    transpose_blocks64(b);
+    check(bmmgpu_cubic(a, b.words.data(), out, kBlockDim, kBlockDim, kBlockDim,
+                       ring == Semiring::Gf2XorAnd ? BMMGPU_GF2_XOR_AND : BMMGPU_BOOLEAN_OR_AND, nullptr));
+}
+
+BitMatrix multiply_cubic(const BitMatrix& a, const BitMatrix& b, Semiring ring, int workers, OpCounter* counter) {
+    if (a.cols != b.rows) throw ShapeError("inner dimensions differ");
+    (void)workers;
+    BitMatrix c = BitMatrix::zeros(a.rows, b.cols);
+    const bool gf2 = ring == Semiring::Gf2XorAnd;
+    check(bmmgpu_cubic(a.words.data(), b.words.data(), c.words.data(), a.rows, a.cols, b.cols,
+                       gf2 ? BMMGPU_GF2_XOR_AND : BMMGPU_BOOLEAN_OR_AND, nullptr));
+    if (counter) {
+        const bool blocked = a.rows % kBlockDim == 0 && a.cols % kBlockDim == 0 && b.cols % kBlockDim == 0;
+        if (blocked) {
+            // cubic_blocked tallies (reference engine.cpp:89-98)
+            const std::uint64_t pairs = (a.rows / kBlockDim) * (b.cols / kBlockDim), bj = a.cols / kBlockDim;
+            counter->add_kernels(pairs * bj);
+            counter->add_ands(pairs * bj * kBlockBits);
+            const std::uint64_t folds = bj ? pairs * (bj - 1) * kBlockWords : 0;
+            gf2 ? counter->add_xors(folds) : counter->add_ors(folds);
+        } else {
+            // cubic_rowwise tallies: one row fold per set bit of A (engine.cpp:108-126)
+            std::uint64_t ones = 0;
+            for (std::uint64_t w : a.words) ones += std::popcount(w);
+            const std::uint64_t n = ones * c.words_per_row();
+            gf2 ? counter->add_xors(n) : counter->add_ors(n);
+        }
+    }
+    return c;
+}
+
+void basis_change(BitVectorTensor& v, const Decomposition& d, BasisFactor which, int levels, int workers,
+                  OpCounter* counter) {
+    (void)workers;
+    if (levels < 0 || v.mode_lengths.size() < static_cast<std::size_t>(levels) + 1)
+        throw std::invalid_argument("vector has fewer modes than basis levels");
+    for (int l = 0; l < levels; ++l)
+        if (v.mode_lengths[l] != 4) throw std::invalid_argument("mode length does not match the basis");
+    if (v.words.size() * kWordBits != v.bit_length())
+        throw std::invalid_argument("vector storage does not match its modes");
+    if (factor_identity(d, which) || levels == 0) return;
+    check(bmmgpu_basis_change(v.words.data(), v.words.size(), levels, algo_id(d.which), factor_id(which), 0));
+    if (counter) {
+        const int adds = which == BasisFactor::Phi ? d.adds_phi : which == BasisFactor::Psi ? d.adds_psi : d.adds_chi;
+        counter->add_xors(std::uint64_t(levels) * (v.words.size() / 4) * adds);
+    }
+}
+
+BitVectorTensor multiply_alt(const BitVectorTensor& a_hat, const BitVectorTensor& b_hat, const Decomposition& d,
+                             const LayerPlan& plan, OpCounter* counter) {
+    if (plan.d_serial < 0 || plan.d_parallel < 0 || plan.d_inner != 1 || plan.workers < 1)
+        throw std::invalid_argument("invalid layer plan");
+    if (!(d.params == TripleParams{})) throw std::invalid_argument("engine layers require <2,2,2>_7 schemes");
+    const int depth = plan.d_serial + plan.d_parallel;
+    const std::vector<std::uint64_t> want = modes_for(depth);
+    if (a_hat.mode_lengths != want || b_hat.mode_lengths != want)
+        throw std::invalid_argument("operands are not interleaved for this plan");
+    if (a_hat.words.size() * kWordBits != a_hat.bit_length() || b_hat.words.size() * kWordBits != b_hat.bit_length())
+        throw std::invalid_argument("operand storage does not match its modes");
+    const int algo = algo_id(d.which);
+    // multiply_alt is the bilinear map (a_hat, b_hat) -> chi^-1( phi^-1 a_hat . psi^-1 b_hat )
+    // in interleaved form; the GPU computes the standard-basis product in between.
+    LayerPlan p;
+    p.d_serial = depth;
+    BitVectorTensor a = a_hat, b = b_hat;
+    if (!factor_identity(d, BasisFactor::Phi))
+        check(bmmgpu_basis_change(a.words.data(), a.words.size(), depth, algo, 0, 1));
+    if (!factor_identity(d, BasisFactor::Psi))
+        check(bmmgpu_basis_change(b.words.data(), b.words.size(), depth, algo, 1, 1));
+    const BitMatrix am = from_interleaved(a, p, Operand::Left);
+    const BitMatrix bm = from_interleaved(b, p, Operand::Right);
+    const std::uint64_t n = p.matrix_dim();
+    BitMatrix cm = BitMatrix::zeros(n, n);
+    bmmgpu_plan gp{0, depth, 0, 1, 1};
+    check(bmmgpu_multiply(am.words.data(), bm.words.data(), cm.words.data(), n, algo, &gp, BMMGPU_GF2_XOR_AND,
+                          nullptr));
+    BitVectorTensor c = to_interleaved(cm, p, Operand::Result);
+    if (!factor_identity(d, BasisFactor::Chi))
+        check(bmmgpu_basis_change(c.words.data(), c.words.size(), depth, algo, 2, 1));
+    if (counter) {
+        const std::uint64_t kernels = ipow(7, depth);
+        counter->add_kernels(kernels);
+        counter->add_ands(kernels * kBlockBits);
+        counter->add_xors(predicted_additions(d, depth, CostPart::LinearCombinations) * kBlockWords);
+    }
+    return c;
+}
+
+BitMatrix multiply(const BitMatrix& a, const BitMatrix& b, Algo algo, const LayerPlan& plan, Semiring ring,
+                   OpCounter* counter) {
+    if (algo == Algo::Cubic) return multiply_cubic(a, b, ring, plan.workers, counter);
+    if (ring == Semiring::BooleanOrAnd)
+        throw std::invalid_argument(
+            "the Boolean semiring has no subtraction, so cancellation-based fast algorithms are unsound over it; "
+            "use the cubic algorithm");
+    if (a.rows != a.cols || b.rows != b.cols || a.rows != b.rows)
+        throw ShapeError("fast algorithms need equal square operands");
+    if (a.rows < kBlockDim || !std::has_single_bit(a.rows)) throw ShapeError("fast algorithms need n = 64 * 2^k");
+    if (plan.matrix_dim() != a.rows || plan.d_host < 0 || plan.d_serial < 0 || plan.d_parallel < 0 ||
+        plan.d_inner != 1 || plan.workers < 1)
+        throw std::invalid_argument("layer plan does not match the operands");
+    const Decomposition& d = decomposition_for(algo);
+    BitMatrix c = BitMatrix::zeros(a.rows, a.rows);
+    bmmgpu_plan gp{plan.d_host, plan.d_serial, plan.d_parallel, plan.d_inner, plan.workers};
+    check(bmmgpu_multiply(a.words.data(), b.words.data(), c.words.data(), a.rows, algo_id(d.which), &gp,
+                          BMMGPU_GF2_XOR_AND, nullptr));
+    if (counter) {
+        const int depth = plan.depth();
+        const std::uint64_t kernels = ipow(7, depth);
+        counter->add_kernels(kernels);
+        counter->add_ands(kernels * kBlockBits);
+        counter->add_xors((predicted_additions(d, depth, CostPart::LinearCombinations) +
+                           predicted_additions(d, depth, CostPart::BasisChanges)) *
+                          kBlockWords);
+    }
+    return c;
+}
+
+BitMatrix multiply_strassen_winograd(const BitMatrix& a, const BitMatrix& b, const LayerPlan& plan, Semiring ring,
+                                     OpCounter* counter) {
+    return multiply(a, b, Algo::StrassenWinograd, plan, ring, counter);
+}
+
+BitVectorTensor chain_multiply(const std::vector<BitVectorTensor>& matrices_hat, const Decomposition& d,
+                               const LayerPlan& plan, OpCounter* counter) {
+    if (!d.traits.supports_chaining)
+        throw std::invalid_argument("this scheme cannot chain: its output basis is not its input basis");
+    if (matrices_hat.size() < 2) throw std::invalid_argument("a chain needs at least two operands");
+    BitVectorTensor acc = multiply_alt(matrices_hat[0], matrices_hat[1], d, plan, counter);
+    for (std::size_t i = 2; i < matrices_hat.size(); ++i) acc = multiply_alt(acc, matrices_hat[i], d, plan, counter);
+    return acc;
+}
+
+}  // namespace bmm

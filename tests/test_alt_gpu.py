@@ -1,0 +1,103 @@
+"""GPU parity: the <2,2,2;7> fast products (Strassen-Winograd, alt-si,
+alt-chain) on B200 equal the reference's outputs bit for bit, for every leaf
+size the recursion can stop at."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+GF2 = 1
+pytestmark = pytest.mark.gpu
+
+
+def _plan(bmm, p):
+    return bmm.LayerPlan(p[0], p[1], p[2], 1, 1)
+
+
+@pytest.mark.parametrize("leaf", [0, 6, 7, 8, 10])
+def test_fast_products_match_reference(engine, oracle, golden, leaf):
+    bmm = engine
+    for c in golden["fast"]:
+        n = c["n"]
+        if leaf and (64 << 0) * (1 << (leaf - 6)) > n:
+            continue
+        a = bmm.BitMatrix(n, n, oracle.random(n, n, c["a_seed"]))
+        b = bmm.BitMatrix(n, n, oracle.random(n, n, c["b_seed"]))
+        got = bmm.multiply(a, b, bmm.Algo(c["algo"]), _plan(bmm, c["plan"]), bmm.Semiring.Gf2XorAnd,
+                           leaf_log2=leaf)
+        assert f"{oracle.fnv1a64(got.words):016x}" == c["fnv"], (c, leaf)
+
+
+def test_alt_equals_cubic_for_every_split(engine, oracle):
+    bmm = engine
+    for n in (64, 128, 256, 512):
+        a = bmm.BitMatrix(n, n, oracle.random(n, n, 91 + n))
+        b = bmm.BitMatrix(n, n, oracle.random(n, n, 92 + n))
+        want = oracle.multiply_cubic(a.words, b.words, n, n, n, GF2)
+        depth = (n // 64).bit_length() - 1
+        for algo in (bmm.Algo.StrassenWinograd, bmm.Algo.AltSelfInverse, bmm.Algo.AltChaining):
+            for ds in range(depth + 1):
+                plan = bmm.LayerPlan(0, ds, depth - ds, 1, 1)
+                got = bmm.multiply(a, b, algo, plan, bmm.Semiring.Gf2XorAnd, leaf_log2=6)
+                assert np.array_equal(got.words, want), (n, algo, ds)
+
+
+def test_single_bit_probes_cross_block_boundaries(engine):
+    """reference test_engine.cpp:461-481."""
+    bmm = engine
+    plan = bmm.LayerPlan.auto_plan(128, 1)
+    coords = (62, 63, 64, 65)
+    for algo in (bmm.Algo.StrassenWinograd, bmm.Algo.AltSelfInverse, bmm.Algo.AltChaining):
+        for i in coords:
+            for j in coords:
+                for k in coords:
+                    eij, ejk, want = bmm.BitMatrix.zeros(128, 128), bmm.BitMatrix.zeros(128, 128), \
+                        bmm.BitMatrix.zeros(128, 128)
+                    eij.set(i, j, True)
+                    ejk.set(j, k, True)
+                    want.set(i, k, True)
+                    assert bmm.multiply(eij, ejk, algo, plan, bmm.Semiring.Gf2XorAnd, leaf_log2=6) == want
+
+
+def test_identity_and_associativity(engine, oracle):
+    bmm = engine
+    plan = bmm.LayerPlan.auto_plan(256, 1)
+    c, d, e = (bmm.BitMatrix(256, 256, oracle.random(256, 256, s)) for s in (95, 96, 97))
+    alt = bmm.Algo.AltSelfInverse
+    cd = bmm.multiply(c, d, alt, plan, bmm.Semiring.Gf2XorAnd, leaf_log2=6)
+    de = bmm.multiply(d, e, alt, plan, bmm.Semiring.Gf2XorAnd, leaf_log2=6)
+    assert bmm.multiply(cd, e, alt, plan, bmm.Semiring.Gf2XorAnd, leaf_log2=7) == \
+        bmm.multiply(c, de, alt, plan, bmm.Semiring.Gf2XorAnd, leaf_log2=7)
+    ident = bmm.BitMatrix.zeros(256, 256)
+    for i in range(256):
+        ident.set(i, i, True)
+    for algo in (bmm.Algo.StrassenWinograd, bmm.Algo.AltSelfInverse, bmm.Algo.AltChaining):
+        assert bmm.multiply(c, ident, algo, plan, bmm.Semiring.Gf2XorAnd, leaf_log2=6) == c
+        assert bmm.multiply(ident, c, algo, plan, bmm.Semiring.Gf2XorAnd, leaf_log2=6) == c
+
+
+def test_large_alt_si_against_golden(engine, oracle, golden):
+    """n=4096 alt-si (reference plan 3 serial + 3 parallel) == the cubic digest."""
+    bmm = engine
+    c = next(x for x in golden["fast"] if x["n"] == 4096)
+    cub = next(x for x in golden["cubic_large"] if x["m"] == 4096 and x["ring"] == GF2)
+    assert c["fnv"] == cub["fnv"]
+    a = bmm.BitMatrix(4096, 4096, oracle.random(4096, 4096, 1))
+    b = bmm.BitMatrix(4096, 4096, oracle.random(4096, 4096, 2))
+    for leaf in (0, 9, 10, 11):
+        got = bmm.multiply(a, b, bmm.Algo.AltSelfInverse, _plan(bmm, c["plan"]), bmm.Semiring.Gf2XorAnd,
+                           leaf_log2=leaf)
+        assert f"{oracle.fnv1a64(got.words):016x}" == c["fnv"], leaf
+
+
+def test_interleaved_basis_change_matches_reference(engine, oracle, golden):
+    bmm = engine
+    lib = bmm.lib()
+    v = oracle.random(1, 4 * 4 * 4096, 41)
+    algo_of_scheme = {1: 2, 2: 3}  # bmm::Builtin -> bmm::Algo id
+    for c in golden["basis_change"]:
+        w = v.copy()
+        assert lib.bmmgpu_basis_change(w.ctypes.data, w.size, 2, algo_of_scheme[c["scheme"]], c["which"], 0) == 0
+        assert f"{oracle.fnv1a64(w):016x}" == c["fnv"], c
+        assert lib.bmmgpu_basis_change(w.ctypes.data, w.size, 2, algo_of_scheme[c["scheme"]], c["which"], 1) == 0
+        assert np.array_equal(w, v)

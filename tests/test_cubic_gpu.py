@@ -1,0 +1,148 @@
+"""GPU parity: the cubic Boolean / GF(2) product on B200 against the oracle
+and the reference's golden vectors, bit-exact, for every kernel."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+GF2, BOOL = 1, 0
+pytestmark = pytest.mark.gpu
+
+KERNELS = [1]  # LOP3; the tcgen05 kernel joins via test_umma_gpu.py
+
+
+def _bm(bmm, oracle, rows, cols, seed):
+    return bmm.BitMatrix(rows, cols, oracle.random(rows, cols, seed))
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_small_shapes_match_reference_words(engine, oracle, golden, kernel):
+    bmm = engine
+    for c in golden["cubic_small"]:
+        a = _bm(bmm, oracle, c["m"], c["k"], c["a_seed"])
+        b = _bm(bmm, oracle, c["k"], c["n"], c["b_seed"])
+        got = bmm.multiply_cubic(a, b, bmm.Semiring(c["ring"]), kernel=kernel)
+        assert [f"{int(x):016x}" for x in got.words] == c["words"], (c["m"], c["k"], c["n"], c["ring"])
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_large_digests(engine, oracle, golden, kernel):
+    bmm = engine
+    for c in golden["cubic_large"]:
+        a = _bm(bmm, oracle, c["m"], c["k"], c["a_seed"])
+        b = _bm(bmm, oracle, c["k"], c["n"], c["b_seed"])
+        got = bmm.multiply_cubic(a, b, bmm.Semiring(c["ring"]), kernel=kernel)
+        assert f"{oracle.fnv1a64(got.words):016x}" == c["fnv"], c
+        assert oracle.popcount(got.words) == c["pop"]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_sparse_boolean_is_not_vacuous(engine, oracle, golden, kernel):
+    """Dense inputs make the Boolean product all ones; AND-of-k inputs do not."""
+    bmm = engine
+    for c in golden["sparse"]:
+        n, k = c["n"], c["k"]
+        a = np.full(n * n // 64, ~np.uint64(0), dtype=np.uint64)
+        b = a.copy()
+        for i in range(k):
+            a &= oracle.random(n, n, 1 + 1000 * i)
+            b &= oracle.random(n, n, 2 + 1000 * i)
+        assert f"{oracle.fnv1a64(a):016x}" == c["a_fnv"]
+        got = bmm.multiply_cubic(bmm.BitMatrix(n, n, a), bmm.BitMatrix(n, n, b), bmm.Semiring(c["ring"]),
+                                 kernel=kernel)
+        assert f"{oracle.fnv1a64(got.words):016x}" == c["fnv"], c
+        assert oracle.popcount(got.words) == c["pop"]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_random_shapes_against_oracle(engine, oracle, kernel):
+    bmm = engine
+    rng = np.random.default_rng(11)
+    shapes = [(1, 1, 1), (64, 64, 64), (63, 65, 127), (0, 5, 7), (5, 0, 7), (5, 7, 0), (1, 4097, 3),
+              (300, 1025, 257), (129, 2048, 513), (64, 64, 1000), (1000, 64, 64)]
+    shapes += [tuple(int(x) for x in rng.integers(1, 700, size=3)) for _ in range(12)]
+    for t, (m, k, n) in enumerate(shapes):
+        a = _bm(bmm, oracle, m, k, 300 + t)
+        b = _bm(bmm, oracle, k, n, 400 + t)
+        for ring in (GF2, BOOL):
+            got = bmm.multiply_cubic(a, b, bmm.Semiring(ring), kernel=kernel)
+            want = oracle.multiply_cubic(a.words, b.words, m, k, n, ring)
+            assert np.array_equal(got.words, want), (m, k, n, ring)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_identity_all_ones_and_worked_example(engine, oracle, kernel):
+    bmm = engine
+    # 2x2 example (reference test_engine.cpp:114-131)
+    a2, b2 = bmm.BitMatrix.zeros(2, 2), bmm.BitMatrix.zeros(2, 2)
+    a2.set(0, 0, True); a2.set(0, 1, True); a2.set(1, 1, True)
+    b2.set(0, 0, True); b2.set(1, 0, True); b2.set(1, 1, True)
+    c = bmm.multiply_cubic(a2, b2, bmm.Semiring.Gf2XorAnd, kernel=kernel)
+    assert [c.get(0, 0), c.get(0, 1), c.get(1, 0), c.get(1, 1)] == [False, True, True, True]
+    c = bmm.multiply_cubic(a2, b2, bmm.Semiring.BooleanOrAnd, kernel=kernel)
+    assert all(c.get(i, j) for i in range(2) for j in range(2))
+    for ring in (bmm.Semiring.Gf2XorAnd, bmm.Semiring.BooleanOrAnd):
+        ident = bmm.BitMatrix.zeros(128, 128)
+        for i in range(128):
+            ident.set(i, i, True)
+        m = _bm(bmm, oracle, 128, 128, 21)
+        assert bmm.multiply_cubic(ident, m, ring, kernel=kernel) == m
+        assert bmm.multiply_cubic(m, ident, ring, kernel=kernel) == m
+    ones = bmm.BitMatrix(256, 256, np.full(256 * 4, ~np.uint64(0), dtype=np.uint64))
+    assert not bmm.multiply_cubic(ones, ones, bmm.Semiring.Gf2XorAnd, kernel=kernel).words.any()
+    assert np.all(bmm.multiply_cubic(ones, ones, bmm.Semiring.BooleanOrAnd, kernel=kernel).words == ~np.uint64(0))
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_accumulate_folds_partials(engine, oracle, kernel):
+    """K-split integration: C = A[:, :k1] B[:k1] (+) A[:, k1:] B[k1:] (XOR / OR)."""
+    bmm = engine
+    m, k, n, k1 = 256, 2048, 512, 1024
+    a = _bm(bmm, oracle, m, k, 71)
+    b = _bm(bmm, oracle, k, n, 72)
+    aw = a.words.reshape(m, k // 64)
+    for ring in (GF2, BOOL):
+        want = oracle.multiply_cubic(a.words, b.words, m, k, n, ring)
+        a1 = bmm.BitMatrix(m, k1, np.ascontiguousarray(aw[:, :k1 // 64]).ravel())
+        a2 = bmm.BitMatrix(m, k - k1, np.ascontiguousarray(aw[:, k1 // 64:]).ravel())
+        b1 = bmm.BitMatrix(k1, n, b.words[: k1 * n // 64].copy())
+        b2 = bmm.BitMatrix(k - k1, n, b.words[k1 * n // 64:].copy())
+        c = bmm.multiply_cubic(a1, b1, bmm.Semiring(ring), kernel=kernel)
+        bmm.multiply_cubic(a2, b2, bmm.Semiring(ring), kernel=kernel, out=c, accumulate=True)
+        assert np.array_equal(c.words, want)
+
+
+def test_device_api_panels(engine, oracle):
+    """bmmgpu_dev_transpose + bmmgpu_dev_cubic on torch-owned HBM buffers."""
+    import torch
+    bmm = engine
+    lib = bmm.lib()
+    for kernel in KERNELS:
+        gm, gn, gk = bmm.granularity(kernel)
+        m, k, n = 300, 3000, 700
+        a = oracle.random(m, k, 5)
+        b = oracle.random(k, n, 6)
+        m_pad, n_pad = -(-m // gm) * gm, -(-n // gn) * gn
+        kw = -(-k // gk) * gk // 64
+        dA = torch.zeros((m_pad, kw), dtype=torch.int64, device="cuda")
+        dA[:m, : (k + 63) // 64] = torch.from_numpy(a.view(np.int64).reshape(m, -1)).cuda()
+        dB = torch.from_numpy(b.view(np.int64)).cuda()
+        dBt = torch.empty((n_pad, kw), dtype=torch.int64, device="cuda")
+        dC = torch.empty((m_pad, n_pad // 64), dtype=torch.int64, device="cuda")
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        assert lib.bmmgpu_dev_transpose(dB.data_ptr(), (n + 63) // 64, k, n, dBt.data_ptr(), n_pad, kw, stream) == 0
+        for ring in (GF2, BOOL):
+            assert lib.bmmgpu_dev_cubic(dA.data_ptr(), kw, dBt.data_ptr(), kw, dC.data_ptr(), n_pad // 64, m_pad,
+                                        n_pad, kw, ring, kernel, 0, stream) == 0
+            torch.cuda.synchronize()
+            got = dC.cpu().numpy().view(np.uint64)[:m, : (n + 63) // 64].ravel()
+            assert np.array_equal(got, oracle.multiply_cubic(a, b, m, k, n, ring))
+
+
+def test_rejects_bad_panels(engine):
+    bmm = engine
+    lib = bmm.lib()
+    assert lib.bmmgpu_dev_cubic(None, 16, None, 16, None, 4, 65, 256, 16, 1, 1, 0, None) == 1
+    assert b"m_pad" in lib.bmmgpu_last_error()
