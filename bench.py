@@ -1,0 +1,447 @@
+#!/usr/bin/env python
+"""Benchmark: effective Pbop/s of the Boolean / GF(2) bit-matrix product on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--kernel auto|lop3|umma]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...   (one rank per GPU)
+    python bench.py --impl reference ...   (the reference's own CPU implementation, oracle/_ref)
+
+Default workload (BASELINE.json configs[2], the one quoted at 1/2/4/8 GPUs):
+Boolean product of A = BitMatrix::random(131072, 131072, 1) and
+B = random(131072, 131072, 2), cubic kernel.  The output rows are split into
+N contiguous slabs, one per rank, with no exchange (strong scaling: total
+work fixed).  One step = Bt = transpose(B) + the slab product, inputs resident
+in HBM; `e2e` repeats the step through the public C ABI (bmmgpu_cubic) from
+pinned host buffers, H2D/D2H inside the timed region.  Inputs (2 GiB per
+operand) are far larger than the 126 MB L2, so no explicit flush is needed.
+
+Metric convention (reference bmm_cli.cpp:134-141):
+effective bop/s = (2 m k n - m n) / T, reported in Pbop/s.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "effective Pbop/s (n^3 bops/s), Boolean & GF(2) products, 1/2/4/8 B200"
+UNIT = "Pbop/s"
+GF2, BOOL = 1, 0
+
+WORKLOADS = {
+    # name: (n, ring, algo, description)
+    "c3-bool-cubic-131072": (131072, BOOL, 0, "Boolean product n=131072 cubic (BASELINE configs[2])"),
+    "c3-gf2-cubic-131072": (131072, GF2, 0, "GF(2) product n=131072 cubic"),
+    "c1-gf2-cubic-8192": (8192, GF2, 0, "GF(2) product n=8192 cubic (BASELINE configs[0])"),
+    "c1-bool-cubic-8192": (8192, BOOL, 0, "Boolean product n=8192 cubic (BASELINE configs[0])"),
+    "c2-gf2-altsi-65536": (65536, GF2, 2, "GF(2) product n=65536 alternative-basis Strassen (BASELINE configs[1])"),
+}
+DEFAULT_WORKLOAD = "c3-bool-cubic-131072"
+# Paper V100 numbers for the same metric/config at 1 GPU, Pbop/s.
+PUBLISHED_1GPU = {"c3-bool-cubic-131072": 0.15127, "c3-gf2-cubic-131072": 0.17014, "c1-gf2-cubic-8192": 0.13283,
+                  "c1-bool-cubic-8192": 0.14000, "c2-gf2-altsi-65536": 0.30177}
+KERNEL_IDS = {"auto": 0, "lop3": 1, "umma": 2}
+
+
+def eff_bops(m: int, k: int, n: int) -> float:
+    return 2.0 * m * k * n - float(m) * n
+
+
+# ------------------------------------------------------------------ distributed plumbing
+class Dist:
+    def __init__(self) -> None:
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local_rank)
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+
+    def barrier(self) -> None:
+        if self.pg is not None:
+            import torch
+            if torch.cuda.is_available():
+                self.pg.barrier(device_ids=[self.local_rank])
+            else:
+                self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if self.pg is None:
+            return x
+        import torch
+        dev = f"cuda:{self.local_rank}" if torch.cuda.is_available() else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self) -> None:
+        if self.pg is not None:
+            self.pg.destroy_process_group()
+
+
+def shard_rows(n: int, rank: int, world: int, gran: int = 64) -> tuple[int, int]:
+    """Contiguous output-row slab of `rank`, aligned to `gran` rows (no exchange between slabs)."""
+    blocks = -(-n // gran)
+    lo = min(n, (blocks * rank // world) * gran)
+    hi = min(n, (blocks * (rank + 1) // world) * gran)
+    return lo, hi
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int) -> None:
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self) -> None:
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self) -> None:
+        assert self.proc is not None and self.proc.stdout is not None
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference CPU arm
+def reference_sample(n: int, ring: int, rows: int, cols: int, hB: np.ndarray | None):
+    """A bounded sample of the workload for the reference CPU implementation:
+    C[0:rows, 0:cols] = A[0:rows, :] . B[:, 0:cols] with the full K = n, through
+    the unmodified reference multiply_cubic (oracle/_ref) on all host cores."""
+    import paper_1909_01554_b200 as bmm
+    from oracle import Reference
+    ref = Reference()
+    a = np.zeros(rows * (n // 64), dtype=np.uint64)
+    bmm.random_rows_into(a, n, 1, 0, rows)
+    if hB is None:
+        hB = np.zeros(n * (n // 64), dtype=np.uint64)
+        bmm.random_rows_into(hB, n, 2, 0, n)
+    b = np.ascontiguousarray(hB.reshape(n, n // 64)[:, : cols // 64]).ravel()
+    workers = os.cpu_count() or 1
+
+    def step() -> float:
+        t0 = time.perf_counter()
+        ref.multiply_cubic(a, b, rows, n, cols, ring, workers)
+        return time.perf_counter() - t0
+
+    return step, eff_bops(rows, n, cols), workers
+
+
+def run_reference(args, dist: Dist) -> None:
+    n, ring, algo, desc = WORKLOADS[args.workload]
+    if dist.rank != 0:
+        return
+    rows, cols = (512, 8192) if n >= 16384 else (min(n, 1024), n)
+    if algo != 0:
+        # the reference alt-si path on a bounded sub-instance: n_s = 4096 full product, workers=1
+        # (more workers make the reference alt path slower)
+        import paper_1909_01554_b200 as bmm
+        from oracle import Reference
+        ref = Reference()
+        ns = 4096
+        a = np.zeros(ns * ns // 64, dtype=np.uint64)
+        b = np.zeros_like(a)
+        bmm.random_rows_into(a, ns, 1, 0, ns)
+        bmm.random_rows_into(b, ns, 2, 0, ns)
+
+        def step() -> float:
+            t0 = time.perf_counter()
+            ref.multiply(a, b, ns, 2, 0, 3, 3, 1, GF2)
+            return time.perf_counter() - t0
+        bops, workers, sample = eff_bops(ns, ns, ns), 1, f"alt-si full product n={ns}, auto plan, 1 worker"
+    else:
+        step, bops, workers = reference_sample(n, ring, rows, cols, None)
+        sample = f"C[0:{rows}, 0:{cols}] of the n={n} product (full K={n}), multiply_cubic, {workers} threads"
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    t = statistics.median(times)
+    value = bops / t / 1e15
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (BitMatrix::random seeds 1, 2)",
+            "config": {"workload": args.workload, "desc": desc, "n": n, "ring": "gf2" if ring else "boolean",
+                       "sample": sample},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, dist: Dist) -> None:
+    import torch
+    import paper_1909_01554_b200 as bmm
+
+    n, ring, algo, desc = WORKLOADS[args.workload]
+    kernel = KERNEL_IDS[args.kernel]
+    lib = bmm.lib()
+    dev = dist.local_rank
+    torch.cuda.set_device(dev)
+    gm, gn, gk = bmm.granularity(kernel)
+    w = n // 64
+    if algo == 0:
+        r0, r1 = shard_rows(n, dist.rank, dist.world, gm)
+    else:
+        if dist.world > 1:
+            raise SystemExit("the alt-basis workload runs on one GPU (BASELINE configs[1])")
+        r0, r1 = 0, n
+    m = r1 - r0
+    # pinned host inputs (the e2e leg copies from these every step)
+    hA = torch.empty(max(m, 1) * w, dtype=torch.int64, pin_memory=True)
+    hB = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
+    hC = torch.empty(max(m, 1) * w, dtype=torch.int64, pin_memory=True)
+    hA_np, hB_np = hA.numpy().view(np.uint64), hB.numpy().view(np.uint64)
+    bmm.random_rows_into(hA_np, n, 1, r0, r1)
+    bmm.random_rows_into(hB_np, n, 2, 0, n)
+
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    m_pad = -(-m // gm) * gm
+    n_pad = -(-n // 256) * 256
+    kw = -(-w // (gk // 64)) * (gk // 64)
+    dA = torch.zeros((m_pad, kw), dtype=torch.int64, device="cuda")
+    dA[:m, :w].copy_(hA[: m * w].view(m, w), non_blocking=True)
+    dB = hB.to("cuda", non_blocking=True)
+    dBt = torch.empty((n_pad, kw), dtype=torch.int64, device="cuda")
+    dC = torch.empty((m_pad, n_pad // 64), dtype=torch.int64, device="cuda")
+    if algo != 0:
+        dA0 = dA.clone()
+    torch.cuda.synchronize()
+
+    kt0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + args.warmup)]
+    kt1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + args.warmup)]
+
+    def check(rc: int) -> None:
+        if rc != 0:
+            raise RuntimeError(lib.bmmgpu_last_error().decode())
+
+    launches_per_step = 0
+
+    def step(i: int) -> None:
+        nonlocal launches_per_step
+        before = lib.bmmgpu_last_launch_count()
+        check(lib.bmmgpu_dev_transpose(dB.data_ptr(), w, n, n, dBt.data_ptr(), n_pad, kw, sp))
+        if algo == 0:
+            kt0[i].record(stream)
+            check(lib.bmmgpu_dev_cubic(dA.data_ptr(), kw, dBt.data_ptr(), kw, dC.data_ptr(), n_pad // 64, m_pad,
+                                       n_pad, kw, ring, kernel, 0, sp))
+            kt1[i].record(stream)
+        else:
+            dA.copy_(dA0)  # the fast path basis-changes its operands in place
+            kt0[i].record(stream)
+            check(lib.bmmgpu_dev_multiply(dA.data_ptr(), kw, dBt.data_ptr(), kw, dC.data_ptr(), n_pad // 64, n,
+                                          algo, args.leaf_log2, kernel, sp))
+            kt1[i].record(stream)
+        launches_per_step = lib.bmmgpu_last_launch_count() - before
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    visible = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip().isdigit()]
+    sampler = ClockSampler(int(visible[dev]) if dev < len(visible) else dev)
+    sampler.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = sampler.stop()
+    local_ms = t0.elapsed_time(t1) / args.steps
+    ms = dist.max(local_ms)
+    kms = statistics.mean(kt0[args.warmup + i].elapsed_time(kt1[args.warmup + i]) for i in range(args.steps))
+    total_bops = eff_bops(n, n, n)
+    value = total_bops / (ms * 1e-3) / 1e15
+
+    # ---- end to end through the public C ABI, host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e and algo == 0:
+        class Opts(ctypes.Structure):
+            _fields_ = [("device_mask", ctypes.c_uint32), ("kernel", ctypes.c_int32),
+                        ("accumulate", ctypes.c_int32), ("leaf_log2", ctypes.c_int32),
+                        ("timing_ms", ctypes.POINTER(ctypes.c_double))]
+        opts = Opts(1 << dev, kernel, 0, 0, ctypes.POINTER(ctypes.c_double)())
+        lib.bmmgpu_cubic.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                     ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32, ctypes.POINTER(Opts)]
+
+        def e2e_step() -> None:
+            check(lib.bmmgpu_cubic(hA.data_ptr(), hB.data_ptr(), hC.data_ptr(), m, n, n, ring, ctypes.byref(opts)))
+
+        e2e_step()
+        dist.barrier()
+        te = []
+        for _ in range(max(1, min(args.steps, args.e2e_steps))):
+            dist.barrier()
+            s0 = time.perf_counter()
+            e2e_step()
+            te.append(time.perf_counter() - s0)
+        e2e_t = dist.max(statistics.median(te))
+        e2e = {"value": total_bops / e2e_t / 1e15, "unit": UNIT, "ms_per_step": e2e_t * 1e3,
+               "h2d_bytes_per_step": int(m * w * 8 + n * w * 8), "d2h_bytes_per_step": int(m * w * 8),
+               "path": "bmmgpu_cubic (include/bmmgpu.h) from pinned host buffers, per rank"}
+    elif not args.no_e2e:
+        import paper_1909_01554_b200 as bmm2
+        a = bmm2.BitMatrix(n, n, hA_np[: n * w])
+        b = bmm2.BitMatrix(n, n, hB_np)
+        out = bmm2.BitMatrix(n, n, hC.numpy().view(np.uint64)[: n * w])
+        plan = bmm2.LayerPlan.auto_plan(n, 1)
+        bmm2.multiply(a, b, bmm2.Algo(algo), plan, bmm2.Semiring(ring), kernel=kernel, leaf_log2=args.leaf_log2)
+        te = []
+        for _ in range(max(1, min(args.steps, args.e2e_steps))):
+            s0 = time.perf_counter()
+            res = bmm2.multiply(a, b, bmm2.Algo(algo), plan, bmm2.Semiring(ring), kernel=kernel,
+                                leaf_log2=args.leaf_log2)
+            te.append(time.perf_counter() - s0)
+        del out, res
+        e2e_t = statistics.median(te)
+        e2e = {"value": total_bops / e2e_t / 1e15, "unit": UNIT, "ms_per_step": e2e_t * 1e3,
+               "h2d_bytes_per_step": int(2 * n * w * 8), "d2h_bytes_per_step": int(n * w * 8),
+               "path": "bmmgpu_multiply (include/bmmgpu.h) from host buffers"}
+
+    # ---- roofline of the dominant kernel
+    peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())
+    resolved = kernel if kernel else 1
+    peak = peaks["lop3_bops"] if resolved == 1 else peaks["umma_mxf4_bops"]
+    launch_bops = eff_bops(m_pad, n_pad, n) if algo == 0 else eff_bops(n, n, n)
+    achieved = launch_bops / (kms * 1e-3)
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(f"{args.workload}:{args.kernel}")
+    roofline = {"bound": "alu" if resolved == 1 else "tensor", "achieved": achieved / 1e12,
+                "peak": peak / 1e12, "unit": "Tbop/s", "frac": achieved / peak, "traffic": traffic,
+                "kernel": "cubic_lop3_kernel" if resolved == 1 else "cubic_umma_kernel",
+                "kernel_ms": kms, "peak_source": "profiles/peaks.json (measured issue rate, microbench/ubench.cu)"}
+
+    # ---- CPU baseline: the reference on this box's host cores, rank 0 at N=1
+    cpu = None
+    if dist.world == 1 and not args.no_cpu_baseline:
+        if algo == 0:
+            rows, cols = (512, 8192) if n >= 16384 else (min(n, 1024), n)
+            stepf, sb, workers = reference_sample(n, ring, rows, cols, hB_np)
+            sample = f"C[0:{rows}, 0:{cols}] of the n={n} product (full K={n}), reference multiply_cubic"
+        else:
+            from oracle import Reference
+            ref = Reference()
+            ns = 4096
+            a4 = np.zeros(ns * ns // 64, dtype=np.uint64)
+            b4 = np.zeros_like(a4)
+            bmm.random_rows_into(a4, ns, 1, 0, ns)
+            bmm.random_rows_into(b4, ns, 2, 0, ns)
+
+            def stepf() -> float:
+                s0 = time.perf_counter()
+                ref.multiply(a4, b4, ns, 2, 0, 3, 3, 1, GF2)
+                return time.perf_counter() - s0
+            sb, workers, sample = eff_bops(ns, ns, ns), 1, f"reference alt-si n={ns}, auto plan, 1 worker"
+        ts = [stepf() for _ in range(args.cpu_reps)]
+        cpu = {"value": sb / statistics.median(ts) / 1e15, "unit": UNIT, "cores": workers, "kind": "reference",
+               "sample": sample, "seconds": sum(ts)}
+
+    if dist.rank == 0:
+        published = PUBLISHED_1GPU.get(args.workload) if dist.world == 1 else None
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": (value / published) if published else None,
+                "dtype": "u32" if resolved == 1 else "e2m1",
+                "data": "synthetic (BitMatrix::random seeds 1, 2, mt19937_64)",
+                "config": {"workload": args.workload, "desc": desc, "n": n, "ring": "gf2" if ring else "boolean",
+                           "algo": ["cubic", "sw", "alt-si", "alt-chain"][algo], "kernel": args.kernel,
+                           "rows_per_rank": m, "l2": "inputs (n^2/8 B per operand) far exceed the 126 MB L2",
+                           "parallelism": f"output row slabs x{dist.world}, no exchange"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "gpu_launches": int(launches_per_step * args.steps)}
+        print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
+    ap.add_argument("--kernel", choices=sorted(KERNEL_IDS), default="auto")
+    ap.add_argument("--leaf-log2", dest="leaf_log2", type=int, default=0)
+    ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=3)
+    ap.add_argument("--cpu-reps", dest="cpu_reps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -110,6 +110,14 @@ int bmmgpu_dev_cubic(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint
                      uint64_t m_pad, uint64_t n_pad, uint64_t kw, int32_t semiring, int32_t kernel,
                      int32_t accumulate, void* stream);
 
+/* Fast GF(2) product on device, n = 64 * 2^depth: dA (n x n/64 words, stride
+ * lda), dBt = Bt of B (n x n/64, stride ldbt; rows padded to 256 in memory),
+ * dC (n x n/64, stride ldc).  dA and dBt are overwritten (basis-changed in
+ * place).  leaf_log2 as in bmmgpu_opts.  Synchronises the stream between
+ * recursion levels (it frees level buffers as it goes). */
+int bmmgpu_dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
+                        uint64_t n, int32_t algo, int32_t leaf_log2, int32_t kernel, void* stream);
+
 /* Number of kernel launches the last host-API call made on its devices. */
 uint64_t bmmgpu_last_launch_count(void);
 

@@ -86,12 +86,13 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_dev_granularity.argtypes = [i32, _u64p, _u64p, _u64p]
         L.bmmgpu_dev_transpose.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp]
         L.bmmgpu_dev_cubic.argtypes = [vp, u64, vp, u64, vp, u64, u64, u64, u64, i32, i32, i32, vp]
+        L.bmmgpu_dev_multiply.argtypes = [vp, u64, vp, u64, vp, u64, u64, i32, i32, i32, vp]
         L.bmmgpu_last_launch_count.restype = u64
         L.bmmgpu_device_count.restype = ctypes.c_int
         L.bmmgpu_last_error.restype = ctypes.c_char_p
         L.bmmgpu_version.restype = ctypes.c_char_p
         for name in ("bmmgpu_cubic", "bmmgpu_multiply", "bmmgpu_basis_change", "bmmgpu_dev_granularity",
-                     "bmmgpu_dev_transpose", "bmmgpu_dev_cubic"):
+                     "bmmgpu_dev_transpose", "bmmgpu_dev_cubic", "bmmgpu_dev_multiply"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -199,8 +200,18 @@ def _host() -> ctypes.CDLL:
         L = ctypes.CDLL(str(HOST_LIB_PATH))
         L.bmmh_random.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p]
         L.bmmh_random.restype = None
+        L.bmmh_random_rows.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                       ctypes.c_void_p]
+        L.bmmh_random_rows.restype = None
         _host_lib = L
     return _host_lib
+
+
+def random_rows_into(out: np.ndarray, cols: int, seed: int, row_begin: int, row_end: int) -> None:
+    """Rows [row_begin, row_end) of BitMatrix.random(*, cols, seed) into `out`
+    (any C-contiguous 8-byte buffer, e.g. pinned host memory)."""
+    if row_end > row_begin:
+        _host().bmmh_random_rows(cols, seed, row_begin, row_end, out.ctypes.data)
 
 
 def _opts(kernel: int, leaf_log2: int = 0, timing: ctypes.c_double | None = None, device_mask: int = 0,

@@ -351,17 +351,24 @@ int alt_multiply_device(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt
     return launch_basis_change(dC, ldc, n, e, make_steps(sc->chi, sc->n_chi, false), s);
 }
 
-// Host entry: reference-layout host buffers in, C out.
-int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, const bmmgpu_plan* plan,
-                      int kernel, int leaf_log2, double* timing_ms) {
-    (void)plan;  // the plan's host/serial/parallel split is a CPU schedule; the GPU picks e from leaf_log2
+// Recursion levels run as passes: the leaf dimension is 2^leaf_log2
+// (default 2^12: the block-product kernels reach full speed at K >= 4096).
+int alt_levels(uint64_t n, int leaf_log2) {
     int depth = 0;
     while ((64ull << depth) < n) ++depth;
-    int leaf = leaf_log2 > 0 ? leaf_log2 : 12;  // 4096-bit leaves by default
+    int leaf = leaf_log2 > 0 ? leaf_log2 : 12;
     if (leaf < 6) leaf = 6;
     int e = depth + 6 - leaf;
     if (e < 0) e = 0;
     if (e > depth) e = depth;
+    return e;
+}
+
+// Host entry: reference-layout host buffers in, C out.
+int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, const bmmgpu_plan* plan,
+                      int kernel, int leaf_log2, double* timing_ms) {
+    (void)plan;  // the plan's host/serial/parallel split is a CPU schedule; the GPU picks e from leaf_log2
+    const int e = alt_levels(n, leaf_log2);
     kernel = resolve_kernel(kernel);
     const uint64_t w = n / 64;
     cudaStream_t s;
@@ -409,6 +416,22 @@ int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_
     cudaEventDestroy(e1);
     if (timing_ms) *timing_ms = ms;
     return kOk;
+}
+
+int dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc, uint64_t n,
+                 int algo, int leaf_log2, int kernel, cudaStream_t s) {
+    if (n < 64 || (n & (n - 1))) {
+        set_error("fast algorithms need n = 64 * 2^k");
+        return kEshape;
+    }
+    if (!scheme_for(algo)) {
+        set_error("no bilinear scheme for this algorithm");
+        return kEinval;
+    }
+    kernel = resolve_kernel(kernel);
+    const int e = alt_levels(n, leaf_log2);
+    if (e == 0) return launch_cubic(kernel, dA, lda, dBt, ldbt, dC, ldc, n, n, n / 64, true, false, s, 1, 0, 0, 0);
+    return alt_multiply_device(dA, lda, dBt, ldbt, dC, ldc, n, algo, e, kernel, s);
 }
 
 // ------------------------------------------------ interleaved basis change (K4)
@@ -465,6 +488,13 @@ int interleaved_basis_change(uint64_t* words, uint64_t total_words, int levels, 
 }
 
 }  // namespace bmmgpu
+
+extern "C" int bmmgpu_dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
+                                   uint64_t ldc, uint64_t n, int32_t algo, int32_t leaf_log2, int32_t kernel,
+                                   void* stream) {
+    return bmmgpu::dev_multiply(dA, lda, dBt, ldbt, dC, ldc, n, algo, leaf_log2, kernel,
+                                static_cast<cudaStream_t>(stream));
+}
 
 extern "C" int bmmgpu_basis_change(uint64_t* words, uint64_t total_words, int32_t levels, int32_t algo,
                                    int32_t factor, int32_t inverse) {
