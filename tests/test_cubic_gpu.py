@@ -10,7 +10,7 @@ import pytest
 GF2, BOOL = 1, 0
 pytestmark = pytest.mark.gpu
 
-KERNELS = [1]  # LOP3; the tcgen05 kernel joins via test_umma_gpu.py
+KERNELS = [1, 2]  # LOP3 (integer ALU), tcgen05 kind::mxf4 (tensor core)
 
 
 def _bm(bmm, oracle, rows, cols, seed):
