@@ -51,7 +51,7 @@ DEFAULT_WORKLOAD = "c3-bool-cubic-131072"
 # Paper V100 numbers for the same metric/config at 1 GPU, Pbop/s.
 PUBLISHED_1GPU = {"c3-bool-cubic-131072": 0.15127, "c3-gf2-cubic-131072": 0.17014, "c1-gf2-cubic-8192": 0.13283,
                   "c1-bool-cubic-8192": 0.14000, "c2-gf2-altsi-65536": 0.30177}
-KERNEL_IDS = {"auto": 0, "lop3": 1, "umma": 2}
+KERNEL_IDS = {"auto": 0, "lop3": 1, "umma": 2, "umma1": 3}
 
 
 def eff_bops(m: int, k: int, n: int) -> float:

@@ -43,7 +43,8 @@ extern "C" {
 /* block-product kernel selection */
 #define BMMGPU_KERNEL_AUTO 0
 #define BMMGPU_KERNEL_LOP3 1      /* LOP3 AND/XOR|OR word kernel (integer ALU)      */
-#define BMMGPU_KERNEL_UMMA_F4 2   /* tcgen05 kind::mxf4 0/1 e2m1, f32 accumulate    */
+#define BMMGPU_KERNEL_UMMA_F4 2   /* tcgen05 kind::mxf4 0/1 e2m1, f32 accumulate, CTA pair */
+#define BMMGPU_KERNEL_UMMA_F4_1SM 3 /* the same on single CTAs (cta_group::1)          */
 
 typedef struct bmmgpu_opts {
     uint32_t device_mask; /* bit g = use CUDA device g; 0 = device 0            */

@@ -55,6 +55,7 @@ class Kernel(enum.IntEnum):
     AUTO = 0
     LOP3 = 1
     UMMA_F4 = 2
+    UMMA_F4_1SM = 3
 
 
 class _Opts(ctypes.Structure):

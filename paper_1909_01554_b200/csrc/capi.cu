@@ -30,6 +30,10 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
                       uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate, cudaStream_t stream,
                       uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
 void umma_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
+int launch_cubic_umma1(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
+                       uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate, cudaStream_t stream,
+                       uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
+void umma1_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
 int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, const bmmgpu_plan* plan,
                       int kernel, int leaf_log2, double* timing_ms);
 
@@ -52,6 +56,7 @@ int granularity(int kernel, uint64_t* gm, uint64_t* gn, uint64_t* gk) {
     switch (resolve_kernel(kernel)) {
         case BMMGPU_KERNEL_LOP3: lop3_granularity(gm, gn, gk); return kOk;
         case BMMGPU_KERNEL_UMMA_F4: umma_granularity(gm, gn, gk); return kOk;
+        case BMMGPU_KERNEL_UMMA_F4_1SM: umma1_granularity(gm, gn, gk); return kOk;
         default: set_error("unknown kernel id " + std::to_string(kernel)); return kEinval;
     }
 }
@@ -66,6 +71,9 @@ int launch_cubic(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* d
         case BMMGPU_KERNEL_UMMA_F4:
             return launch_cubic_umma(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream, batch,
                                      sA_batch, sB_batch, sC_batch);
+        case BMMGPU_KERNEL_UMMA_F4_1SM:
+            return launch_cubic_umma1(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream, batch,
+                                      sA_batch, sB_batch, sC_batch);
         default: set_error("unknown kernel id " + std::to_string(kernel)); return kEinval;
     }
 }

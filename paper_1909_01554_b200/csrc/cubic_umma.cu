@@ -1,5 +1,7 @@
-// cubic_umma.cu -- K2: the cubic bit-matrix product on the 5th-generation
-// tensor cores (tcgen05.mma kind::mxf4, f32 accumulators in TMEM).
+// cubic_umma.cu -- K2 (single-CTA form, kernel id BMMGPU_KERNEL_UMMA_F4_1SM): the
+// cubic bit-matrix product on the 5th-generation tensor cores (tcgen05.mma
+// kind::mxf4, f32 accumulators in TMEM).  The CTA-pair form in
+// cubic_umma2.cu is the default; this one stays as the simpler reference.
 //
 // Same contract as cubic_lop3.cu (reference kernel64 + cubic_blocked,
 // engine.cpp:34-100): C bit (i,j) = parity (GF(2)) or any (Boolean) of the
@@ -225,13 +227,13 @@ __global__ void __launch_bounds__(U_THREADS, 1)
 
 }  // namespace
 
-void umma_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits) {
+void umma1_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits) {
     *gm = U_BM;
     *gn = U_BN;
     *gk_bits = U_KBITS;
 }
 
-int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
+int launch_cubic_umma1(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
                       uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate, cudaStream_t stream,
                       uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch) {
     if (m_pad % U_BM || n_pad % U_BN || (kw * 64) % U_KBITS || lda % 2 || ldbt % 2 || ldc % 4) {

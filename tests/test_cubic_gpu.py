@@ -10,7 +10,7 @@ import pytest
 GF2, BOOL = 1, 0
 pytestmark = pytest.mark.gpu
 
-KERNELS = [1, 2]  # LOP3 (integer ALU), tcgen05 kind::mxf4 (tensor core)
+KERNELS = [1, 2, 3]  # LOP3 (integer ALU); tcgen05 kind::mxf4 CTA pair; tcgen05 kind::mxf4 single CTA
 
 
 def _bm(bmm, oracle, rows, cols, seed):
