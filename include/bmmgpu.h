@@ -45,6 +45,7 @@ extern "C" {
 #define BMMGPU_KERNEL_LOP3 1      /* LOP3 AND/XOR|OR word kernel (integer ALU)      */
 #define BMMGPU_KERNEL_UMMA_F4 2   /* tcgen05 kind::mxf4 0/1 e2m1, f32 accumulate, CTA pair */
 #define BMMGPU_KERNEL_UMMA_F4_1SM 3 /* the same on single CTAs (cta_group::1)          */
+#define BMMGPU_KERNEL_UMMA_F4_PAIR_NP 4 /* CTA pair, one launch CTA per tile (no persistent loop) */
 
 typedef struct bmmgpu_opts {
     uint32_t device_mask; /* bit g = use CUDA device g; 0 = device 0            */

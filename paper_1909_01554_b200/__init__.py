@@ -56,6 +56,7 @@ class Kernel(enum.IntEnum):
     LOP3 = 1
     UMMA_F4 = 2
     UMMA_F4_1SM = 3
+    UMMA_F4_PAIR_NP = 4
 
 
 class _Opts(ctypes.Structure):

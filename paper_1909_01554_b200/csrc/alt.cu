@@ -183,37 +183,7 @@ int launch_basis_change(uint64_t* M, uint64_t ld, uint64_t n, int levels, const 
     return kOk;
 }
 
-struct DevMem {
-    void* p = nullptr;
-    DevMem() = default;
-    DevMem(const DevMem&) = delete;
-    DevMem& operator=(const DevMem&) = delete;
-    DevMem(DevMem&& o) noexcept : p(o.p) { o.p = nullptr; }
-    DevMem& operator=(DevMem&& o) noexcept {
-        if (this != &o) {
-            release();
-            p = o.p;
-            o.p = nullptr;
-        }
-        return *this;
-    }
-    ~DevMem() { release(); }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-    }
-    int alloc(size_t bytes) {
-        release();
-        cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
-        if (e != cudaSuccess) {
-            set_error("cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
-            p = nullptr;
-            return kEcuda;
-        }
-        return kOk;
-    }
-    uint64_t* u() const { return static_cast<uint64_t*>(p); }
-};
+using DevMem = DeviceBuffer;  // stream-ordered, pool-cached (common.cuh)
 
 }  // namespace
 
@@ -279,7 +249,7 @@ int alt_multiply_device(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt
         const uint64_t Ll = n >> l;
         const uint64_t Pn = P * 7;
         const size_t tb = size_t(Pn * t_bs[l + 1] * 8), sb = size_t(Pn * s_bs[l + 1] * 8);
-        if ((st = T[l + 1].alloc(tb)) || (st = S[l + 1].alloc(sb))) return st;
+        if ((st = T[l + 1].alloc(tb, s)) || (st = S[l + 1].alloc(sb, s))) return st;
         if (l + 1 == e && (t_rows != L || s_rows != L || kwl != L / 64)) {
             BMMGPU_CUDA_TRY(cudaMemsetAsync(T[l + 1].p, 0, tb, s));
             BMMGPU_CUDA_TRY(cudaMemsetAsync(S[l + 1].p, 0, sb, s));
@@ -293,8 +263,7 @@ int alt_multiply_device(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt
         count_launch(2);
         BMMGPU_CUDA_TRY(cudaGetLastError());
         if (l > 0) {
-            // parents no longer needed
-            BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
+            // parents no longer needed (stream-ordered free: no host sync)
             T[l].release();
             S[l].release();
         }
@@ -306,7 +275,7 @@ int alt_multiply_device(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt
     // Leaves: 7^e batched block products, Q row-major (t_rows x cwl words each).
     DevMem Q;
     const uint64_t q_bs = t_rows * cwl;
-    if ((st = Q.alloc(size_t(batch * q_bs * 8)))) return st;
+    if ((st = Q.alloc(size_t(batch * q_bs * 8), s))) return st;
     for (uint64_t b0 = 0; b0 < batch; b0 += 65535) {
         const uint64_t nb = std::min<uint64_t>(65535, batch - b0);
         if ((st = launch_cubic(kernel, T[e].u() + b0 * t_bs[e], kwl, S[e].u() + b0 * s_bs[e], kwl,
@@ -314,7 +283,6 @@ int alt_multiply_device(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt
                                q_bs)))
             return st;
     }
-    BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
     T[e].release();
     S[e].release();
 
@@ -334,14 +302,13 @@ int alt_multiply_device(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt
         } else {
             out_ld = Ll / 64;
             out_bs = Ll * (Ll / 64);
-            if ((st = nxt.alloc(size_t(Pp * out_bs * 8)))) return st;
+            if ((st = nxt.alloc(size_t(Pp * out_bs * 8), s))) return st;
             out = nxt.u();
         }
         const uint64_t total = Pp * (Ll / 2) * (Ll / 128);
         compress_kernel<<<grid_for(total), 256, 0, s>>>(cur.u(), cur_ld, cur_bs, Pp, Ll, out, out_ld, out_bs, mg);
         count_launch();
         BMMGPU_CUDA_TRY(cudaGetLastError());
-        BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
         cur = std::move(nxt);
         cur_ld = out_ld;
         cur_bs = out_bs;
@@ -386,9 +353,8 @@ int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_
     const uint64_t rows_b = e == 0 ? round_up(n, gn) : n;
     const uint64_t kw = e == 0 ? round_up(w, gk / 64) : w;
     const uint64_t cw = e == 0 ? rows_b / 64 : w;
-    if ((st = dA.alloc(rows_a * kw * 8)) || (st = dB.alloc(n * w * 8)) ||
-        (st = dBt.alloc(round_up(rows_b, 256) * kw * 8)) ||
-        (st = dC.alloc(rows_a * cw * 8)))
+    if ((st = dA.alloc(rows_a * kw * 8, s)) || (st = dB.alloc(n * w * 8, s)) ||
+        (st = dBt.alloc(round_up(rows_b, 256) * kw * 8, s)) || (st = dC.alloc(rows_a * cw * 8, s)))
         return st;
     if (e == 0) {
         BMMGPU_CUDA_TRY(cudaMemsetAsync(dA.p, 0, rows_a * kw * 8, s));
@@ -473,7 +439,7 @@ int interleaved_basis_change(uint64_t* words, uint64_t total_words, int levels, 
     }
     DevMem d;
     int rc;
-    if ((rc = d.alloc(total_words * 8))) return rc;
+    if ((rc = d.alloc(total_words * 8, nullptr))) return rc;
     BMMGPU_CUDA_TRY(cudaMemcpy(d.p, words, total_words * 8, cudaMemcpyHostToDevice));
     uint64_t outer = 1;
     for (int l = 0; l < levels; ++l) {

@@ -34,6 +34,10 @@ int launch_cubic_umma1(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, ui
                        uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate, cudaStream_t stream,
                        uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
 void umma1_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
+int launch_cubic_umma2np(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
+                         uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate,
+                         cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
+void umma2np_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
 int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, const bmmgpu_plan* plan,
                       int kernel, int leaf_log2, double* timing_ms);
 
@@ -43,6 +47,21 @@ std::atomic<uint64_t> g_launches{0};
 }  // namespace
 
 void set_error(const std::string& msg) { g_error = msg; }
+
+void enable_pool_caching() {
+    static std::mutex mu;
+    static uint32_t done_mask = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32) return;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done_mask & (1u << dev)) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t threshold = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+    done_mask |= 1u << dev;
+}
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int resolve_kernel(int kernel) {
@@ -57,6 +76,7 @@ int granularity(int kernel, uint64_t* gm, uint64_t* gn, uint64_t* gk) {
         case BMMGPU_KERNEL_LOP3: lop3_granularity(gm, gn, gk); return kOk;
         case BMMGPU_KERNEL_UMMA_F4: umma_granularity(gm, gn, gk); return kOk;
         case BMMGPU_KERNEL_UMMA_F4_1SM: umma1_granularity(gm, gn, gk); return kOk;
+        case BMMGPU_KERNEL_UMMA_F4_PAIR_NP: umma2np_granularity(gm, gn, gk); return kOk;
         default: set_error("unknown kernel id " + std::to_string(kernel)); return kEinval;
     }
 }
@@ -74,30 +94,14 @@ int launch_cubic(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* d
         case BMMGPU_KERNEL_UMMA_F4_1SM:
             return launch_cubic_umma1(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream, batch,
                                       sA_batch, sB_batch, sC_batch);
+        case BMMGPU_KERNEL_UMMA_F4_PAIR_NP:
+            return launch_cubic_umma2np(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream,
+                                        batch, sA_batch, sB_batch, sC_batch);
         default: set_error("unknown kernel id " + std::to_string(kernel)); return kEinval;
     }
 }
 
 namespace {
-
-// RAII device buffer.
-struct DevBuf {
-    void* p = nullptr;
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
-    int alloc(size_t bytes) {
-        if (bytes == 0) bytes = 16;
-        cudaError_t e = cudaMalloc(&p, bytes);
-        if (e != cudaSuccess) {
-            set_error("cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
-            p = nullptr;
-            return kEcuda;
-        }
-        return kOk;
-    }
-    uint64_t* u64() const { return static_cast<uint64_t*>(p); }
-};
 
 struct SlabJob {
     int device;
@@ -126,8 +130,9 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
         cudaStream_t s;
         ~StreamGuard() { cudaStreamDestroy(s); }
     } sg{s};
-    DevBuf dA, dB, dBt, dC;
-    if ((st = dA.alloc(m_pad * kw * 8)) || (st = dBt.alloc(n_pad * kw * 8)) || (st = dC.alloc(m_pad * cw * 8)))
+    DeviceBuffer dA, dB, dBt, dC;
+    if ((st = dA.alloc(m_pad * kw * 8, s)) || (st = dBt.alloc(n_pad * kw * 8, s)) ||
+        (st = dC.alloc(m_pad * cw * 8, s)))
         return st;
     // A slab into the zero-padded panel (pad columns / rows stay zero).
     BMMGPU_CUDA_TRY(cudaMemsetAsync(dA.p, 0, m_pad * kw * 8, s));
@@ -137,9 +142,9 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
                                           cudaMemcpyHostToDevice, s));
     // B, then Bt on device.
     if (k > 0 && nb > 0) {
-        if ((st = dB.alloc(k * nb * 8))) return st;
+        if ((st = dB.alloc(k * nb * 8, s))) return st;
         BMMGPU_CUDA_TRY(cudaMemcpyAsync(dB.p, B, k * nb * 8, cudaMemcpyHostToDevice, s));
-        if ((st = launch_transpose(dB.u64(), nb, k, n, dBt.u64(), n_pad, kw, s))) return st;
+        if ((st = launch_transpose(dB.u(), nb, k, n, dBt.u(), n_pad, kw, s))) return st;
     } else {
         BMMGPU_CUDA_TRY(cudaMemsetAsync(dBt.p, 0, n_pad * kw * 8, s));
         count_launch();
@@ -154,7 +159,7 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
     BMMGPU_CUDA_TRY(cudaEventCreate(&e0));
     BMMGPU_CUDA_TRY(cudaEventCreate(&e1));
     BMMGPU_CUDA_TRY(cudaEventRecord(e0, s));
-    st = launch_cubic(kernel, dA.u64(), kw, dBt.u64(), kw, dC.u64(), cw, m_pad, n_pad, kw, gf2, accumulate, s, 1, 0, 0,
+    st = launch_cubic(kernel, dA.u(), kw, dBt.u(), kw, dC.u(), cw, m_pad, n_pad, kw, gf2, accumulate, s, 1, 0, 0,
                       0);
     if (st) {
         cudaEventDestroy(e0);

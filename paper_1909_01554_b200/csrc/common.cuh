@@ -21,6 +21,49 @@ void count_launch(uint64_t n = 1);
         }                                                                                         \
     } while (0)
 
+// Stream-ordered device buffer from the device's default memory pool.  The
+// pool keeps freed memory (release threshold = max), so the multi-GB level
+// buffers of repeated calls are recycled instead of re-mapped, and freeing a
+// level's buffer needs no stream synchronisation.
+void enable_pool_caching();
+
+struct DeviceBuffer {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    DeviceBuffer() = default;
+    explicit DeviceBuffer(cudaStream_t stream) : s(stream) {}
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    DeviceBuffer(DeviceBuffer&& o) noexcept : p(o.p), s(o.s) { o.p = nullptr; }
+    DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            s = o.s;
+            o.p = nullptr;
+        }
+        return *this;
+    }
+    ~DeviceBuffer() { release(); }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+    }
+    int alloc(size_t bytes, cudaStream_t stream) {
+        release();
+        s = stream;
+        enable_pool_caching();
+        cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, s);
+        if (e != cudaSuccess) {
+            set_error("cudaMallocAsync(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+            p = nullptr;
+            return kEcuda;
+        }
+        return kOk;
+    }
+    uint64_t* u() const { return static_cast<uint64_t*>(p); }
+};
+
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline uint64_t round_up(uint64_t a, uint64_t b) { return ceil_div(a, b) * b; }
 

@@ -10,7 +10,8 @@ import pytest
 GF2, BOOL = 1, 0
 pytestmark = pytest.mark.gpu
 
-KERNELS = [1, 2, 3]  # LOP3 (integer ALU); tcgen05 kind::mxf4 CTA pair; tcgen05 kind::mxf4 single CTA
+# LOP3 (integer ALU); tcgen05 kind::mxf4 CTA pair (persistent); single CTA; CTA pair, one tile per launch CTA
+KERNELS = [1, 2, 3, 4]
 
 
 def _bm(bmm, oracle, rows, cols, seed):
