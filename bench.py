@@ -97,11 +97,11 @@ class Dist:
 
 
 def shard_rows(n: int, rank: int, world: int, gran: int = 64) -> tuple[int, int]:
-    """Contiguous output-row slab of `rank`, aligned to `gran` rows (no exchange between slabs)."""
-    blocks = -(-n // gran)
-    lo = min(n, (blocks * rank // world) * gran)
-    hi = min(n, (blocks * (rank + 1) // world) * gran)
-    return lo, hi
+    """Contiguous output-row slab of `rank`, aligned to `gran` rows (no exchange
+    between slabs): the C ABI's bmmgpu_slab_rows, the same rule bmmgpu_cubic
+    applies across devices."""
+    import paper_1909_01554_b200 as bmm
+    return bmm.slab_rows(n, world, rank, gran)
 
 
 # ------------------------------------------------------------------ clocks
@@ -350,18 +350,18 @@ def run_ours(args, dist: Dist) -> None:
         b = bmm2.BitMatrix(n, n, hB_np)
         out = bmm2.BitMatrix(n, n, hC.numpy().view(np.uint64)[: n * w])
         plan = bmm2.LayerPlan.auto_plan(n, 1)
-        bmm2.multiply(a, b, bmm2.Algo(algo), plan, bmm2.Semiring(ring), kernel=kernel, leaf_log2=args.leaf_log2)
+        bmm2.multiply(a, b, bmm2.Algo(algo), plan, bmm2.Semiring(ring), kernel=kernel, leaf_log2=args.leaf_log2,
+                      out=out)
         te = []
         for _ in range(max(1, min(args.steps, args.e2e_steps))):
             s0 = time.perf_counter()
-            res = bmm2.multiply(a, b, bmm2.Algo(algo), plan, bmm2.Semiring(ring), kernel=kernel,
-                                leaf_log2=args.leaf_log2)
+            bmm2.multiply(a, b, bmm2.Algo(algo), plan, bmm2.Semiring(ring), kernel=kernel,
+                          leaf_log2=args.leaf_log2, out=out)
             te.append(time.perf_counter() - s0)
-        del out, res
         e2e_t = statistics.median(te)
         e2e = {"value": total_bops / e2e_t / 1e15, "unit": UNIT, "ms_per_step": e2e_t * 1e3,
                "h2d_bytes_per_step": int(2 * n * w * 8), "d2h_bytes_per_step": int(n * w * 8),
-               "path": "bmmgpu_multiply (include/bmmgpu.h) from host buffers"}
+               "path": "bmmgpu_multiply (include/bmmgpu.h) from pinned host buffers"}
 
     # ---- roofline of the dominant kernel
     peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())

@@ -120,6 +120,13 @@ int bmmgpu_dev_cubic(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint
 int bmmgpu_dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
                         uint64_t n, int32_t algo, int32_t leaf_log2, int32_t kernel, void* stream);
 
+/* The output-row slab [begin, end) of part `index` of `parts` (gran-aligned,
+ * contiguous, covering [0, m) exactly once).  The single partition rule of the
+ * multi-GPU driver (device slabs in bmmgpu_cubic, ranks in bench.py); output
+ * slabs are independent, so no exchange step exists.
+ * Pure host arithmetic, no device needed. */
+int bmmgpu_slab_rows(uint64_t m, uint32_t parts, uint32_t index, uint64_t gran, uint64_t* begin, uint64_t* end);
+
 /* Number of kernel launches the last host-API call made on its devices. */
 uint64_t bmmgpu_last_launch_count(void);
 

@@ -89,6 +89,8 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_dev_transpose.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp]
         L.bmmgpu_dev_cubic.argtypes = [vp, u64, vp, u64, vp, u64, u64, u64, u64, i32, i32, i32, vp]
         L.bmmgpu_dev_multiply.argtypes = [vp, u64, vp, u64, vp, u64, u64, i32, i32, i32, vp]
+        L.bmmgpu_slab_rows.argtypes = [u64, ctypes.c_uint32, ctypes.c_uint32, u64, _u64p, _u64p]
+        L.bmmgpu_slab_rows.restype = ctypes.c_int
         L.bmmgpu_last_launch_count.restype = u64
         L.bmmgpu_device_count.restype = ctypes.c_int
         L.bmmgpu_last_error.restype = ctypes.c_char_p
@@ -113,6 +115,14 @@ def _check(status: int) -> None:
 
 def device_count() -> int:
     return int(lib().bmmgpu_device_count())
+
+
+def slab_rows(m: int, parts: int, index: int, gran: int = 64) -> tuple[int, int]:
+    """Output-row slab of part `index` of `parts` (bmmgpu_slab_rows): the one
+    partition rule shared by the multi-device driver and the multi-rank bench."""
+    lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib().bmmgpu_slab_rows(m, parts, index, gran, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
 
 
 def granularity(kernel: int = Kernel.AUTO) -> tuple[int, int, int]:
@@ -252,8 +262,10 @@ def multiply_cubic(a: BitMatrix, b: BitMatrix, ring: Semiring, workers: int = 1,
 
 
 def multiply(a: BitMatrix, b: BitMatrix, algo: Algo, plan: LayerPlan, ring: Semiring, *,
-             kernel: int = Kernel.AUTO, leaf_log2: int = 0, timing: ctypes.c_double | None = None) -> BitMatrix:
-    """bmm::multiply (reference engine.cpp:351-382) on the GPU."""
+             kernel: int = Kernel.AUTO, leaf_log2: int = 0, timing: ctypes.c_double | None = None,
+             out: BitMatrix | None = None) -> BitMatrix:
+    """bmm::multiply (reference engine.cpp:351-382) on the GPU.  `out` may supply
+    the result storage (e.g. pinned host memory)."""
     if algo == Algo.Cubic:
         return multiply_cubic(a, b, ring, plan.workers, kernel=kernel, timing=timing)
     if ring == Semiring.BooleanOrAnd:
@@ -267,7 +279,9 @@ def multiply(a: BitMatrix, b: BitMatrix, algo: Algo, plan: LayerPlan, ring: Semi
     if (plan.matrix_dim() != n or plan.d_host < 0 or plan.d_serial < 0 or plan.d_parallel < 0
             or plan.d_inner != 1 or plan.workers < 1):
         raise ValueError("layer plan does not match the operands")
-    c = BitMatrix.zeros(n, n)
+    c = out if out is not None else BitMatrix.zeros(n, n)
+    if (c.rows, c.cols) != (n, n) or c.words.size != n * (n // 64):
+        raise ShapeError("output shape mismatch")
     p = _Plan(plan.d_host, plan.d_serial, plan.d_parallel, plan.d_inner, plan.workers)
     _check(lib().bmmgpu_multiply(_contig(a).ctypes.data, _contig(b).ctypes.data, c.words.ctypes.data, n, int(algo),
                                  ctypes.byref(p), int(ring), ctypes.byref(_opts(kernel, leaf_log2, timing))))

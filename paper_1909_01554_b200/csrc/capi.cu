@@ -209,6 +209,17 @@ using namespace bmmgpu;
 extern "C" {
 
 const char* bmmgpu_last_error(void) { return g_error.c_str(); }
+
+int bmmgpu_slab_rows(uint64_t m, uint32_t parts, uint32_t index, uint64_t gran, uint64_t* begin, uint64_t* end) {
+    if (parts == 0 || index >= parts || gran == 0 || !begin || !end) {
+        set_error("bmmgpu_slab_rows: need 0 <= index < parts and gran > 0");
+        return kEinval;
+    }
+    const uint64_t blocks = ceil_div(m, gran);
+    *begin = std::min(m, (blocks * index / parts) * gran);
+    *end = std::min(m, (blocks * (index + 1) / parts) * gran);
+    return kOk;
+}
 const char* bmmgpu_version(void) { return "bmm-b200 0.1 (sm_100a)"; }
 uint64_t bmmgpu_last_launch_count(void) { return g_launches.load(); }
 
@@ -256,13 +267,11 @@ int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, 
     }
     // Contiguous row slabs, aligned to 64 rows so device tiles never straddle.
     const uint64_t G = devs.size();
-    const uint64_t blocks = ceil_div(m, 64);
     std::vector<SlabJob> jobs;
     for (uint64_t g = 0; g < G; ++g) {
         SlabJob j;
         j.device = devs[g];
-        j.row_begin = std::min(m, (blocks * g / G) * 64);
-        j.row_end = std::min(m, (blocks * (g + 1) / G) * 64);
+        bmmgpu_slab_rows(m, uint32_t(G), uint32_t(g), 64, &j.row_begin, &j.row_end);
         jobs.push_back(j);
     }
     const bool gf2 = semiring == BMMGPU_GF2_XOR_AND;

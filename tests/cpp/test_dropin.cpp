@@ -1,0 +1,360 @@
+// test_dropin.cpp -- the drop-in C++ API (include/bmm/*.hpp + libbmm_b200.so)
+// exercised the way the reference's own suites exercise bmm_core
+// (reference proj/tests/test_bitmatrix.cpp, test_engine.cpp, test_decomposition.cpp).
+// Usage: test_dropin host   -- container, layout, I/O, plan, counts (no GPU)
+//        test_dropin gpu    -- every product through the GPU engine
+#include <bit>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "bmm/bitmatrix.hpp"
+#include "bmm/counter.hpp"
+#include "bmm/decomposition.hpp"
+#include "bmm/engine.hpp"
+#include "bmm/plan.hpp"
+
+using namespace bmm;
+
+namespace {
+
+int g_checks = 0, g_failures = 0;
+std::string g_case;
+
+#define CHECK(cond)                                                                         \
+    do {                                                                                    \
+        ++g_checks;                                                                         \
+        if (!(cond)) {                                                                      \
+            ++g_failures;                                                                   \
+            std::fprintf(stderr, "FAIL [%s] %s:%d: %s\n", g_case.c_str(), __FILE__, __LINE__, #cond); \
+        }                                                                                   \
+    } while (0)
+
+template <class E, class F>
+bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+// Bit-level schoolbook product: the independent oracle the reference tests use.
+BitMatrix naive(const BitMatrix& a, const BitMatrix& b, Semiring ring) {
+    BitMatrix c = BitMatrix::zeros(a.rows, b.cols);
+    for (std::uint64_t i = 0; i < a.rows; ++i)
+        for (std::uint64_t j = 0; j < b.cols; ++j) {
+            bool acc = false;
+            for (std::uint64_t k = 0; k < a.cols; ++k) {
+                const bool p = a.get(i, k) && b.get(k, j);
+                acc = ring == Semiring::Gf2XorAnd ? (acc != p) : (acc || p);
+            }
+            c.set(i, j, acc);
+        }
+    return c;
+}
+
+LayerPlan plan_for(int ds, int dp, int dh = 0) {
+    LayerPlan p;
+    p.d_host = dh;
+    p.d_serial = ds;
+    p.d_parallel = dp;
+    return p;
+}
+
+BitVectorTensor random_hat(std::vector<std::uint64_t> modes, std::uint64_t seed) {
+    BitVectorTensor t;
+    t.mode_lengths = std::move(modes);
+    t.words.resize(t.bit_length() / 64);
+    std::mt19937_64 g(seed);
+    for (auto& w : t.words) w = g();
+    return t;
+}
+
+std::uint64_t pow_u64(std::uint64_t b, int e) {
+    std::uint64_t r = 1;
+    while (e-- > 0) r *= b;
+    return r;
+}
+
+void run(const char* name, const std::function<void()>& f) {
+    g_case = name;
+    try {
+        f();
+    } catch (const std::exception& e) {
+        ++g_failures;
+        std::fprintf(stderr, "FAIL [%s] unexpected exception: %s\n", name, e.what());
+    }
+}
+
+// ------------------------------------------------------------------ host cases
+void host_cases() {
+    run("zeros and padding", [] {
+        BitMatrix m = BitMatrix::zeros(130, 130);
+        CHECK(m.words_per_row() == 3 && m.words.size() == 390 && !m.get(129, 129));
+        m.set(0, 64, true);
+        CHECK(m.get(0, 64) && m.words[1] == 1 && m.words[0] == 0);
+        CHECK(throws<ShapeError>([&] { (void)m.get(130, 0); }));
+        CHECK(throws<ShapeError>([&] { m.set(0, 130, true); }));
+    });
+    run("random determinism density padding", [] {
+        for (std::uint64_t seed = 0; seed < 4; ++seed) {
+            BitMatrix m = BitMatrix::random(1024, 1024, seed);
+            std::uint64_t ones = 0;
+            for (auto w : m.words) ones += std::popcount(w);
+            const double d = double(ones) / (1024.0 * 1024.0);
+            CHECK(d > 0.45 && d < 0.55);
+        }
+        CHECK(BitMatrix::random(130, 130, 7) == BitMatrix::random(130, 130, 7));
+        BitMatrix odd = BitMatrix::random(130, 130, 3);
+        for (std::uint64_t i = 0; i < odd.rows; ++i) CHECK((odd.row(i)[2] >> 2) == 0);
+        // same std::mt19937_64 stream as the reference: first word of random(8192,8192,1)
+        CHECK(BitMatrix::random(1, 64, 1).words[0] == 0x2245bd5fbb686f68ull);
+    });
+    run("bmm1 round trip and malformed files", [] {
+        const std::string path = "dropin_test.bmm";
+        BitMatrix m = BitMatrix::random(100, 200, 42);
+        write_bmm1(m, path);
+        CHECK(read_bmm1(path) == m);
+        {
+            std::FILE* f = std::fopen(path.c_str(), "ab");
+            std::fputc(0, f);
+            std::fclose(f);
+        }
+        CHECK(throws<FormatError>([&] { (void)read_bmm1(path); }));
+        {
+            std::FILE* f = std::fopen(path.c_str(), "wb");
+            std::fwrite("BMM2", 1, 4, f);
+            std::fclose(f);
+        }
+        CHECK(throws<FormatError>([&] { (void)read_bmm1(path); }));
+        BitMatrix odd = BitMatrix::zeros(2, 70);
+        write_bmm1(odd, path);
+        {
+            std::FILE* f = std::fopen(path.c_str(), "r+b");
+            std::fseek(f, 20 + 8 + 7, SEEK_SET);  // last byte of row 0's second word: pad bits
+            std::fputc(0x80, f);
+            std::fclose(f);
+        }
+        CHECK(throws<FormatError>([&] { (void)read_bmm1(path); }));
+        CHECK(throws<FormatError>([&] { (void)read_bmm1("does/not/exist.bmm"); }));
+        std::remove(path.c_str());
+    });
+    run("block transpose per bit and involution", [] {
+        BitMatrix m = BitMatrix::random(128, 192, 9), t = m;
+        transpose_blocks64(t);
+        for (std::uint64_t bi = 0; bi < 2; ++bi)
+            for (std::uint64_t bj = 0; bj < 3; ++bj)
+                for (unsigned r = 0; r < 64; ++r)
+                    for (unsigned c = 0; c < 64; ++c)
+                        if (t.get(bi * 64 + r, bj * 64 + c) != m.get(bi * 64 + c, bj * 64 + r)) CHECK(false);
+        transpose_blocks64(t);
+        CHECK(t == m);
+        BitMatrix odd = BitMatrix::zeros(65, 64);
+        CHECK(throws<ShapeError>([&] { transpose_blocks64(odd); }));
+    });
+    run("interleave worked example, bijection, round trips", [] {
+        LayerPlan p = plan_for(1, 0);
+        CHECK(interleaved_bit_index(p, Operand::Left, 66, 5) == 2 * 4096 + 2 * 64 + 5);
+        CHECK(interleaved_bit_index(p, Operand::Right, 66, 5) == 2 * 4096 + 5 * 64 + 2);
+        CHECK(throws<ShapeError>([&] { (void)interleaved_bit_index(p, Operand::Left, 128, 0); }));
+        LayerPlan p4 = plan_for(4, 0);
+        std::vector<bool> seen(1024 * 1024, false);
+        bool ok = true;
+        for (std::uint64_t i = 0; i < 1024; ++i)
+            for (std::uint64_t j = 0; j < 1024; ++j) {
+                const auto idx = interleaved_bit_index(p4, Operand::Right, i, j);
+                ok = ok && idx < seen.size() && !seen[idx];
+                seen[idx] = true;
+            }
+        CHECK(ok);
+        for (int depth = 0; depth <= 2; ++depth) {
+            LayerPlan q = plan_for(depth, 0);
+            const auto n = q.matrix_dim();
+            for (Operand op : {Operand::Left, Operand::Right, Operand::Result}) {
+                BitMatrix m = BitMatrix::random(n, n, 77 + depth);
+                BitVectorTensor t = to_interleaved(m, q, op);
+                CHECK(t.bit_length() == n * n && from_interleaved(t, q, op) == m);
+            }
+        }
+        CHECK(throws<ShapeError>([&] { (void)to_interleaved(BitMatrix::zeros(64, 64), p, Operand::Left); }));
+    });
+    run("pad_pow2", [] {
+        BitMatrix small = BitMatrix::random(50, 50, 2);
+        BitMatrix padded = pad_pow2(small);
+        CHECK(padded.rows == 64 && padded.cols == 64 && !padded.get(63, 0));
+        CHECK(pad_pow2(BitMatrix::random(100, 200, 3)).rows == 256);
+        BitMatrix exact = BitMatrix::random(128, 128, 4);
+        CHECK(pad_pow2(exact) == exact);
+    });
+    run("auto_plan", [] {
+        LayerPlan p = LayerPlan::auto_plan(4096, 2);
+        CHECK(p.d_serial == 3 && p.d_parallel == 3 && p.matrix_dim() == 4096 && p.workers == 2);
+        CHECK(LayerPlan::auto_plan(16384, 0).workers == 1);
+        CHECK(throws<ShapeError>([] { (void)LayerPlan::auto_plan(96, 1); }));
+    });
+    run("predicted additions and builtins", [] {
+        // reference test_decomposition.cpp:267-294
+        CHECK(predicted_additions(builtin(Builtin::AltSelfInverse), 1, CostPart::LinearCombinations) == 12);
+        CHECK(predicted_additions(builtin(Builtin::AltSelfInverse), 1, CostPart::BasisChanges) == 6);
+        CHECK(predicted_additions(builtin(Builtin::StrassenWinograd), 1, CostPart::LinearCombinations) == 15);
+        CHECK(&decomposition_for(Algo::AltSelfInverse) == &builtin(Builtin::AltSelfInverse));
+        CHECK(throws<std::invalid_argument>([] { (void)decomposition_for(Algo::Cubic); }));
+        CHECK(builtin(Builtin::AltChaining).traits.supports_chaining);
+        CHECK(!builtin(Builtin::AltSelfInverse).traits.supports_chaining);
+    });
+}
+
+// ------------------------------------------------------------------ gpu cases
+void gpu_cases() {
+    run("kernel64 matches the bitwise definition", [] {
+        const BitMatrix a = BitMatrix::random(64, 64, 11), b = BitMatrix::random(64, 64, 12);
+        BitMatrix bt = b;
+        transpose_blocks64(bt);
+        std::uint64_t out[64];
+        for (Semiring ring : {Semiring::Gf2XorAnd, Semiring::BooleanOrAnd}) {
+            kernel64(a.row(0), bt.row(0), out, ring);
+            const BitMatrix want = naive(a, b, ring);
+            for (int i = 0; i < 64; ++i) CHECK(out[i] == want.row(i)[0]);
+        }
+    });
+    run("cubic vs naive incl. odd shapes and the 2x2 example", [] {
+        BitMatrix a2 = BitMatrix::zeros(2, 2), b2 = BitMatrix::zeros(2, 2);
+        a2.set(0, 0, true), a2.set(0, 1, true), a2.set(1, 1, true);
+        b2.set(0, 0, true), b2.set(1, 0, true), b2.set(1, 1, true);
+        const BitMatrix g = multiply_cubic(a2, b2, Semiring::Gf2XorAnd);
+        CHECK(!g.get(0, 0) && g.get(0, 1) && g.get(1, 0) && g.get(1, 1));
+        for (Semiring ring : {Semiring::Gf2XorAnd, Semiring::BooleanOrAnd}) {
+            const BitMatrix wa = BitMatrix::random(128, 192, 22), wb = BitMatrix::random(192, 64, 23);
+            CHECK(multiply_cubic(wa, wb, ring) == naive(wa, wb, ring));
+            const BitMatrix oa = BitMatrix::random(130, 70, 24), ob = BitMatrix::random(70, 50, 25);
+            CHECK(multiply_cubic(oa, ob, ring) == naive(oa, ob, ring));
+        }
+        CHECK(throws<ShapeError>(
+            [] { (void)multiply_cubic(BitMatrix::random(64, 65, 26), BitMatrix::random(64, 64, 27), Semiring::Gf2XorAnd); }));
+    });
+    run("cubic counters", [] {
+        const BitMatrix a = BitMatrix::random(128, 128, 31), b = BitMatrix::random(128, 128, 32);
+        OpCounter c;
+        multiply_cubic(a, b, Semiring::Gf2XorAnd, 1, &c);
+        CHECK(c.kernel_invocations == 8 && c.word_ands == 8 * kBlockBits && c.word_xors == 4 * kBlockWords &&
+              c.word_ors == 0);
+        c.reset();
+        multiply_cubic(a, b, Semiring::BooleanOrAnd, 1, &c);
+        CHECK(c.kernel_invocations == 8 && c.word_ors == 4 * kBlockWords && c.word_xors == 0);
+    });
+    run("basis changes invert", [] {
+        const Decomposition& asi = builtin(Builtin::AltSelfInverse);
+        const Decomposition& ach = builtin(Builtin::AltChaining);
+        const BitVectorTensor orig = random_hat({4, 4, kBlockBits}, 41);
+        BitVectorTensor t = orig;
+        OpCounter c;
+        basis_change(t, asi, BasisFactor::Phi, 2, 1, &c);
+        CHECK(t != orig && c.word_xors == 1024);
+        basis_change(t, asi, BasisFactor::Phi, 2, 1, &c);
+        CHECK(t == orig && c.word_xors == 2048);
+        t = orig;
+        basis_change(t, ach, BasisFactor::Phi, 2);
+        basis_change(t, ach, BasisFactor::Chi, 2);
+        CHECK(t == orig);
+        BitVectorTensor wrong = random_hat({7, kBlockBits}, 42);
+        CHECK(throws<std::invalid_argument>([&] { basis_change(wrong, asi, BasisFactor::Phi, 1); }));
+    });
+    run("alt multiply matches cubic for every split and scheme", [] {
+        const BitMatrix a = BitMatrix::random(256, 256, 53), b = BitMatrix::random(256, 256, 54);
+        const BitMatrix want = multiply_cubic(a, b, Semiring::Gf2XorAnd);
+        for (Builtin w : {Builtin::AltSelfInverse, Builtin::AltChaining, Builtin::StrassenWinograd}) {
+            const Decomposition& d = builtin(w);
+            for (int ds = 0; ds <= 2; ++ds) {
+                const LayerPlan p = plan_for(ds, 2 - ds);
+                BitVectorTensor ah = to_interleaved(a, p, Operand::Left), bh = to_interleaved(b, p, Operand::Right);
+                basis_change(ah, d, BasisFactor::Phi, p.depth());
+                basis_change(bh, d, BasisFactor::Psi, p.depth());
+                BitVectorTensor ch = multiply_alt(ah, bh, d, p);
+                basis_change(ch, d, BasisFactor::Chi, p.depth());
+                CHECK(from_interleaved(ch, p, Operand::Result) == want);
+            }
+        }
+    });
+    run("alt multiply is bilinear and counts kernels", [] {
+        const Decomposition& asi = builtin(Builtin::AltSelfInverse);
+        const LayerPlan p = plan_for(1, 1);
+        const auto a1 = random_hat({4, 4, kBlockBits}, 63), a2 = random_hat({4, 4, kBlockBits}, 64),
+                   b1 = random_hat({4, 4, kBlockBits}, 65);
+        BitVectorTensor s = a1;
+        for (std::size_t i = 0; i < s.words.size(); ++i) s.words[i] ^= a2.words[i];
+        BitVectorTensor lhs = multiply_alt(s, b1, asi, p), r1 = multiply_alt(a1, b1, asi, p),
+                        r2 = multiply_alt(a2, b1, asi, p);
+        for (std::size_t i = 0; i < r1.words.size(); ++i) r1.words[i] ^= r2.words[i];
+        CHECK(lhs == r1);
+        OpCounter c;
+        multiply_alt(a1, b1, asi, p, &c);
+        CHECK(c.kernel_invocations == pow_u64(7, 2) && c.word_ands == pow_u64(7, 2) * kBlockBits);
+        CHECK(c.word_xors == predicted_additions(asi, 2, CostPart::LinearCombinations) * kBlockWords);
+        CHECK(throws<std::invalid_argument>([&] { (void)multiply_alt(a1, b1, asi, plan_for(3, 0)); }));
+    });
+    run("multiply dispatch, identity, associativity, errors", [] {
+        for (std::uint64_t n : {64ull, 128ull, 256ull}) {
+            const BitMatrix a = BitMatrix::random(n, n, 91 + n), b = BitMatrix::random(n, n, 92 + n);
+            const LayerPlan p = LayerPlan::auto_plan(n, 1);
+            const BitMatrix want = multiply(a, b, Algo::Cubic, p, Semiring::Gf2XorAnd);
+            for (Algo al : {Algo::StrassenWinograd, Algo::AltSelfInverse, Algo::AltChaining})
+                CHECK(multiply(a, b, al, p, Semiring::Gf2XorAnd) == want);
+        }
+        const BitMatrix a = BitMatrix::random(128, 128, 93), b = BitMatrix::random(128, 128, 94);
+        const LayerPlan p128 = LayerPlan::auto_plan(128, 1);
+        CHECK(throws<std::invalid_argument>([&] { (void)multiply(a, b, Algo::AltSelfInverse, p128, Semiring::BooleanOrAnd); }));
+        CHECK(throws<ShapeError>([&] {
+            (void)multiply(a, BitMatrix::random(128, 64, 98), Algo::AltSelfInverse, p128, Semiring::Gf2XorAnd);
+        }));
+        CHECK(throws<std::invalid_argument>(
+            [&] { (void)multiply(a, b, Algo::AltSelfInverse, LayerPlan::auto_plan(256, 1), Semiring::Gf2XorAnd); }));
+        const BitMatrix c = BitMatrix::random(256, 256, 95), d = BitMatrix::random(256, 256, 96),
+                        e = BitMatrix::random(256, 256, 97);
+        const LayerPlan p256 = LayerPlan::auto_plan(256, 1);
+        const auto cd = multiply(c, d, Algo::AltSelfInverse, p256, Semiring::Gf2XorAnd);
+        const auto de = multiply(d, e, Algo::AltSelfInverse, p256, Semiring::Gf2XorAnd);
+        CHECK(multiply(cd, e, Algo::AltSelfInverse, p256, Semiring::Gf2XorAnd) ==
+              multiply(c, de, Algo::AltSelfInverse, p256, Semiring::Gf2XorAnd));
+        OpCounter ctr;
+        multiply(a, b, Algo::AltSelfInverse, p128, Semiring::Gf2XorAnd, &ctr);
+        CHECK(ctr.kernel_invocations == 7);
+    });
+    run("chained multiplies stay in the output basis", [] {
+        const Decomposition& ach = builtin(Builtin::AltChaining);
+        const LayerPlan p = plan_for(1, 1);
+        const BitMatrix m0 = BitMatrix::random(256, 256, 101), m1 = BitMatrix::random(256, 256, 102),
+                        m2 = BitMatrix::random(256, 256, 103);
+        const BitMatrix want =
+            multiply_cubic(multiply_cubic(m0, m1, Semiring::Gf2XorAnd), m2, Semiring::Gf2XorAnd);
+        BitVectorTensor first = to_interleaved(m0, p, Operand::Left);
+        basis_change(first, ach, BasisFactor::Phi, p.depth());
+        std::vector<BitVectorTensor> ops = {first};
+        for (const BitMatrix* m : {&m1, &m2}) {
+            BitVectorTensor h = to_interleaved(*m, p, Operand::Right);
+            basis_change(h, ach, BasisFactor::Psi, p.depth());
+            ops.push_back(h);
+        }
+        BitVectorTensor ch = chain_multiply(ops, ach, p);
+        basis_change(ch, ach, BasisFactor::Chi, p.depth());
+        CHECK(from_interleaved(ch, p, Operand::Result) == want);
+        CHECK(throws<std::invalid_argument>([&] { (void)chain_multiply(ops, builtin(Builtin::AltSelfInverse), p); }));
+    });
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    const std::string mode = argc > 1 ? argv[1] : "host";
+    if (mode == "host" || mode == "all") host_cases();
+    if (mode == "gpu" || mode == "all") gpu_cases();
+    std::printf("%s: %d checks, %d failures\n", mode.c_str(), g_checks, g_failures);
+    return g_failures ? 1 : 0;
+}

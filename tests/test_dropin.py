@@ -1,0 +1,42 @@
+"""The C++ drop-in (include/bmm/*.hpp + libbmm_b200.so): a C++ program written
+against the reference's header API, compiled here with g++ and run -- host
+cases on CPU, product cases on the GPU (-m gpu)."""
+from __future__ import annotations
+
+import subprocess
+
+import pytest
+
+from conftest import HAS_GPU, ROOT
+
+SRC = ROOT / "tests" / "cpp" / "test_dropin.cpp"
+BIN = ROOT / "build" / "test_dropin"
+
+
+@pytest.fixture(scope="module")
+def dropin_binary():
+    import paper_1909_01554_b200 as bmm
+    lib_dir = bmm.HOST_LIB_PATH.parent
+    if not BIN.exists() or BIN.stat().st_mtime < max(SRC.stat().st_mtime, bmm.HOST_LIB_PATH.stat().st_mtime):
+        BIN.parent.mkdir(exist_ok=True)
+        subprocess.run(["g++", "-std=c++20", "-O1", "-I", str(ROOT / "include"), str(SRC), "-o", str(BIN),
+                        "-L", str(lib_dir), "-lbmm_b200", "-lbmmgpu", f"-Wl,-rpath,{lib_dir}"], check=True)
+    return BIN
+
+
+def _run(binary, mode: str) -> str:
+    r = subprocess.run([str(binary), mode], capture_output=True, text=True, cwd=str(ROOT / "build"), timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    return r.stdout
+
+
+def test_dropin_host_api(dropin_binary):
+    out = _run(dropin_binary, "host")
+    assert "0 failures" in out
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not HAS_GPU, reason="no CUDA device")
+def test_dropin_products_on_gpu(dropin_binary):
+    out = _run(dropin_binary, "gpu")
+    assert "0 failures" in out

@@ -1,0 +1,67 @@
+"""CPU, world_size 2 over gloo: the multi-rank plumbing bench.py uses for
+N GPUs (one process per GPU, output-row slabs, no data exchange, max-over-ranks
+timing) and the slab partition rule of the C ABI."""
+from __future__ import annotations
+
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, world: int, port: int, n: int, q) -> None:
+    import sys
+    sys.path.insert(0, str(ROOT))
+    os.environ.update({"RANK": str(rank), "LOCAL_RANK": str(rank), "WORLD_SIZE": str(world),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import torch
+    import torch.distributed as dist
+    import bench
+    d = bench.Dist()  # gloo: no CUDA in this container
+    assert d.pg is not None and dist.get_backend() == "gloo"
+    lo, hi = bench.shard_rows(n, d.rank, d.world, 256)
+    spans = [None] * world
+    dist.all_gather_object(spans, (lo, hi))
+    t = d.max(float(rank + 1) * 1.5)  # max-over-ranks of a per-rank time
+    d.barrier()
+    if rank == 0:
+        q.put((spans, t))
+    d.close()
+
+
+@pytest.mark.parametrize("world,n", [(2, 131072), (2, 1000), (2, 256)])
+def test_ranks_partition_rows_and_reduce_time(world, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    mp.start_processes(_worker, args=(world, port, n, q), nprocs=world, join=True, start_method="spawn")
+    spans, t = q.get(timeout=60)
+    assert t == 1.5 * world
+    covered = []
+    for lo, hi in spans:
+        assert lo % 256 == 0 and lo <= hi
+        covered.extend(range(lo, hi))
+    assert covered == list(range(n))  # disjoint, contiguous, complete: no exchange needed
+
+
+def test_slab_rule_matches_for_every_part_count():
+    import paper_1909_01554_b200 as bmm
+    for m in (0, 1, 63, 64, 65, 1000, 131072, 1 << 20):
+        for parts in (1, 2, 3, 4, 7, 8):
+            prev = 0
+            for i in range(parts):
+                lo, hi = bmm.slab_rows(m, parts, i, 64)
+                assert lo == prev and (lo % 64 == 0 or lo == m)
+                prev = hi
+            assert prev == m
+    with pytest.raises(ValueError):
+        bmm.slab_rows(10, 2, 2, 64)
