@@ -91,12 +91,15 @@ __device__ __forceinline__ void expand_store_sw128(uint8_t* region, int r, int g
     *reinterpret_cast<uint4*>(row + (((j0 + 3) ^ rr) << 4)) = make_uint4(y.x & M1, y.y & M1, y.z & M1, y.w & M1);
 }
 
-template <bool kGf2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     cubic_umma2_kernel(const uint64_t* __restrict__ A, uint64_t lda, const uint64_t* __restrict__ Bt, uint64_t ldbt,
-                       uint64_t* __restrict__ C, uint64_t ldc, uint64_t kw, int accumulate, TileMap map,
+                       uint64_t* __restrict__ C, uint64_t ldc, uint64_t kw, int flags, TileMap map,
                        uint32_t total_tiles) {
     extern __shared__ uint8_t smem_raw[];
+    // semiring as a runtime flag: one compiled main loop serves both (a template
+    // parameter let the two instantiations schedule the producer loop differently)
+    const bool kGf2 = (flags & 2) != 0;
+    const bool accumulate = (flags & 1) != 0;
     __shared__ __align__(8) uint64_t full_bar[P_STAGES];
     __shared__ __align__(8) uint64_t empty_bar[P_STAGES];
     __shared__ __align__(8) uint64_t acc_full_bar;
@@ -210,7 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             map.decode(t, b, tm, tn);
             uint32_t words[8];
             if (n_stages > 0) {
-                umma::mbar_wait(&acc_full_bar, local & 1);
+                umma::mbar_wait_sleep(&acc_full_bar, local & 1, 512);
                 umma::fence_after_sync();
 #pragma unroll 1
                 for (int c = 0; c < 8; ++c) {
@@ -302,9 +305,10 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
     const uint64_t max_pairs = std::min<uint64_t>(P_MAX_PAIRS, std::max(1, sms / 2));
     const uint64_t pairs = std::min<uint64_t>(total, max_pairs);
     TileMap map{uint32_t(m_tiles), uint32_t(n_tiles), uint32_t(per_prod), sA_batch, sB_batch, sC_batch};
-    auto kern = gf2 ? cubic_umma2_kernel<true> : cubic_umma2_kernel<false>;
+    auto kern = cubic_umma2_kernel;
     BMMGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P_SMEM)));
-    kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw, accumulate ? 1 : 0, map,
+    kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw,
+                                                             (accumulate ? 1 : 0) | (gf2 ? 2 : 0), map,
                                                              uint32_t(total));
     count_launch();
     BMMGPU_CUDA_TRY(cudaGetLastError());

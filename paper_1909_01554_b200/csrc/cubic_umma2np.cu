@@ -63,12 +63,13 @@ __device__ __forceinline__ void expand_store_sw128(uint8_t* region, int r, int g
     *reinterpret_cast<uint4*>(row + (((j0 + 3) ^ rr) << 4)) = make_uint4(y.x & M1, y.y & M1, y.z & M1, y.w & M1);
 }
 
-template <bool kGf2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     cubic_umma2np_kernel(const uint64_t* __restrict__ A, uint64_t lda, const uint64_t* __restrict__ Bt, uint64_t ldbt,
                        uint64_t* __restrict__ C, uint64_t ldc, uint64_t kw, int accumulate, uint32_t n_tiles,
                        uint32_t m_tiles, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch) {
     extern __shared__ uint8_t smem_raw[];
+    // semiring as a runtime flag (bit 1 of `accumulate`): one compiled main loop for both
+    const bool kGf2 = (accumulate & 2) != 0;
     __shared__ __align__(8) uint64_t full_bar[P_STAGES];
     __shared__ __align__(8) uint64_t empty_bar[P_STAGES];
     __shared__ __align__(8) uint64_t accum_bar;
@@ -195,7 +196,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         uint4* dst = reinterpret_cast<uint4*>(C + (row0 + warp * 32 + lane) * ldc + colp / 64);
         uint4 w0 = make_uint4(words[0], words[1], words[2], words[3]);
         uint4 w1 = make_uint4(words[4], words[5], words[6], words[7]);
-        if (accumulate) {
+        if (accumulate & 1) {
             const uint4 o0 = dst[0], o1 = dst[1];
             if (kGf2) {
                 w0 = make_uint4(w0.x ^ o0.x, w0.y ^ o0.y, w0.z ^ o0.z, w0.w ^ o0.w);
@@ -236,7 +237,7 @@ int launch_cubic_umma2np(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, 
         set_error("umma2np kernel: K above 2^24 bits would exceed exact fp32 accumulation");
         return kEinval;
     }
-    auto kern = gf2 ? cubic_umma2np_kernel<true> : cubic_umma2np_kernel<false>;
+    auto kern = cubic_umma2np_kernel;
     BMMGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P_SMEM)));
     const uint64_t m_tiles = m_pad / P_BM, n_tiles = n_pad / P_BN;
     const uint64_t blocks = 2 * m_tiles * n_tiles;
@@ -245,7 +246,7 @@ int launch_cubic_umma2np(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, 
         return kEinval;
     }
     const dim3 grid{unsigned(blocks), unsigned(batch), 1u};
-    kern<<<grid, P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw, accumulate ? 1 : 0, uint32_t(n_tiles),
+    kern<<<grid, P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw, (accumulate ? 1 : 0) | (gf2 ? 2 : 0), uint32_t(n_tiles),
                                               uint32_t(m_tiles), sA_batch, sB_batch, sC_batch);
     count_launch();
     BMMGPU_CUDA_TRY(cudaGetLastError());

@@ -29,6 +29,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
 }
+// For waits that last a whole tile (the epilogue waiting for its accumulator):
+// back off so idle warps do not compete with the producers for issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+}
 
 // Cluster-scope variants for the CTA pair (cta_group::2).
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -111,6 +116,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t sbo) {
     return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t((sbo >> 4) & 0x3FFF) << 32) |
            (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+
+// K-major, 64-byte swizzle: 8-row x 64 B atoms (512 B, 512-B aligned), 16-B
+// chunk j of row r at j ^ ((r >> 1) & 3).
+__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr, uint32_t sbo) {
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t((sbo >> 4) & 0x3FFF) << 32) |
+           (uint64_t(1) << 46) | (uint64_t(4) << 61);
 }
 
 // TMEM allocation for a CTA pair: one warp (same warp id) in each CTA.
