@@ -46,6 +46,8 @@ WORKLOADS = {
     "c1-gf2-cubic-8192": (8192, GF2, 0, "GF(2) product n=8192 cubic (BASELINE configs[0])"),
     "c1-bool-cubic-8192": (8192, BOOL, 0, "Boolean product n=8192 cubic (BASELINE configs[0])"),
     "c2-gf2-altsi-65536": (65536, GF2, 2, "GF(2) product n=65536 alternative-basis Strassen (BASELINE configs[1])"),
+    "c4-gf2-cubic-262144": (262144, GF2, 0, "GF(2) product n=262144, output row slabs (BASELINE configs[3])"),
+    "c4-gf2-altsi-262144": (262144, GF2, 2, "GF(2) product n=262144 alternative-basis Strassen"),
 }
 DEFAULT_WORKLOAD = "c3-bool-cubic-131072"
 # Paper V100 numbers for the same metric/config at 1 GPU, Pbop/s.
@@ -321,13 +323,8 @@ def run_ours(args, dist: Dist) -> None:
     # ---- end to end through the public C ABI, host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e and algo == 0:
-        class Opts(ctypes.Structure):
-            _fields_ = [("device_mask", ctypes.c_uint32), ("kernel", ctypes.c_int32),
-                        ("accumulate", ctypes.c_int32), ("leaf_log2", ctypes.c_int32),
-                        ("timing_ms", ctypes.POINTER(ctypes.c_double))]
-        opts = Opts(1 << dev, kernel, 0, 0, ctypes.POINTER(ctypes.c_double)())
-        lib.bmmgpu_cubic.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
-                                     ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32, ctypes.POINTER(Opts)]
+        opts = bmm._opts(kernel, device_mask=1 << dev, device_budget=args.device_budget,
+                         force_streaming=args.stream)
 
         def e2e_step() -> None:
             check(lib.bmmgpu_cubic(hA.data_ptr(), hB.data_ptr(), hC.data_ptr(), m, n, n, ring, ctypes.byref(opts)))
@@ -442,6 +439,10 @@ def main() -> None:
     ap.add_argument("--cpu-reps", dest="cpu_reps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stream", action="store_true",
+                    help="e2e leg through the out-of-core driver (A panels resident, B streamed in K-chunks)")
+    ap.add_argument("--device-budget", dest="device_budget", type=int, default=0,
+                    help="HBM bytes the e2e call may use (0 = free memory)")
     args = ap.parse_args()
     dist = Dist()
     try:

@@ -54,6 +54,12 @@ typedef struct bmmgpu_opts {
     int32_t leaf_log2;    /* fast algos: log2 of the leaf dimension the recursion stops at
                              and hands to the block-product kernel (>= 6); 0 = auto */
     double* timing_ms;    /* optional out: device time of the product on the slowest device */
+    uint64_t device_budget; /* HBM bytes one call may use per device; 0 = what is free.  Products
+                               whose operands do not fit run through the out-of-core driver:
+                               A row panels resident, B streamed in double-buffered K-chunks
+                               from host memory, partial products XOR/OR-integrated on device */
+    int32_t force_streaming; /* 1: use the out-of-core driver even when everything fits */
+    int32_t reserved;
 } bmmgpu_opts;
 
 /* bmm::LayerPlan (reference include/bmm/plan.hpp:26-44) */

@@ -61,7 +61,9 @@ class Kernel(enum.IntEnum):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("device_mask", ctypes.c_uint32), ("kernel", ctypes.c_int32), ("accumulate", ctypes.c_int32),
-                ("leaf_log2", ctypes.c_int32), ("timing_ms", ctypes.POINTER(ctypes.c_double))]
+                ("leaf_log2", ctypes.c_int32), ("timing_ms", ctypes.POINTER(ctypes.c_double)),
+                ("device_budget", ctypes.c_uint64), ("force_streaming", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class _Plan(ctypes.Structure):
@@ -227,13 +229,15 @@ def random_rows_into(out: np.ndarray, cols: int, seed: int, row_begin: int, row_
 
 
 def _opts(kernel: int, leaf_log2: int = 0, timing: ctypes.c_double | None = None, device_mask: int = 0,
-          accumulate: bool = False) -> _Opts:
+          accumulate: bool = False, device_budget: int = 0, force_streaming: bool = False) -> _Opts:
     o = _Opts()
     o.device_mask = device_mask
     o.kernel = int(kernel)
     o.accumulate = int(accumulate)
     o.leaf_log2 = int(leaf_log2)
     o.timing_ms = ctypes.pointer(timing) if timing is not None else ctypes.POINTER(ctypes.c_double)()
+    o.device_budget = int(device_budget)
+    o.force_streaming = int(force_streaming)
     return o
 
 
@@ -246,10 +250,13 @@ def _contig(m: BitMatrix) -> np.ndarray:
 
 def multiply_cubic(a: BitMatrix, b: BitMatrix, ring: Semiring, workers: int = 1, *, kernel: int = Kernel.AUTO,
                    device_mask: int = 0, out: BitMatrix | None = None, accumulate: bool = False,
-                   timing: ctypes.c_double | None = None) -> BitMatrix:
+                   timing: ctypes.c_double | None = None, device_budget: int = 0,
+                   force_streaming: bool = False) -> BitMatrix:
     """bmm::multiply_cubic (reference engine.cpp:132-144) on the GPU.
 
-    With `accumulate`, `out` is XOR/OR-folded with A.B (K-split integration)."""
+    With `accumulate`, `out` is XOR/OR-folded with A.B (K-split integration).
+    `device_budget` (bytes per device) / `force_streaming` select the
+    out-of-core driver (csrc/stream.cu) for products larger than HBM."""
     if a.cols != b.rows:
         raise ShapeError("inner dimensions differ")
     c = out if out is not None else BitMatrix.zeros(a.rows, b.cols)
@@ -257,7 +264,8 @@ def multiply_cubic(a: BitMatrix, b: BitMatrix, ring: Semiring, workers: int = 1,
         raise ShapeError("output shape mismatch")
     aw, bw = _contig(a), _contig(b)
     _check(lib().bmmgpu_cubic(aw.ctypes.data, bw.ctypes.data, c.words.ctypes.data, a.rows, a.cols, b.cols,
-                              int(ring), ctypes.byref(_opts(kernel, 0, timing, device_mask, accumulate))))
+                              int(ring), ctypes.byref(_opts(kernel, 0, timing, device_mask, accumulate,
+                                                            device_budget, force_streaming))))
     return c
 
 

@@ -40,6 +40,9 @@ int launch_cubic_umma2np(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, 
 void umma2np_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
 int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, const bmmgpu_plan* plan,
                       int kernel, int leaf_log2, double* timing_ms);
+int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const uint64_t* A, const uint64_t* B,
+                      uint64_t* C, uint64_t k, uint64_t n, bool gf2, int kernel, bool accumulate, uint64_t budget,
+                      float* ms_out);
 
 namespace {
 thread_local std::string g_error;
@@ -111,9 +114,10 @@ struct SlabJob {
     float ms = 0.f;
 };
 
-// One device's share of C = A.B: rows [row_begin, row_end) of A and C.
+// One device's share of C = A.B: rows [row_begin, row_end) of A and C.  In
+// core when A slab, B, Bt and C fit the budget, else the streamed driver.
 int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t k, uint64_t n,
-                   bool gf2, int kernel, bool accumulate) {
+                   bool gf2, int kernel, bool accumulate, uint64_t budget, bool force_streaming) {
     BMMGPU_CUDA_TRY(cudaSetDevice(job.device));
     const uint64_t m = job.row_end - job.row_begin;
     if (m == 0) return kOk;
@@ -124,6 +128,18 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
     const uint64_t m_pad = round_up(m, gm), n_pad = round_up(std::max<uint64_t>(n, 1), gn);
     const uint64_t kw = round_up(std::max<uint64_t>(ka, 1), gk / 64);
     const uint64_t cw = n_pad / 64;
+    {
+        uint64_t limit = budget;
+        if (limit == 0) {
+            size_t free_b = 0, total_b = 0;
+            BMMGPU_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+            limit = uint64_t(double(free_b) * 0.9);
+        }
+        const uint64_t in_core = (m_pad * kw + k * nb + n_pad * kw + m_pad * cw) * 8;
+        if (force_streaming || in_core > limit)
+            return stream_cubic_slab(job.device, job.row_begin, job.row_end, A, B, C, k, n, gf2, kernel,
+                                     accumulate, limit, &job.ms);
+    }
     cudaStream_t s;
     BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     struct StreamGuard {
@@ -276,7 +292,8 @@ int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, 
     }
     const bool gf2 = semiring == BMMGPU_GF2_XOR_AND;
     auto work = [&](SlabJob& j) {
-        j.status = run_cubic_slab(j, A, B, C, k, n, gf2, o.kernel, o.accumulate != 0);
+        j.status = run_cubic_slab(j, A, B, C, k, n, gf2, o.kernel, o.accumulate != 0, o.device_budget,
+                                  o.force_streaming != 0);
         if (j.status) j.error = g_error;
     };
     if (G == 1) {
