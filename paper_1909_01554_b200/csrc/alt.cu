@@ -187,25 +187,14 @@ using DevMem = DeviceBuffer;  // stream-ordered, pool-cached (common.cuh)
 
 }  // namespace
 
-// Device-resident fast product: dA (n x n/64, stride lda), dBt (Bt of B, n x
-// n/64, stride ldbt), dC (n x n/64, stride ldc).  dA and dBt are CLOBBERED
-// (basis-changed in place).  e recursion levels, leaves of size n >> e.
-int alt_multiply_device(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
-                        uint64_t n, int algo, int e, int kernel, cudaStream_t s) {
-    const Scheme* sc = scheme_for(algo);
-    if (!sc) {
-        set_error("no bilinear scheme for this algorithm");
-        return kEinval;
-    }
+// Breadth-first ("parallel") levels of the recursion in the scheme's basis:
+// e whole-array expand passes, one batched launch of the 7^e leaf products,
+// e compress passes into dC (reference parallel_leaf, engine.cpp:232-272).
+int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
+                uint64_t n, const Scheme* sc, int e, int kernel, cudaStream_t s) {
     int st;
-    if (e < 1 || (n >> e) < 64) {
-        set_error("alt_multiply_device: need 1 <= e and leaves of at least 64 bits");
-        return kEinval;
-    }
-    // phi on A, psi on B (seen through Bt) over the top e levels.
-    if ((st = launch_basis_change(dA, lda, n, e, make_steps(sc->phi, sc->n_phi, false), s))) return st;
-    if ((st = launch_basis_change(dBt, ldbt, n, e, make_steps(sc->psi, sc->n_psi, true), s))) return st;
-
+    if (e == 0)
+        return launch_cubic(kernel, dA, lda, dBt, ldbt, dC, ldc, n, n, n / 64, true, false, s, 1, 0, 0, 0);
     const Masks7 ma = make_expand(sc->alpha, false), mb = make_expand(sc->beta, true);
     Masks4 mg{};
     for (int q = 0; q < 4; ++q) mg.m[q] = uint8_t(row_mask(sc->gamma[q]));
@@ -314,8 +303,129 @@ int alt_multiply_device(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt
         cur_bs = out_bs;
         P = Pp;
     }
-    // chi on C over the top e levels.
+    return kOk;
+}
+
+namespace {
+
+// child = XOR of the quadrants of an L x L matrix selected by a 4-bit mask
+// (one alpha / beta row of a depth-first level, reference engine.cpp:284-285).
+__global__ void select_kernel(const uint64_t* __restrict__ in, uint64_t ld_in, uint64_t L, uint64_t* __restrict__ out,
+                              uint64_t ld_out, uint32_t mask) {
+    const uint64_t half = L / 2, hw = L / 128, total = half * hw;
+    for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t w = idx % hw, r = idx / hw;
+        const uint64_t* base = in + r * ld_in + w;
+        uint64_t v = 0;
+        if (mask & 1) v ^= base[0];
+        if (mask & 2) v ^= base[hw];
+        if (mask & 4) v ^= base[half * ld_in];
+        if (mask & 8) v ^= base[half * ld_in + hw];
+        out[r * ld_out + w] = v;
+    }
+}
+
+// quadrant q of C ^= child for every q in mask (one gamma column, folded as
+// each child product finishes; reference engine.cpp:288).
+__global__ void scatter_xor_kernel(const uint64_t* __restrict__ q_in, uint64_t ld_q, uint64_t L, uint64_t* C,
+                                   uint64_t ldc, uint32_t mask) {
+    const uint64_t half = L / 2, hw = L / 128, total = half * hw;
+    for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t w = idx % hw, r = idx / hw;
+        const uint64_t v = q_in[r * ld_q + w];
+        uint64_t* base = C + r * ldc + w;
+        if (mask & 1) base[0] ^= v;
+        if (mask & 2) base[hw] ^= v;
+        if (mask & 4) base[half * ldc] ^= v;
+        if (mask & 8) base[half * ldc + hw] ^= v;
+    }
+}
+
+}  // namespace
+
+// Depth-first ("serial") levels on top of the breadth-first ones: the 7
+// children of a level are formed, multiplied and folded into C one at a
+// time, so the working set per level is three quarter-size matrices
+// (reference alt_recurse with its per-level T/S/Q scratch, engine.cpp:274-289).
+// This is what lets products whose fully expanded levels would not fit in HBM
+// (n = 262144: (7/4)^e growth) run the fast algorithm.
+int alt_serial(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
+               uint64_t n, const Scheme* sc, int e_serial, int e_par, int kernel, cudaStream_t s) {
+    if (e_serial == 0) return alt_breadth(dA, lda, dBt, ldbt, dC, ldc, n, sc, e_par, kernel, s);
+    const uint64_t half = n / 2, hw = half / 64;
+    const Masks7 ma = make_expand(sc->alpha, false), mb = make_expand(sc->beta, true);
+    int st;
+    BMMGPU_CUDA_TRY(cudaMemset2DAsync(dC, ldc * 8, 0, (n / 64) * 8, n, s));
+    count_launch();
+    DevMem T, S, Q;
+    if ((st = T.alloc(half * hw * 8, s)) || (st = S.alloc(half * hw * 8, s)) || (st = Q.alloc(half * hw * 8, s)))
+        return st;
+    const uint64_t total = half * hw;
+    for (int h = 0; h < 7; ++h) {
+        select_kernel<<<grid_for(total), 256, 0, s>>>(dA, lda, n, T.u(), hw, ma.m[h]);
+        select_kernel<<<grid_for(total), 256, 0, s>>>(dBt, ldbt, n, S.u(), hw, mb.m[h]);
+        count_launch(2);
+        BMMGPU_CUDA_TRY(cudaGetLastError());
+        if ((st = alt_serial(T.u(), hw, S.u(), hw, Q.u(), hw, half, sc, e_serial - 1, e_par, kernel, s))) return st;
+        uint32_t cmask = 0;
+        for (int q = 0; q < 4; ++q)
+            if (row_mask(sc->gamma[q]) & (1u << h)) cmask |= 1u << q;
+        scatter_xor_kernel<<<grid_for(total), 256, 0, s>>>(Q.u(), hw, n, dC, ldc, cmask);
+        count_launch();
+        BMMGPU_CUDA_TRY(cudaGetLastError());
+    }
+    return kOk;
+}
+
+// Device-resident fast product: dA (n x n/64, stride lda), dBt (Bt of B, n x
+// n/64, stride ldbt), dC (n x n/64, stride ldc).  dA and dBt are CLOBBERED
+// (basis-changed in place).  e recursion levels (leaves of size n >> e), the
+// top e_serial of them depth-first.
+int alt_multiply_device(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
+                        uint64_t n, int algo, int e, int e_serial, int kernel, cudaStream_t s) {
+    const Scheme* sc = scheme_for(algo);
+    if (!sc) {
+        set_error("no bilinear scheme for this algorithm");
+        return kEinval;
+    }
+    int st;
+    if (e < 1 || (n >> e) < 64 || e_serial < 0 || e_serial > e) {
+        set_error("alt_multiply_device: need 1 <= e, 0 <= e_serial <= e and leaves of at least 64 bits");
+        return kEinval;
+    }
+    // phi on A, psi on B (seen through Bt) over the top e levels (reference engine.cpp:371-374).
+    if ((st = launch_basis_change(dA, lda, n, e, make_steps(sc->phi, sc->n_phi, false), s))) return st;
+    if ((st = launch_basis_change(dBt, ldbt, n, e, make_steps(sc->psi, sc->n_psi, true), s))) return st;
+    if ((st = alt_serial(dA, lda, dBt, ldbt, dC, ldc, n, sc, e_serial, e - e_serial, kernel, s))) return st;
+    // chi on C over the top e levels (reference engine.cpp:379-380).
     return launch_basis_change(dC, ldc, n, e, make_steps(sc->chi, sc->n_chi, false), s);
+}
+
+// Depth-first levels needed so the breadth-first part fits in `budget` bytes:
+// its peak is about four level-e arrays, 4 (7/4)^e_par (n >> e_serial)^2 / 8 bytes.
+// At least one level stays breadth-first (it pads the leaves to the kernel's tiles).
+int alt_serial_levels(uint64_t n, int e, uint64_t budget) {
+    for (int es = 0; es < e - 1; ++es) {
+        const uint64_t L = n >> es;
+        double bytes = 4.0 * double(L) * double(L) / 8.0;
+        for (int l = 0; l < e - es; ++l) bytes *= 1.75;
+        if (bytes <= double(budget)) return es;
+    }
+    return e > 0 ? e - 1 : 0;
+}
+
+uint64_t free_budget() {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
+    return uint64_t(double(free_b) * 0.8);
+}
+
+// Depth-first level count for this device (BMMGPU_ALT_SERIAL forces it; tests use it).
+int choose_serial_levels(uint64_t n, int e) {
+    if (const char* env = getenv("BMMGPU_ALT_SERIAL")) return std::max(0, std::min(atoi(env), e - 1));
+    return alt_serial_levels(n, e, free_budget());
 }
 
 // Recursion levels run as passes: the leaf dimension is 2^leaf_log2
@@ -371,7 +481,7 @@ int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_
         st = launch_cubic(kernel, dA.u(), kw, dBt.u(), kw, dC.u(), cw, rows_a, rows_b, kw, true, false, s, 1, 0, 0,
                           0);
     else
-        st = alt_multiply_device(dA.u(), w, dBt.u(), w, dC.u(), w, n, algo, e, kernel, s);
+        st = alt_multiply_device(dA.u(), w, dBt.u(), w, dC.u(), w, n, algo, e, choose_serial_levels(n, e), kernel, s);
     if (st) return st;
     BMMGPU_CUDA_TRY(cudaEventRecord(e1, s));
     BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(C, w * 8, dC.p, cw * 8, w * 8, n, cudaMemcpyDeviceToHost, s));
@@ -397,7 +507,7 @@ int dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint6
     kernel = resolve_kernel(kernel);
     const int e = alt_levels(n, leaf_log2);
     if (e == 0) return launch_cubic(kernel, dA, lda, dBt, ldbt, dC, ldc, n, n, n / 64, true, false, s, 1, 0, 0, 0);
-    return alt_multiply_device(dA, lda, dBt, ldbt, dC, ldc, n, algo, e, kernel, s);
+    return alt_multiply_device(dA, lda, dBt, ldbt, dC, ldc, n, algo, e, choose_serial_levels(n, e), kernel, s);
 }
 
 // ------------------------------------------------ interleaved basis change (K4)

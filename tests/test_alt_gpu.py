@@ -101,3 +101,19 @@ def test_interleaved_basis_change_matches_reference(engine, oracle, golden):
         assert f"{oracle.fnv1a64(w):016x}" == c["fnv"], c
         assert lib.bmmgpu_basis_change(w.ctypes.data, w.size, 2, algo_of_scheme[c["scheme"]], c["which"], 1) == 0
         assert np.array_equal(w, v)
+
+
+@pytest.mark.parametrize("serial", [1, 2, 3])
+def test_depth_first_levels_match_reference(engine, oracle, golden, serial, monkeypatch):
+    """The top `serial` recursion levels run depth-first (children formed, multiplied
+    and folded one at a time), the rest breadth-first: same bits for every split."""
+    bmm = engine
+    monkeypatch.setenv("BMMGPU_ALT_SERIAL", str(serial))
+    for c in golden["fast"]:
+        n = c["n"]
+        a = bmm.BitMatrix(n, n, oracle.random(n, n, c["a_seed"]))
+        b = bmm.BitMatrix(n, n, oracle.random(n, n, c["b_seed"]))
+        for leaf in (6, 7):
+            got = bmm.multiply(a, b, bmm.Algo(c["algo"]), _plan(bmm, c["plan"]), bmm.Semiring.Gf2XorAnd,
+                               leaf_log2=leaf)
+            assert f"{oracle.fnv1a64(got.words):016x}" == c["fnv"], (c, leaf, serial)
