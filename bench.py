@@ -439,8 +439,9 @@ def main() -> None:
     ap.add_argument("--cpu-reps", dest="cpu_reps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--stream", action="store_true",
-                    help="e2e leg through the out-of-core driver (A panels resident, B streamed in K-chunks)")
+    ap.add_argument("--stream", type=int, default=0, choices=[0, 1, 2],
+                    help="e2e driver: 0 auto, 1 out-of-core tiles (A panels resident, B streamed in K-chunks), "
+                         "2 K-outer pipeline (C resident, A/B K-chunks uploaded behind the product)")
     ap.add_argument("--device-budget", dest="device_budget", type=int, default=0,
                     help="HBM bytes the e2e call may use (0 = free memory)")
     args = ap.parse_args()

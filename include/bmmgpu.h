@@ -58,7 +58,9 @@ typedef struct bmmgpu_opts {
                                whose operands do not fit run through the out-of-core driver:
                                A row panels resident, B streamed in double-buffered K-chunks
                                from host memory, partial products XOR/OR-integrated on device */
-    int32_t force_streaming; /* 1: use the out-of-core driver even when everything fits */
+    int32_t force_streaming; /* 0 auto; 1: the out-of-core tile driver (A panels resident, B
+                                streamed per column tile); 2: the K-outer pipeline (C resident,
+                                A/B K-chunks uploaded while the previous chunk multiplies) */
     int32_t reserved;
 } bmmgpu_opts;
 

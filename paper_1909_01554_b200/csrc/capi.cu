@@ -40,6 +40,9 @@ int launch_cubic_umma2np(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, 
 void umma2np_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
 int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, const bmmgpu_plan* plan,
                       int kernel, int leaf_log2, double* timing_ms);
+int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const uint64_t* A, const uint64_t* B,
+                       uint64_t* C, uint64_t k, uint64_t n, bool gf2, int kernel, bool accumulate, uint64_t budget,
+                       float* ms_out, int chunks);
 int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const uint64_t* A, const uint64_t* B,
                       uint64_t* C, uint64_t k, uint64_t n, bool gf2, int kernel, bool accumulate, uint64_t budget,
                       float* ms_out);
@@ -117,7 +120,7 @@ struct SlabJob {
 // One device's share of C = A.B: rows [row_begin, row_end) of A and C.  In
 // core when A slab, B, Bt and C fit the budget, else the streamed driver.
 int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t k, uint64_t n,
-                   bool gf2, int kernel, bool accumulate, uint64_t budget, bool force_streaming) {
+                   bool gf2, int kernel, bool accumulate, uint64_t budget, int force_streaming) {
     BMMGPU_CUDA_TRY(cudaSetDevice(job.device));
     const uint64_t m = job.row_end - job.row_begin;
     if (m == 0) return kOk;
@@ -136,9 +139,17 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
             limit = uint64_t(double(free_b) * 0.9);
         }
         const uint64_t in_core = (m_pad * kw + k * nb + n_pad * kw + m_pad * cw) * 8;
-        if (force_streaming || in_core > limit)
+        const uint64_t c_slab = m_pad * cw * 8;
+        // force_streaming 1: the out-of-core tile driver; 2: the K-outer pipeline.
+        // Otherwise: long K with C resident -> K-outer pipeline (H2D hidden behind
+        // the product); everything fits -> in core; else the tile driver.
+        if (force_streaming == 1 || (force_streaming == 0 && in_core > limit && 3 * c_slab > limit))
             return stream_cubic_slab(job.device, job.row_begin, job.row_end, A, B, C, k, n, gf2, kernel,
                                      accumulate, limit, &job.ms);
+        if (force_streaming == 2 || (force_streaming == 0 && k >= 32768 && 3 * c_slab <= limit) ||
+            in_core > limit)
+            return stream_kouter_slab(job.device, job.row_begin, job.row_end, A, B, C, k, n, gf2, kernel,
+                                      accumulate, limit, &job.ms, 4);
     }
     cudaStream_t s;
     BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -293,7 +304,7 @@ int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, 
     const bool gf2 = semiring == BMMGPU_GF2_XOR_AND;
     auto work = [&](SlabJob& j) {
         j.status = run_cubic_slab(j, A, B, C, k, n, gf2, o.kernel, o.accumulate != 0, o.device_budget,
-                                  o.force_streaming != 0);
+                                  o.force_streaming);
         if (j.status) j.error = g_error;
     };
     if (G == 1) {

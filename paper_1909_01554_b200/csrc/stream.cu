@@ -183,4 +183,91 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
     return kOk;
 }
 
+// K-outer pipelined form for slabs whose C fits in HBM (the common in-core case
+// of the host API): K is cut into chunks; while the tensor cores fold chunk q
+// into the resident C, the copy stream uploads A[:, q+1] and B[q+1, :].  The
+// transfer of the inputs therefore hides behind the product instead of
+// preceding it; only the first chunk and the final D2H of C are exposed.
+int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const uint64_t* A, const uint64_t* B,
+                       uint64_t* C, uint64_t k, uint64_t n, bool gf2, int kernel, bool accumulate, uint64_t budget,
+                       float* ms_out, int chunks) {
+    BMMGPU_CUDA_TRY(cudaSetDevice(device));
+    const uint64_t m = row_end - row_begin;
+    if (m == 0 || n == 0) return kOk;
+    uint64_t gm, gn, gk;
+    int st = granularity(kernel, &gm, &gn, &gk);
+    if (st) return st;
+    const uint64_t gkw = gk / 64;
+    const uint64_t ka = ceil_div(k, 64), nb = ceil_div(n, 64);
+    const uint64_t m_pad = round_up(m, gm), n_pad = round_up(n, gn), cw = n_pad / 64;
+    const uint64_t kw = round_up(std::max<uint64_t>(ka, 1), gkw);
+    uint64_t KCw = round_up(ceil_div(kw, uint64_t(std::max(chunks, 1))), gkw);
+    auto need = [&](uint64_t kc) { return (m_pad * cw + 2 * (m_pad * kc + kc * 64 * nb + n_pad * kc)) * 8; };
+    while (need(KCw) > budget && KCw > gkw) KCw = round_up(KCw / 2, gkw);
+    if (need(KCw) > budget) {
+        set_error("K-outer driver: the resident C slab does not fit the device budget");
+        return kEinval;
+    }
+    const uint64_t KC = KCw * 64, n_chunks = ceil_div(kw, KCw);
+
+    cudaStream_t cs, xs;
+    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+    struct Guard {
+        cudaStream_t a, b;
+        ~Guard() {
+            cudaStreamDestroy(a);
+            cudaStreamDestroy(b);
+        }
+    } guard{cs, xs};
+    Events ev;  // 0,1 ready[buf]; 2,3 free[buf]; 5 start; 6 stop
+    for (int i = 0; i < 8; ++i)
+        BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&ev.e[i], i == 5 || i == 6 ? 0 : cudaEventDisableTiming));
+    DeviceBuffer dC, dA[2], dB[2], dBt[2];
+    if ((st = dC.alloc(m_pad * cw * 8, cs))) return st;
+    for (int b = 0; b < 2; ++b)
+        if ((st = dA[b].alloc(m_pad * KCw * 8, cs)) || (st = dB[b].alloc(KC * nb * 8, cs)) ||
+            (st = dBt[b].alloc(n_pad * KCw * 8, cs)))
+            return st;
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(cs));
+    BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[5], cs));
+    BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[2], cs));
+    BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[3], cs));
+    if (accumulate) {
+        BMMGPU_CUDA_TRY(cudaMemsetAsync(dC.p, 0, m_pad * cw * 8, cs));
+        BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dC.p, cw * 8, C + row_begin * nb, nb * 8, nb * 8, m,
+                                          cudaMemcpyHostToDevice, cs));
+        count_launch();
+    }
+    for (uint64_t q = 0; q < n_chunks; ++q) {
+        const int buf = int(q & 1);
+        const uint64_t w0 = q * KCw;
+        const uint64_t aw = w0 < ka ? std::min<uint64_t>(KCw, ka - w0) : 0;  // A words of this chunk
+        const uint64_t k0 = q * KC;
+        const uint64_t krows = k0 < k ? std::min<uint64_t>(KC, k - k0) : 0;
+        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(xs, ev.e[2 + buf], 0));
+        BMMGPU_CUDA_TRY(cudaMemsetAsync(dA[buf].p, 0, m_pad * KCw * 8, xs));
+        count_launch();
+        if (aw > 0)
+            BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dA[buf].p, KCw * 8, A + row_begin * ka + w0, ka * 8, aw * 8, m,
+                                              cudaMemcpyHostToDevice, xs));
+        if (krows > 0)
+            BMMGPU_CUDA_TRY(cudaMemcpyAsync(dB[buf].p, B + k0 * nb, krows * nb * 8, cudaMemcpyHostToDevice, xs));
+        BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[buf], xs));
+        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(cs, ev.e[buf], 0));
+        if ((st = launch_transpose(dB[buf].u(), nb, krows, n, dBt[buf].u(), n_pad, KCw, cs))) return st;
+        if ((st = launch_cubic(kernel, dA[buf].u(), KCw, dBt[buf].u(), KCw, dC.u(), cw, m_pad, n_pad, KCw, gf2,
+                               accumulate || q > 0, cs, 1, 0, 0, 0)))
+            return st;
+        BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[2 + buf], cs));
+    }
+    BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(C + row_begin * nb, nb * 8, dC.p, cw * 8, nb * 8, m, cudaMemcpyDeviceToHost,
+                                      cs));
+    BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[6], cs));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(cs));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(xs));
+    if (ms_out) cudaEventElapsedTime(ms_out, ev.e[5], ev.e[6]);
+    return kOk;
+}
+
 }  // namespace bmmgpu

@@ -149,8 +149,8 @@ def test_rejects_bad_panels(engine):
     assert b"m_pad" in lib.bmmgpu_last_error()
 
 
-@pytest.mark.parametrize("budget", [0, 3 << 20, 1 << 20, 600 << 10])
-def test_out_of_core_streamed_driver(engine, oracle, budget):
+@pytest.mark.parametrize("mode,budget", [(1, 0), (1, 3 << 20), (1, 1 << 20), (1, 600 << 10), (2, 0), (2, 2 << 20)])
+def test_out_of_core_streamed_driver(engine, oracle, mode, budget):
     """csrc/stream.cu: resident A panels, B streamed in double-buffered K-chunks,
     partial products folded on device -- bit-exact for every tiling the budget forces."""
     bmm = engine
@@ -159,10 +159,10 @@ def test_out_of_core_streamed_driver(engine, oracle, budget):
         b = _bm(bmm, oracle, k, n, 82)
         for ring in (GF2, BOOL):
             want = oracle.multiply_cubic(a.words, b.words, m, k, n, ring)
-            got = bmm.multiply_cubic(a, b, bmm.Semiring(ring), force_streaming=True, device_budget=budget)
+            got = bmm.multiply_cubic(a, b, bmm.Semiring(ring), force_streaming=mode, device_budget=budget)
             assert np.array_equal(got.words, want), (m, k, n, ring, budget)
             # accumulate through the streamed path: C (+)= A.B twice gives 0 (GF2) / the product (Boolean)
-            bmm.multiply_cubic(a, b, bmm.Semiring(ring), out=got, accumulate=True, force_streaming=True,
+            bmm.multiply_cubic(a, b, bmm.Semiring(ring), out=got, accumulate=True, force_streaming=mode,
                                device_budget=budget)
             if ring == GF2:
                 assert not got.words.any()
