@@ -60,6 +60,16 @@ constexpr uint32_t P_MAX_PAIRS = 74;  // 148 SMs
 
 static_assert(P_SMEM <= 232448 - 1024, "stage ring exceeds shared memory");
 
+// Pipeline timestamps (global timer, ns) of pair 0 when launched with the trace flag
+// (BMMGPU_UMMA_TRACE=1; microbench/trace_umma2.py): 0 MMA full, 512 commit,
+// 1024/2048 empty seen (CTA 0/1), 1536/2560 arrive (warp 0), +3072 arrive (warp 7).
+__device__ unsigned long long g_trace[6144];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 struct TileMap {
     uint32_t m_tiles, n_tiles, per_prod;  // per_prod = m_tiles * n_tiles
     uint64_t sA, sB, sC;                  // batch strides (words)
@@ -160,12 +170,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             for (uint64_t k = 0; k < n_stages; ++k, ++it) {
                 const int s = int(it % P_STAGES);
                 if (it >= P_STAGES) umma::mbar_wait(&empty_bar[s], uint32_t(((it / P_STAGES) + 1) & 1));
+                if ((flags & 16) && pair == 0 && tid == 0 && it < 512) g_trace[(rank ? 2048 : 1024) + it] = gtime();
                 uint8_t* sa = smem + size_t(s) * P_STAGE;
                 expand_store_sw128(sa, r, g, a0);
                 expand_store_sw128(sa + P_REGION, r, g, b0);
                 umma::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) umma::mbar_arrive_cluster(full_leader0 + s * 8);
+                if ((flags & 16) && pair == 0 && lane == 0 && (warp == 0 || warp == 7) && it < 512)
+                    g_trace[(rank ? 2560 : 1536) + (warp == 7 ? 3072 : 0) + it] = gtime();
                 a0 = a1; b0 = b1;
                 a1 = a2; b1 = b2;
                 if (k + P_PREFETCH < n_stages) {
@@ -188,6 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                 for (uint64_t k = 0; k < n_stages; ++k, ++it) {
                     const int s = int(it % P_STAGES);
                     umma::mbar_wait(&full_bar[s], uint32_t((it / P_STAGES) & 1));
+                    if ((flags & 16) && pair == 0 && it < 512) g_trace[it] = gtime();
                     umma::fence_after_sync();
                     const uint32_t a0 = base + uint32_t(s) * P_STAGE;
                     const uint32_t b0 = a0 + P_REGION;
@@ -199,6 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                         umma::mma_mxf4_pair(tmem, da, db, idesc, sf, sf, (k | j) ? 1u : 0u);
                     }
                     umma::mma_commit_pair(&empty_bar[s], 0x3);
+                    if ((flags & 16) && pair == 0 && it < 512) g_trace[512 + it] = gtime();
                 }
                 umma::mma_commit_pair(&acc_full_bar, 0x3);
             }
@@ -308,7 +323,9 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
     auto kern = cubic_umma2_kernel;
     BMMGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P_SMEM)));
     kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw,
-                                                             (accumulate ? 1 : 0) | (gf2 ? 2 : 0), map,
+                                                             (accumulate ? 1 : 0) | (gf2 ? 2 : 0) |
+                                                                 (getenv("BMMGPU_UMMA_TRACE") ? 16 : 0),
+                                                             map,
                                                              uint32_t(total));
     count_launch();
     BMMGPU_CUDA_TRY(cudaGetLastError());
@@ -316,3 +333,8 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
 }
 
 }  // namespace bmmgpu
+
+// Debug: copy the pipeline timestamps of the last traced launch.
+extern "C" int bmmgpu_debug_umma2_trace(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, bmmgpu::g_trace, sizeof(bmmgpu::g_trace)) == cudaSuccess ? 0 : 5;
+}
