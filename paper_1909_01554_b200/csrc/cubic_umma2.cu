@@ -63,12 +63,28 @@ static_assert(P_SMEM <= 232448 - 1024, "stage ring exceeds shared memory");
 // Pipeline timestamps (global timer, ns) of pair 0 when launched with the trace flag
 // (BMMGPU_UMMA_TRACE=1; microbench/trace_umma2.py): 0 MMA full, 512 commit,
 // 1024/2048 empty seen (CTA 0/1), 1536/2560 arrive (warp 0), +3072 arrive (warp 7).
+// Compiled in only with -DBMMGPU_TRACE (the build never sets it by default).
 __device__ unsigned long long g_trace[6144];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+#ifdef BMMGPU_TRACE
+#define TRACE_AT(cond, idx)                                \
+    do {                                                   \
+        if ((flags & 16) && (cond)) g_trace[idx] = gtime(); \
+    } while (0)
+#else
+#define TRACE_AT(cond, idx) \
+    do {                    \
+    } while (0)
+#endif
+
+#ifndef BMMGPU_RASTER_GROUP
+#define BMMGPU_RASTER_GROUP 8
+#endif
+constexpr uint32_t kRasterGroup = BMMGPU_RASTER_GROUP;  // row panels per rasterisation group
 
 struct TileMap {
     uint32_t m_tiles, n_tiles, per_prod;  // per_prod = m_tiles * n_tiles
@@ -79,7 +95,7 @@ struct TileMap {
     __device__ __forceinline__ void decode(uint32_t t, uint32_t& b, uint32_t& tm, uint32_t& tn) const {
         b = t / per_prod;
         const uint32_t r = t - b * per_prod;
-        const uint32_t group = 8, per_group = group * n_tiles;
+        const uint32_t group = kRasterGroup, per_group = group * n_tiles;
         const uint32_t first_m = (r / per_group) * group;
         const uint32_t gsize = min(group, m_tiles - first_m);
         const uint32_t in_g = r % per_group;
@@ -170,15 +186,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             for (uint64_t k = 0; k < n_stages; ++k, ++it) {
                 const int s = int(it % P_STAGES);
                 if (it >= P_STAGES) umma::mbar_wait(&empty_bar[s], uint32_t(((it / P_STAGES) + 1) & 1));
-                if ((flags & 16) && pair == 0 && tid == 0 && it < 512) g_trace[(rank ? 2048 : 1024) + it] = gtime();
+                TRACE_AT(pair == 0 && tid == 0 && it < 512, (rank ? 2048 : 1024) + it);
                 uint8_t* sa = smem + size_t(s) * P_STAGE;
                 expand_store_sw128(sa, r, g, a0);
                 expand_store_sw128(sa + P_REGION, r, g, b0);
                 umma::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) umma::mbar_arrive_cluster(full_leader0 + s * 8);
-                if ((flags & 16) && pair == 0 && lane == 0 && (warp == 0 || warp == 7) && it < 512)
-                    g_trace[(rank ? 2560 : 1536) + (warp == 7 ? 3072 : 0) + it] = gtime();
+                TRACE_AT(pair == 0 && lane == 0 && (warp == 0 || warp == 7) && it < 512,
+                         (rank ? 2560 : 1536) + (warp == 7 ? 3072 : 0) + it);
                 a0 = a1; b0 = b1;
                 a1 = a2; b1 = b2;
                 if (k + P_PREFETCH < n_stages) {
@@ -201,7 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                 for (uint64_t k = 0; k < n_stages; ++k, ++it) {
                     const int s = int(it % P_STAGES);
                     umma::mbar_wait(&full_bar[s], uint32_t((it / P_STAGES) & 1));
-                    if ((flags & 16) && pair == 0 && it < 512) g_trace[it] = gtime();
+                    TRACE_AT(pair == 0 && it < 512, it);
                     umma::fence_after_sync();
                     const uint32_t a0 = base + uint32_t(s) * P_STAGE;
                     const uint32_t b0 = a0 + P_REGION;
@@ -213,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                         umma::mma_mxf4_pair(tmem, da, db, idesc, sf, sf, (k | j) ? 1u : 0u);
                     }
                     umma::mma_commit_pair(&empty_bar[s], 0x3);
-                    if ((flags & 16) && pair == 0 && it < 512) g_trace[512 + it] = gtime();
+                    TRACE_AT(pair == 0 && it < 512, 512 + it);
                 }
                 umma::mma_commit_pair(&acc_full_bar, 0x3);
             }
