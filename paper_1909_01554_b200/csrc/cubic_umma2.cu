@@ -44,7 +44,10 @@ namespace {
 constexpr int P_BM = 256;                 // pair tile rows (128 per CTA)
 constexpr int P_BN = 256;                 // pair tile columns (Bt rows, 128 per CTA)
 constexpr int P_KBITS = 256;              // K bits per stage (4 MMAs of K = 64)
-constexpr int P_STAGES = 6;
+#ifndef BMMGPU_STAGES
+#define BMMGPU_STAGES 6
+#endif
+constexpr int P_STAGES = BMMGPU_STAGES;
 constexpr int P_ROWS = 128;               // rows of A and of Bt held per CTA
 constexpr int P_REGION = P_ROWS * 128;    // bytes of one operand per stage (16 KB)
 constexpr int P_STAGE = 2 * P_REGION;
@@ -168,7 +171,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         // ------------------------------------------------ producers: thread r owns row r of A and of Bt
         const int r = tid >> 1, g = tid & 1;  // row r, 128-bit half g of each 256-bit stage
         const uint32_t full_leader0 = umma::mapa_shared(smem_u32(&full_bar[0]), 0);
-        uint64_t it = 0;  // global stage counter (ring position)
+        uint64_t it = 0;            // global stage counter
+        int s = 0;                  // ring slot of stage `it`
+        uint32_t empty_parity = 1;  // parity of the empty-barrier phase to wait for in slot s
         for (uint32_t t = pair; t < total_tiles; t += n_pairs) {
             uint32_t b, tm, tn;
             map.decode(t, b, tm, tn);
@@ -184,8 +189,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             if (n_stages > 1) { a1 = __ldg(pa + 2); b1 = __ldg(pb + 2); }
             if (n_stages > 2) { a2 = __ldg(pa + 4); b2 = __ldg(pb + 4); }
             for (uint64_t k = 0; k < n_stages; ++k, ++it) {
-                const int s = int(it % P_STAGES);
-                if (it >= P_STAGES) umma::mbar_wait(&empty_bar[s], uint32_t(((it / P_STAGES) + 1) & 1));
+                if (it >= P_STAGES) umma::mbar_wait(&empty_bar[s], empty_parity);
                 TRACE_AT(pair == 0 && tid == 0 && it < 512, (rank ? 2048 : 1024) + it);
                 uint8_t* sa = smem + size_t(s) * P_STAGE;
                 expand_store_sw128(sa, r, g, a0);
@@ -201,30 +205,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                     a2 = __ldg(pa + 2 * (k + P_PREFETCH));
                     b2 = __ldg(pb + 2 * (k + P_PREFETCH));
                 }
+                if (++s == P_STAGES) {
+                    s = 0;
+                    if (it + 1 > P_STAGES) empty_parity ^= 1;  // first wrap waits for phase 0
+                    else empty_parity = 0;
+                }
             }
         }
     } else if (warp == P_MMA_WARP) {
         // ------------------------------------------------ MMA issuer (leader CTA, one lane)
         if (rank == 0 && lane == 0) {
             constexpr uint32_t idesc = umma::idesc_mxf4(P_BM, P_BN);
-            const uint32_t base = smem_u32(smem);
+            const uint64_t desc_base = umma::smem_desc_sw128(smem_u32(smem), 1024);
             uint64_t it = 0;
+            int s = 0;
+            uint32_t full_parity = 0;
             uint32_t local = 0;
             for (uint32_t t = pair; t < total_tiles; t += n_pairs, ++local) {
                 // the accumulator must have been drained by both CTAs' epilogues
                 if (local > 0) umma::mbar_wait(&acc_empty_bar, (local - 1) & 1);
                 umma::fence_after_sync();
-                for (uint64_t k = 0; k < n_stages; ++k, ++it) {
-                    const int s = int(it % P_STAGES);
-                    umma::mbar_wait(&full_bar[s], uint32_t((it / P_STAGES) & 1));
+                for (uint64_t k = 0; k < n_stages; ++k, ++it, s = (s + 1 == P_STAGES) ? (full_parity ^= 1, 0) : s + 1) {
+                    umma::mbar_wait(&full_bar[s], full_parity);
                     TRACE_AT(pair == 0 && it < 512, it);
                     umma::fence_after_sync();
-                    const uint32_t a0 = base + uint32_t(s) * P_STAGE;
-                    const uint32_t b0 = a0 + P_REGION;
+                    // descriptors differ only in the start-address field (bytes >> 4)
+                    const uint64_t da0 = desc_base + uint64_t((uint32_t(s) * P_STAGE) >> 4);
+                    const uint64_t db0 = da0 + (P_REGION >> 4);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const uint64_t da = umma::smem_desc_sw128(a0 + 32 * j, 1024);
-                        const uint64_t db = umma::smem_desc_sw128(b0 + 32 * j, 1024);
+                        const uint64_t da = da0 + 2 * j;  // + 32 bytes per K=64 step
+                        const uint64_t db = db0 + 2 * j;
                         const uint32_t sf = tmem + ((j & 1) ? P_SF_ODD : P_SF_EVEN);
                         umma::mma_mxf4_pair(tmem, da, db, idesc, sf, sf, (k | j) ? 1u : 0u);
                     }
