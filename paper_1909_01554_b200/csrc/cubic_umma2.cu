@@ -51,14 +51,24 @@ constexpr int P_STAGES = BMMGPU_STAGES;
 constexpr int P_ROWS = 128;               // rows of A and of Bt held per CTA
 constexpr int P_REGION = P_ROWS * 128;    // bytes of one operand per stage (16 KB)
 constexpr int P_STAGE = 2 * P_REGION;
-constexpr int P_PRODUCERS = 256;          // two threads per row of A and of Bt
+constexpr int P_PRODUCERS = 256;          // expanders: two threads per row of A and of Bt
 constexpr int P_MMA_WARP = P_PRODUCERS / 32;
-constexpr int P_THREADS = P_PRODUCERS + 32 + 128;  // producers, MMA/TMEM warp, 4 epilogue warps
-constexpr size_t P_SMEM = size_t(P_STAGES) * P_STAGE + 1024;  // + alignment slack
+constexpr int P_LOADER_WARP0 = P_MMA_WARP + 1 + 4;  // after the MMA warp and 4 epilogue warps
+constexpr int P_LOADERS = 64;
+constexpr int P_THREADS = P_PRODUCERS + 32 + 128 + P_LOADERS;
+// Packed operand bits, copied global -> shared by the loader warps with cp.async
+// (A rows then Bt rows, 32 bytes per row per stage).  Keeping global loads out of
+// the expander threads matters: their fence.proxy.async (MEMBAR.CTA) would wait
+// for every load still in flight and serialise one L2 round trip per stage.
+#ifndef BMMGPU_PK_STAGES
+#define BMMGPU_PK_STAGES 4
+#endif
+constexpr int P_PK_STAGES = BMMGPU_PK_STAGES;
+constexpr int P_PK_STAGE = 2 * P_ROWS * 32;  // 8 KB
+constexpr size_t P_SMEM = size_t(P_STAGES) * P_STAGE + size_t(P_PK_STAGES) * P_PK_STAGE + 1024;  // + alignment slack
 constexpr uint32_t P_TMEM_COLS = 512;
 constexpr uint32_t P_SF_EVEN = 256;
 constexpr uint32_t P_SF_ODD = 384;
-constexpr int P_PREFETCH = 3;
 constexpr uint32_t P_MAX_PAIRS = 74;  // 148 SMs
 
 static_assert(P_SMEM <= 232448 - 1024, "stage ring exceeds shared memory");
@@ -131,6 +141,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     const bool accumulate = (flags & 1) != 0;
     __shared__ __align__(8) uint64_t full_bar[P_STAGES];
     __shared__ __align__(8) uint64_t empty_bar[P_STAGES];
+    __shared__ __align__(8) uint64_t pk_full_bar[P_PK_STAGES];
+    __shared__ __align__(8) uint64_t pk_empty_bar[P_PK_STAGES];
     __shared__ __align__(8) uint64_t acc_full_bar;
     __shared__ __align__(8) uint64_t acc_empty_bar;
     __shared__ uint32_t tmem_base_sh;
@@ -146,6 +158,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         for (int s = 0; s < P_STAGES; ++s) {
             umma::mbar_init(&full_bar[s], 2 * (P_PRODUCERS / 32));
             umma::mbar_init(&empty_bar[s], 1);
+        }
+        for (int s = 0; s < P_PK_STAGES; ++s) {
+            umma::mbar_init(&pk_full_bar[s], P_LOADERS);
+            umma::mbar_init(&pk_empty_bar[s], P_PRODUCERS / 32);
         }
         umma::mbar_init(&acc_full_bar, 1);
         umma::mbar_init(&acc_empty_bar, 2 * 4);
@@ -171,45 +187,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         // ------------------------------------------------ producers: thread r owns row r of A and of Bt
         const int r = tid >> 1, g = tid & 1;  // row r, 128-bit half g of each 256-bit stage
         const uint32_t full_leader0 = umma::mapa_shared(smem_u32(&full_bar[0]), 0);
+        const uint8_t* pk = smem + size_t(P_STAGES) * P_STAGE + tid * 16;  // this thread's packed A bits
         uint64_t it = 0;            // global stage counter
         int s = 0;                  // ring slot of stage `it`
         uint32_t empty_parity = 1;  // parity of the empty-barrier phase to wait for in slot s
+        int ps = 0;                 // packed ring slot
+        uint32_t pk_parity = 0;
         for (uint32_t t = pair; t < total_tiles; t += n_pairs) {
-            uint32_t b, tm, tn;
-            map.decode(t, b, tm, tn);
-            const uint4* pa =
-                reinterpret_cast<const uint4*>(A + b * map.sA + (uint64_t(tm) * P_BM + rank * P_ROWS + r) * lda) + g;
-            const uint4* pb =
-                reinterpret_cast<const uint4*>(Bt + b * map.sB + (uint64_t(tn) * P_BN + rank * P_ROWS + r) * ldbt) +
-                g;
-            // three stages of packed bits in flight, 128 bits of A and of Bt per stage each
-            uint4 z = make_uint4(0, 0, 0, 0);
-            uint4 a0 = z, b0 = z, a1 = z, b1 = z, a2 = z, b2 = z;
-            if (n_stages > 0) { a0 = __ldg(pa); b0 = __ldg(pb); }
-            if (n_stages > 1) { a1 = __ldg(pa + 2); b1 = __ldg(pb + 2); }
-            if (n_stages > 2) { a2 = __ldg(pa + 4); b2 = __ldg(pb + 4); }
             for (uint64_t k = 0; k < n_stages; ++k, ++it) {
                 if (it >= P_STAGES) umma::mbar_wait(&empty_bar[s], empty_parity);
                 TRACE_AT(pair == 0 && tid == 0 && it < 512, (rank ? 2048 : 1024) + it);
+                umma::mbar_wait(&pk_full_bar[ps], pk_parity);
+                const uint4 a = *reinterpret_cast<const uint4*>(pk + ps * P_PK_STAGE);
+                const uint4 bb = *reinterpret_cast<const uint4*>(pk + ps * P_PK_STAGE + P_PK_STAGE / 2);
                 uint8_t* sa = smem + size_t(s) * P_STAGE;
-                expand_store_sw128(sa, r, g, a0);
-                expand_store_sw128(sa + P_REGION, r, g, b0);
+                expand_store_sw128(sa, r, g, a);
+                expand_store_sw128(sa + P_REGION, r, g, bb);
                 umma::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) umma::mbar_arrive_cluster(full_leader0 + s * 8);
+                if (lane == 0) {
+                    umma::mbar_arrive_cluster(full_leader0 + s * 8);
+                    umma::mbar_arrive(&pk_empty_bar[ps]);
+                }
                 TRACE_AT(pair == 0 && lane == 0 && (warp == 0 || warp == 7) && it < 512,
                          (rank ? 2560 : 1536) + (warp == 7 ? 3072 : 0) + it);
-                a0 = a1; b0 = b1;
-                a1 = a2; b1 = b2;
-                if (k + P_PREFETCH < n_stages) {
-                    a2 = __ldg(pa + 2 * (k + P_PREFETCH));
-                    b2 = __ldg(pb + 2 * (k + P_PREFETCH));
-                }
                 if (++s == P_STAGES) {
                     s = 0;
                     if (it + 1 > P_STAGES) empty_parity ^= 1;  // first wrap waits for phase 0
                     else empty_parity = 0;
                 }
+                if (++ps == P_PK_STAGES) { ps = 0; pk_parity ^= 1; }
             }
         }
     } else if (warp == P_MMA_WARP) {
@@ -243,6 +250,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                     TRACE_AT(pair == 0 && it < 512, 512 + it);
                 }
                 umma::mma_commit_pair(&acc_full_bar, 0x3);
+            }
+        }
+    } else if (warp >= P_LOADER_WARP0) {
+        // ------------------------------------------------ loaders: packed bits global -> shared (cp.async)
+        const uint32_t lt = tid - P_LOADER_WARP0 * 32;
+        uint8_t* pk = smem + size_t(P_STAGES) * P_STAGE;
+        uint64_t it = 0;
+        int ps = 0;
+        uint32_t pk_empty_parity = 1;
+        for (uint32_t t = pair; t < total_tiles; t += n_pairs) {
+            uint32_t b, tm, tn;
+            map.decode(t, b, tm, tn);
+            // chunk c = lt + 64 q (q < 4) of each operand: row c >> 1, 16-byte half c & 1
+            const uint8_t* ga = reinterpret_cast<const uint8_t*>(A + b * map.sA + (uint64_t(tm) * P_BM + rank * P_ROWS) * lda);
+            const uint8_t* gb =
+                reinterpret_cast<const uint8_t*>(Bt + b * map.sB + (uint64_t(tn) * P_BN + rank * P_ROWS) * ldbt);
+            const uint8_t* pa[4];
+            const uint8_t* pb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t c = lt + 64 * q;
+                pa[q] = ga + (c >> 1) * lda * 8 + (c & 1) * 16;
+                pb[q] = gb + (c >> 1) * ldbt * 8 + (c & 1) * 16;
+            }
+            for (uint64_t k = 0; k < n_stages; ++k, ++it) {
+                if (it >= P_PK_STAGES) umma::mbar_wait(&pk_empty_bar[ps], pk_empty_parity);
+                uint8_t* dst = pk + ps * P_PK_STAGE + lt * 16;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    cp_async16(dst + q * 1024, pa[q] + k * 32);
+                    cp_async16(dst + P_PK_STAGE / 2 + q * 1024, pb[q] + k * 32);
+                }
+                umma::cp_async_mbar_arrive_noinc(&pk_full_bar[ps]);
+                if (++ps == P_PK_STAGES) {
+                    ps = 0;
+                    if (it + 1 > P_PK_STAGES) pk_empty_parity ^= 1;
+                    else pk_empty_parity = 0;
+                }
             }
         }
     } else {
