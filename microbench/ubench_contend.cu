@@ -12,14 +12,20 @@ using namespace bmmgpu;
 constexpr int STAGES = 6, STAGE = 32768;
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
-    k_contend(uint32_t* out, int mma_iters, int sts_iters, int mode, unsigned long long* cycles) {
+    k_contend(uint32_t* out, int mma_iters, int sts_iters, int mode, unsigned long long* cycles, int fill) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ uint32_t tmem_base_sh;
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const unsigned tid = threadIdx.x, warp = tid >> 5;
     const uint32_t rank = umma::cluster_ctarank();
-    for (int i = tid; i < STAGES * STAGE / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x22222222u;
+    // operand data: fill 0 = all 1.0 (0x22222222), 1 = random bits expanded like the
+    // product kernel (x & 0x22222222 / x & 0x11111111 chunks), 2 = zeros
+    for (int i = tid; i < STAGES * STAGE / 4; i += blockDim.x) {
+        uint32_t x = (i + 1) * 2654435761u + blockIdx.x * 40503u;
+        x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+        reinterpret_cast<uint32_t*>(smem)[i] = fill == 0 ? 0x22222222u : fill == 2 ? 0u : (x & (((i >> 2) & 2) ? 0x11111111u : 0x22222222u));
+    }
     if (warp == 0) umma::tmem_alloc2(&tmem_base_sh, 512);
     if (tid == 0) {
         umma::mbar_init(&bar[0], 1);
@@ -97,13 +103,14 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const int mma_iters = 6000, sts_iters = 6000;
-    for (int mode : {1, 2, 3}) {
-        k_contend<<<sms, 384, smem>>>(out, 60, 60, mode, cyc);
+    const int mma_iters = 60000, sts_iters = 60000;  // ~18 ms: long enough for power limits to act
+    for (int fill : {0, 1, 2})
+    for (int mode : {1, 3}) {
+        k_contend<<<sms, 384, smem>>>(out, 60, 60, mode, cyc, fill);
         cudaDeviceSynchronize();
         for (int i = 0; i < 2 * sms; ++i) cyc[i] = 0;
         cudaEventRecord(e0);
-        k_contend<<<sms, 384, smem>>>(out, mma_iters, sts_iters, mode, cyc);
+        k_contend<<<sms, 384, smem>>>(out, mma_iters, sts_iters, mode, cyc, fill);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms = 0;
@@ -114,8 +121,8 @@ int main() {
         mma_c /= (sms / 2);
         sts_c /= sms;
         // per stage: MMA cycles (4 pair MMAs, M256 N256 K256) and STS bytes per cycle per SM (32 KB / stage)
-        printf("{\"mode\": %d, \"ms\": %.3f, \"mma_cycles_per_stage\": %.1f, \"sts_bytes_per_cycle\": %.1f, \"err\": \"%s\"}\n",
-               mode, ms, mma_c / mma_iters, sts_c > 0 ? 32768.0 * sts_iters / sts_c : 0.0,
+        printf("{\"fill\": %d, \"mode\": %d, \"ms\": %.3f, \"Pbops\": %.3f, \"mma_cycles_per_stage\": %.1f, \"sts_bytes_per_cycle\": %.1f, \"err\": \"%s\"}\n",
+               fill, mode, ms, double(sms / 2) * mma_iters * 2.0 * 256 * 256 * 256 / (ms * 1e-3) / 1e15, mma_c / mma_iters, sts_c > 0 ? 32768.0 * sts_iters / sts_c : 0.0,
                cudaGetErrorString(cudaGetLastError()));
     }
     return 0;

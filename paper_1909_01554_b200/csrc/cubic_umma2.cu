@@ -45,7 +45,7 @@ constexpr int P_BM = 256;                 // pair tile rows (128 per CTA)
 constexpr int P_BN = 256;                 // pair tile columns (Bt rows, 128 per CTA)
 constexpr int P_KBITS = 256;              // K bits per stage (4 MMAs of K = 64)
 #ifndef BMMGPU_STAGES
-#define BMMGPU_STAGES 6
+#define BMMGPU_STAGES 4
 #endif
 constexpr int P_STAGES = BMMGPU_STAGES;
 constexpr int P_ROWS = 128;               // rows of A and of Bt held per CTA
@@ -60,12 +60,14 @@ constexpr int P_THREADS = P_PRODUCERS + 32 + 128 + P_LOADERS;
 // (A rows then Bt rows, 32 bytes per row per stage).  Keeping global loads out of
 // the expander threads matters: their fence.proxy.async (MEMBAR.CTA) would wait
 // for every load still in flight and serialise one L2 round trip per stage.
-#ifndef BMMGPU_PK_STAGES
-#define BMMGPU_PK_STAGES 4
+#ifndef BMMGPU_SST_SLOTS
+#define BMMGPU_SST_SLOTS 2
 #endif
-constexpr int P_PK_STAGES = BMMGPU_PK_STAGES;
-constexpr int P_PK_STAGE = 2 * P_ROWS * 32;  // 8 KB
-constexpr size_t P_SMEM = size_t(P_STAGES) * P_STAGE + size_t(P_PK_STAGES) * P_PK_STAGE + 1024;  // + alignment slack
+constexpr int P_SST_SLOTS = BMMGPU_SST_SLOTS;  // packed ring slots, one superstage (4 stages) each
+constexpr int P_SST_OP = P_ROWS * 128;         // one operand of a superstage: 128 rows x 128 bytes
+constexpr int P_SST = 2 * P_SST_OP;            // 32 KB
+static_assert(P_STAGES % 2 == 0, "the two expander groups alternate ring slots");
+constexpr size_t P_SMEM = size_t(P_STAGES) * P_STAGE + size_t(P_SST_SLOTS) * P_SST + 1024;  // + alignment slack
 constexpr uint32_t P_TMEM_COLS = 512;
 constexpr uint32_t P_SF_EVEN = 256;
 constexpr uint32_t P_SF_ODD = 384;
@@ -91,6 +93,35 @@ __device__ __forceinline__ unsigned long long gtime() {
 #else
 #define TRACE_AT(cond, idx) \
     do {                    \
+    } while (0)
+#endif
+
+// Isolation probes for the pipeline (results garbage; only with -DBMMGPU_PROBE,
+// BMMGPU_UMMA_PROBE=v sets flag bits 32*v; microbench/probe.sh):
+// 32 no MMAs, 64 no operand stores, 128 loaders only (expanders just drain the packed ring),
+// 256 expanders ignore the packed ring.
+// The probe build also accounts the cycles each role spends waiting (g_probe, 8
+// counters per CTA: expander warp 0 empty / packed-full waits / loop total, MMA
+// lane full / acc_empty waits / loop total, loader warp 0 packed-empty wait / total).
+#ifdef BMMGPU_PROBE
+#define PROBE(bit) ((flags & (bit)) != 0)
+__device__ unsigned long long g_probe[2 * P_MAX_PAIRS * 8];
+#define PWAIT(slot, ...)                     \
+    do {                                     \
+        const long long _t0 = clock64();     \
+        __VA_ARGS__;                         \
+        pw[slot] += clock64() - _t0;         \
+    } while (0)
+#define PSTORE(first, last, cond)                                                              \
+    do {                                                                                       \
+        if (cond)                                                                              \
+            for (int _i = first; _i <= last; ++_i) g_probe[blockIdx.x * 8 + _i] = pw[_i];      \
+    } while (0)
+#else
+#define PROBE(bit) false
+#define PWAIT(slot, ...) __VA_ARGS__
+#define PSTORE(first, last, cond) \
+    do {                          \
     } while (0)
 #endif
 
@@ -141,8 +172,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     const bool accumulate = (flags & 1) != 0;
     __shared__ __align__(8) uint64_t full_bar[P_STAGES];
     __shared__ __align__(8) uint64_t empty_bar[P_STAGES];
-    __shared__ __align__(8) uint64_t pk_full_bar[P_PK_STAGES];
-    __shared__ __align__(8) uint64_t pk_empty_bar[P_PK_STAGES];
+    __shared__ __align__(8) uint64_t pk_full_bar[P_SST_SLOTS];
+    __shared__ __align__(8) uint64_t pk_empty_bar[P_SST_SLOTS];
     __shared__ __align__(8) uint64_t acc_full_bar;
     __shared__ __align__(8) uint64_t acc_empty_bar;
     __shared__ uint32_t tmem_base_sh;
@@ -156,12 +187,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     if (warp == P_MMA_WARP) umma::tmem_alloc2(&tmem_base_sh, P_TMEM_COLS);
     if (tid == 0) {
         for (int s = 0; s < P_STAGES; ++s) {
-            umma::mbar_init(&full_bar[s], 2 * (P_PRODUCERS / 32));
+            umma::mbar_init(&full_bar[s], 2 * (P_PRODUCERS / 64));  // one expander group per CTA
             umma::mbar_init(&empty_bar[s], 1);
         }
-        for (int s = 0; s < P_PK_STAGES; ++s) {
+        for (int s = 0; s < P_SST_SLOTS; ++s) {
             umma::mbar_init(&pk_full_bar[s], P_LOADERS);
-            umma::mbar_init(&pk_empty_bar[s], P_PRODUCERS / 32);
+            umma::mbar_init(&pk_empty_bar[s], P_PRODUCERS / 32);  // every expander warp, every superstage
         }
         umma::mbar_init(&acc_full_bar, 1);
         umma::mbar_init(&acc_empty_bar, 2 * 4);
@@ -184,41 +215,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     umma::fence_after_sync();
 
     if (warp < P_PRODUCERS / 32) {
-        // ------------------------------------------------ producers: thread r owns row r of A and of Bt
-        const int r = tid >> 1, g = tid & 1;  // row r, 128-bit half g of each 256-bit stage
+        // ------------------------------------------------ expanders: two groups of 4 warps take
+        // alternate stages (global stage parity = group), thread r of a group owns row r of A
+        // and of Bt.  While one group drains its stores through the proxy fence the other
+        // group's stores keep the shared-memory port busy.  Per superstage (4 stages of packed
+        // bits) a warp reads its rows' bits for its two stages, frees the packed slot, then
+        // expands and stores each stage into the tensor-core ring.
+        const uint32_t grp = warp >> 2, r = tid & (P_ROWS - 1), rsw = r & 7;
         const uint32_t full_leader0 = umma::mapa_shared(smem_u32(&full_bar[0]), 0);
-        const uint8_t* pk = smem + size_t(P_STAGES) * P_STAGE + tid * 16;  // this thread's packed A bits
-        uint64_t it = 0;            // global stage counter
-        int s = 0;                  // ring slot of stage `it`
-        uint32_t empty_parity = 1;  // parity of the empty-barrier phase to wait for in slot s
-        int ps = 0;                 // packed ring slot
+        const uint8_t* pkrow = smem + size_t(P_STAGES) * P_STAGE + r * 128;
+        uint64_t base = 0;  // global stage index of stage 0 of the current tile
+        int slot = 0;
         uint32_t pk_parity = 0;
-        for (uint32_t t = pair; t < total_tiles; t += n_pairs) {
-            for (uint64_t k = 0; k < n_stages; ++k, ++it) {
-                if (it >= P_STAGES) umma::mbar_wait(&empty_bar[s], empty_parity);
-                TRACE_AT(pair == 0 && tid == 0 && it < 512, (rank ? 2048 : 1024) + it);
-                umma::mbar_wait(&pk_full_bar[ps], pk_parity);
-                const uint4 a = *reinterpret_cast<const uint4*>(pk + ps * P_PK_STAGE);
-                const uint4 bb = *reinterpret_cast<const uint4*>(pk + ps * P_PK_STAGE + P_PK_STAGE / 2);
-                uint8_t* sa = smem + size_t(s) * P_STAGE;
-                expand_store_sw128(sa, r, g, a);
-                expand_store_sw128(sa + P_REGION, r, g, bb);
-                umma::fence_proxy_async_smem();
+#ifdef BMMGPU_PROBE
+        unsigned long long pw[8] = {};
+        const long long p_t0 = clock64();
+#endif
+        for (uint32_t t = pair; t < total_tiles; t += n_pairs, base += n_stages) {
+            const uint32_t sub0 = (uint32_t(base) ^ grp) & 1;  // first stage of this group in a superstage
+            for (uint64_t k0 = 0; k0 < n_stages; k0 += 4) {
+                if (!PROBE(256)) PWAIT(1, umma::mbar_wait(&pk_full_bar[slot], pk_parity));
+                const uint8_t* q = pkrow + slot * P_SST;
+                uint4 v[2][4];  // [stage][A lo, A hi, Bt lo, Bt hi]
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const uint32_t c = 2 * (sub0 + 2 * i);  // 16-byte chunk of the stage's low half
+                    v[i][0] = *reinterpret_cast<const uint4*>(q + ((c ^ rsw) << 4));
+                    v[i][1] = *reinterpret_cast<const uint4*>(q + (((c + 1) ^ rsw) << 4));
+                    v[i][2] = *reinterpret_cast<const uint4*>(q + P_SST_OP + ((c ^ rsw) << 4));
+                    v[i][3] = *reinterpret_cast<const uint4*>(q + P_SST_OP + (((c + 1) ^ rsw) << 4));
+                }
                 __syncwarp();
-                if (lane == 0) {
-                    umma::mbar_arrive_cluster(full_leader0 + s * 8);
-                    umma::mbar_arrive(&pk_empty_bar[ps]);
+                if (lane == 0 && !PROBE(256)) umma::mbar_arrive(&pk_empty_bar[slot]);
+                if (++slot == P_SST_SLOTS) { slot = 0; pk_parity ^= 1; }
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const uint64_t k = k0 + sub0 + 2 * i;
+                    if (k >= n_stages) break;
+                    const uint64_t it = base + k;
+                    const uint32_t s = uint32_t(it % P_STAGES);
+                    if (it >= P_STAGES && !PROBE(128))
+                        PWAIT(0, umma::mbar_wait(&empty_bar[s], uint32_t((it / P_STAGES - 1) & 1)));
+                    uint8_t* sa = smem + size_t(s) * P_STAGE;
+                    if (!PROBE(64 | 128)) {
+                        expand_store_sw128(sa, r, 0, v[i][0]);
+                        expand_store_sw128(sa, r, 1, v[i][1]);
+                        expand_store_sw128(sa + P_REGION, r, 0, v[i][2]);
+                        expand_store_sw128(sa + P_REGION, r, 1, v[i][3]);
+                    }
+                    umma::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0 && !PROBE(128)) umma::mbar_arrive_cluster(full_leader0 + s * 8);
                 }
-                TRACE_AT(pair == 0 && lane == 0 && (warp == 0 || warp == 7) && it < 512,
-                         (rank ? 2560 : 1536) + (warp == 7 ? 3072 : 0) + it);
-                if (++s == P_STAGES) {
-                    s = 0;
-                    if (it + 1 > P_STAGES) empty_parity ^= 1;  // first wrap waits for phase 0
-                    else empty_parity = 0;
-                }
-                if (++ps == P_PK_STAGES) { ps = 0; pk_parity ^= 1; }
             }
         }
+#ifdef BMMGPU_PROBE
+        pw[2] = clock64() - p_t0;
+#endif
+        PSTORE(0, 2, tid == 0);
     } else if (warp == P_MMA_WARP) {
         // ------------------------------------------------ MMA issuer (leader CTA, one lane)
         if (rank == 0 && lane == 0) {
@@ -228,12 +282,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             int s = 0;
             uint32_t full_parity = 0;
             uint32_t local = 0;
+#ifdef BMMGPU_PROBE
+            unsigned long long pw[8] = {};
+            const long long p_t0 = clock64();
+#endif
             for (uint32_t t = pair; t < total_tiles; t += n_pairs, ++local) {
                 // the accumulator must have been drained by both CTAs' epilogues
-                if (local > 0) umma::mbar_wait(&acc_empty_bar, (local - 1) & 1);
+                if (local > 0) PWAIT(4, umma::mbar_wait(&acc_empty_bar, (local - 1) & 1));
                 umma::fence_after_sync();
-                for (uint64_t k = 0; k < n_stages; ++k, ++it, s = (s + 1 == P_STAGES) ? (full_parity ^= 1, 0) : s + 1) {
-                    umma::mbar_wait(&full_bar[s], full_parity);
+                for (uint64_t k = 0; k < (PROBE(128) ? 0 : n_stages); ++k, ++it, s = (s + 1 == P_STAGES) ? (full_parity ^= 1, 0) : s + 1) {
+                    PWAIT(3, umma::mbar_wait(&full_bar[s], full_parity));
                     TRACE_AT(pair == 0 && it < 512, it);
                     umma::fence_after_sync();
                     // descriptors differ only in the start-address field (bytes >> 4)
@@ -244,6 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                         const uint64_t da = da0 + 2 * j;  // + 32 bytes per K=64 step
                         const uint64_t db = db0 + 2 * j;
                         const uint32_t sf = tmem + ((j & 1) ? P_SF_ODD : P_SF_EVEN);
+                        if (PROBE(32)) continue;
                         umma::mma_mxf4_pair(tmem, da, db, idesc, sf, sf, (k | j) ? 1u : 0u);
                     }
                     umma::mma_commit_pair(&empty_bar[s], 0x3);
@@ -251,45 +310,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                 }
                 umma::mma_commit_pair(&acc_full_bar, 0x3);
             }
+#ifdef BMMGPU_PROBE
+            pw[5] = clock64() - p_t0;
+#endif
+            PSTORE(3, 5, true);
         }
     } else if (warp >= P_LOADER_WARP0) {
         // ------------------------------------------------ loaders: packed bits global -> shared (cp.async)
-        const uint32_t lt = tid - P_LOADER_WARP0 * 32;
-        uint8_t* pk = smem + size_t(P_STAGES) * P_STAGE;
-        uint64_t it = 0;
-        int ps = 0;
-        uint32_t pk_empty_parity = 1;
-        for (uint32_t t = pair; t < total_tiles; t += n_pairs) {
+        // Superstage slot: [A, Bt][row][128 bytes = 4 stages], 16-byte chunk c of row r at
+        // c ^ (r & 7).  Loader thread lt always moves chunk c = lt & 7 of rows (lt >> 3) + 8 i,
+        // so a warp instruction covers four whole 128-byte rows.
+        const uint32_t lt = tid - P_LOADER_WARP0 * 32, c = lt & 7, r0 = lt >> 3;
+        uint8_t* pk = smem + size_t(P_STAGES) * P_STAGE + r0 * 128 + ((c ^ (r0 & 7)) << 4);
+        int slot = 0;
+        uint32_t pk_empty_parity = 0;
+        uint64_t qn = 0;  // superstages issued
+#ifdef BMMGPU_PROBE
+        unsigned long long pw[8] = {};
+        const long long p_t0 = clock64();
+#endif
+        for (uint32_t t = pair; t < (PROBE(256) ? 0 : total_tiles); t += n_pairs) {
             uint32_t b, tm, tn;
             map.decode(t, b, tm, tn);
-            // chunk c = lt + 64 q (q < 4) of each operand: row c >> 1, 16-byte half c & 1
-            const uint8_t* ga = reinterpret_cast<const uint8_t*>(A + b * map.sA + (uint64_t(tm) * P_BM + rank * P_ROWS) * lda);
-            const uint8_t* gb =
-                reinterpret_cast<const uint8_t*>(Bt + b * map.sB + (uint64_t(tn) * P_BN + rank * P_ROWS) * ldbt);
-            const uint8_t* pa[4];
-            const uint8_t* pb[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t c = lt + 64 * q;
-                pa[q] = ga + (c >> 1) * lda * 8 + (c & 1) * 16;
-                pb[q] = gb + (c >> 1) * ldbt * 8 + (c & 1) * 16;
-            }
-            for (uint64_t k = 0; k < n_stages; ++k, ++it) {
-                if (it >= P_PK_STAGES) umma::mbar_wait(&pk_empty_bar[ps], pk_empty_parity);
-                uint8_t* dst = pk + ps * P_PK_STAGE + lt * 16;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    cp_async16(dst + q * 1024, pa[q] + k * 32);
-                    cp_async16(dst + P_PK_STAGE / 2 + q * 1024, pb[q] + k * 32);
+            const uint8_t* ga = reinterpret_cast<const uint8_t*>(
+                                    A + b * map.sA + (uint64_t(tm) * P_BM + rank * P_ROWS + r0) * lda) + c * 16;
+            const uint8_t* gb = reinterpret_cast<const uint8_t*>(
+                                    Bt + b * map.sB + (uint64_t(tn) * P_BN + rank * P_ROWS + r0) * ldbt) + c * 16;
+            const uint64_t sa8 = 8 * lda * 8, sb8 = 8 * ldbt * 8;  // 8 rows further
+            for (uint64_t k0 = 0; k0 < n_stages; k0 += 4, ++qn) {
+                if (qn >= P_SST_SLOTS) PWAIT(6, umma::mbar_wait(&pk_empty_bar[slot], pk_empty_parity));
+                if (k0 + (c >> 1) < n_stages) {  // this chunk's stage exists
+                    uint8_t* dst = pk + slot * P_SST;
+                    const uint8_t* pa = ga + k0 * 32;
+                    const uint8_t* pb = gb + k0 * 32;
+#pragma unroll 4
+                    for (int i = 0; i < P_ROWS / 8; ++i) {
+                        cp_async16(dst + i * 1024, pa + i * sa8);
+                        cp_async16(dst + P_SST_OP + i * 1024, pb + i * sb8);
+                    }
                 }
-                umma::cp_async_mbar_arrive_noinc(&pk_full_bar[ps]);
-                if (++ps == P_PK_STAGES) {
-                    ps = 0;
-                    if (it + 1 > P_PK_STAGES) pk_empty_parity ^= 1;
-                    else pk_empty_parity = 0;
+                umma::cp_async_mbar_arrive_noinc(&pk_full_bar[slot]);
+                if (++slot == P_SST_SLOTS) {
+                    slot = 0;
+                    if (qn + 1 > P_SST_SLOTS) pk_empty_parity ^= 1;
                 }
             }
         }
+#ifdef BMMGPU_PROBE
+        pw[7] = clock64() - p_t0;
+#endif
+        PSTORE(6, 7, lt == 0);
     } else {
         // ------------------------------------------------ epilogue (warps 9-12)
         const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
@@ -396,7 +466,8 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
     BMMGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P_SMEM)));
     kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw,
                                                              (accumulate ? 1 : 0) | (gf2 ? 2 : 0) |
-                                                                 (getenv("BMMGPU_UMMA_TRACE") ? 16 : 0),
+                                                                 (getenv("BMMGPU_UMMA_TRACE") ? 16 : 0) |
+                                                                 (getenv("BMMGPU_UMMA_PROBE") && *getenv("BMMGPU_UMMA_PROBE") ? 32 * atoi(getenv("BMMGPU_UMMA_PROBE")) : 0),
                                                              map,
                                                              uint32_t(total));
     count_launch();
@@ -405,6 +476,16 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
 }
 
 }  // namespace bmmgpu
+
+// Debug: the per-CTA wait counters of the last launch of a -DBMMGPU_PROBE build.
+extern "C" int bmmgpu_debug_umma2_probe(unsigned long long* out) {
+#ifdef BMMGPU_PROBE
+    return cudaMemcpyFromSymbol(out, bmmgpu::g_probe, sizeof(bmmgpu::g_probe)) == cudaSuccess ? 0 : 5;
+#else
+    (void)out;
+    return 1;
+#endif
+}
 
 // Debug: copy the pipeline timestamps of the last traced launch.
 extern "C" int bmmgpu_debug_umma2_trace(unsigned long long* out) {
