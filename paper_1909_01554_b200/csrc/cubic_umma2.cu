@@ -35,6 +35,8 @@
 // drain the CTA's 128 accumulator rows 32 columns at a time, release the
 // accumulator to the leader (acc_empty) and store the bits.  (Eight producer
 // warps measured ~8% faster than four with one thread per row.)
+#include <cuda.h>
+
 #include "umma.cuh"
 
 namespace bmmgpu {
@@ -125,6 +127,10 @@ __device__ unsigned long long g_probe[2 * P_MAX_PAIRS * 8];
     } while (0)
 #endif
 
+#ifndef BMMGPU_EPI_SLEEP
+#define BMMGPU_EPI_SLEEP 512  // ns the epilogue warps sleep between polls of acc_full (0: spin)
+#endif
+
 #ifndef BMMGPU_RASTER_GROUP
 #define BMMGPU_RASTER_GROUP 8
 #endif
@@ -161,10 +167,14 @@ __device__ __forceinline__ void expand_store_sw128(uint8_t* region, int r, int g
     *reinterpret_cast<uint4*>(row + (((j0 + 3) ^ rr) << 4)) = make_uint4(y.x & M1, y.y & M1, y.z & M1, y.w & M1);
 }
 
+// kTma: the packed superstages arrive by TMA (one 3-D tiled box per operand, 128-byte
+// swizzle, K tail zero-filled by the bounds check) instead of the cp.async loader warps.
+template <bool kTma>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     cubic_umma2_kernel(const uint64_t* __restrict__ A, uint64_t lda, const uint64_t* __restrict__ Bt, uint64_t ldbt,
                        uint64_t* __restrict__ C, uint64_t ldc, uint64_t kw, int flags, TileMap map,
-                       uint32_t total_tiles) {
+                       uint32_t total_tiles, const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmB) {
     extern __shared__ uint8_t smem_raw[];
     // semiring as a runtime flag: one compiled main loop serves both (a template
     // parameter let the two instantiations schedule the producer loop differently)
@@ -191,7 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             umma::mbar_init(&empty_bar[s], 1);
         }
         for (int s = 0; s < P_SST_SLOTS; ++s) {
-            umma::mbar_init(&pk_full_bar[s], P_LOADERS);
+            umma::mbar_init(&pk_full_bar[s], kTma ? 1 : P_LOADERS);
             umma::mbar_init(&pk_empty_bar[s], P_PRODUCERS / 32);  // every expander warp, every superstage
         }
         umma::mbar_init(&acc_full_bar, 1);
@@ -315,6 +325,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #endif
             PSTORE(3, 5, true);
         }
+    } else if (kTma && warp >= P_LOADER_WARP0) {
+        // ------------------------------------------------ loader: one thread issues two TMA boxes per superstage
+        if (tid == P_LOADER_WARP0 * 32) {
+            umma::tma_prefetch_desc(&tmA);
+            umma::tma_prefetch_desc(&tmB);
+            uint8_t* pk = smem + size_t(P_STAGES) * P_STAGE;
+            int slot = 0;
+            uint32_t pk_empty_parity = 0;
+            uint64_t qn = 0;
+            for (uint32_t t = pair; t < (PROBE(256) ? 0 : total_tiles); t += n_pairs) {
+                uint32_t b, tm, tn;
+                map.decode(t, b, tm, tn);
+                const int32_t ra = int32_t(tm * P_BM + rank * P_ROWS), rb = int32_t(tn * P_BN + rank * P_ROWS);
+                for (uint64_t k0 = 0; k0 < n_stages; k0 += 4, ++qn) {
+                    if (qn >= P_SST_SLOTS) umma::mbar_wait(&pk_empty_bar[slot], pk_empty_parity);
+                    uint8_t* dst = pk + slot * P_SST;
+                    umma::mbar_arrive_expect_tx(&pk_full_bar[slot], P_SST);
+                    umma::tma_load_3d(dst, &tmA, int32_t(k0 * 4), ra, int32_t(b), &pk_full_bar[slot]);
+                    umma::tma_load_3d(dst + P_SST_OP, &tmB, int32_t(k0 * 4), rb, int32_t(b), &pk_full_bar[slot]);
+                    if (++slot == P_SST_SLOTS) {
+                        slot = 0;
+                        if (qn + 1 > P_SST_SLOTS) pk_empty_parity ^= 1;
+                    }
+                }
+            }
+        }
     } else if (warp >= P_LOADER_WARP0) {
         // ------------------------------------------------ loaders: packed bits global -> shared (cp.async)
         // Superstage slot: [A, Bt][row][128 bytes = 4 stages], 16-byte chunk c of row r at
@@ -370,7 +406,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             map.decode(t, b, tm, tn);
             uint32_t words[8];
             if (n_stages > 0) {
-                umma::mbar_wait_sleep(&acc_full_bar, local & 1, 512);
+                if (BMMGPU_EPI_SLEEP > 0)
+                    umma::mbar_wait_sleep(&acc_full_bar, local & 1, BMMGPU_EPI_SLEEP);
+                else
+                    umma::mbar_wait(&acc_full_bar, local & 1);
                 umma::fence_after_sync();
 #pragma unroll 1
                 for (int c = 0; c < 8; ++c) {
@@ -423,6 +462,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 
 }  // namespace
 
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+EncodeTiledFn encode_tiled() {
+    static const EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return EncodeTiledFn(nullptr);
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
+// Tensor map of a packed operand: [batch][rows][kw words], box 16 words (one 128-byte
+// superstage row) x 128 rows x 1, 128-byte swizzle = the loader's shared layout.
+bool make_operand_map(CUtensorMap* m, const uint64_t* base, uint64_t kw, uint64_t rows, uint64_t ld, uint64_t batch,
+                      uint64_t s_batch) {
+    const EncodeTiledFn fn = encode_tiled();
+    if (!fn || kw < 16 || rows < uint64_t(P_ROWS) || ld % 2 || (batch > 1 && (s_batch == 0 || s_batch % 2)) ||
+        (reinterpret_cast<uintptr_t>(base) & 15))
+        return false;
+    const cuuint64_t dims[3] = {kw, rows, batch};
+    const cuuint64_t strides[2] = {ld * 8, (batch > 1 ? s_batch : rows * ld) * 8};
+    const cuuint32_t box[3] = {16, uint32_t(P_ROWS), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void umma_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits) {
     *gm = P_BM;
     *gn = P_BN;
@@ -462,14 +535,20 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
     const uint64_t max_pairs = std::min<uint64_t>(P_MAX_PAIRS, std::max(1, sms / 2));
     const uint64_t pairs = std::min<uint64_t>(total, max_pairs);
     TileMap map{uint32_t(m_tiles), uint32_t(n_tiles), uint32_t(per_prod), sA_batch, sB_batch, sC_batch};
-    auto kern = cubic_umma2_kernel;
+    // TMA loads when the operands can be described by tensor maps (BMMGPU_UMMA_LOADER=cpasync
+    // forces the cp.async loader warps, which have no such constraints)
+    CUtensorMap tmA{}, tmB{};
+    const char* ld_env = getenv("BMMGPU_UMMA_LOADER");
+    const bool tma = !(ld_env && !strcmp(ld_env, "cpasync")) &&
+                     make_operand_map(&tmA, dA, kw, m_pad, lda, batch, sA_batch) &&
+                     make_operand_map(&tmB, dBt, kw, n_pad, ldbt, batch, sB_batch);
+    auto kern = tma ? cubic_umma2_kernel<true> : cubic_umma2_kernel<false>;
     BMMGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P_SMEM)));
-    kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw,
-                                                             (accumulate ? 1 : 0) | (gf2 ? 2 : 0) |
-                                                                 (getenv("BMMGPU_UMMA_TRACE") ? 16 : 0) |
-                                                                 (getenv("BMMGPU_UMMA_PROBE") && *getenv("BMMGPU_UMMA_PROBE") ? 32 * atoi(getenv("BMMGPU_UMMA_PROBE")) : 0),
-                                                             map,
-                                                             uint32_t(total));
+    const char* probe = getenv("BMMGPU_UMMA_PROBE");
+    const int flags = (accumulate ? 1 : 0) | (gf2 ? 2 : 0) | (getenv("BMMGPU_UMMA_TRACE") ? 16 : 0) |
+                      (probe && *probe ? 32 * atoi(probe) : 0);
+    kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw, flags, map,
+                                                             uint32_t(total), tmA, tmB);
     count_launch();
     BMMGPU_CUDA_TRY(cudaGetLastError());
     return kOk;

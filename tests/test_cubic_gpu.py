@@ -168,3 +168,19 @@ def test_out_of_core_streamed_driver(engine, oracle, mode, budget):
                 assert not got.words.any()
             else:
                 assert np.array_equal(got.words, want)
+
+
+@pytest.mark.parametrize("loader", ["tma", "cpasync"])
+def test_umma_pair_loaders(engine, oracle, monkeypatch, loader):
+    """The persistent pair kernel's two packed-bit loaders (TMA boxes / cp.async warps),
+    including K tails that end inside a 4-stage superstage (TMA zero-fills past K)."""
+    bmm = engine
+    monkeypatch.setenv("BMMGPU_UMMA_LOADER", loader)
+    shapes = [(256, 1024, 256), (256, 1280, 256), (512, 4096 + 768, 300), (300, 2048 + 64, 700), (700, 1536, 513)]
+    for t, (m, k, n) in enumerate(shapes):
+        a = _bm(bmm, oracle, m, k, 900 + t)
+        b = _bm(bmm, oracle, k, n, 950 + t)
+        for ring in (GF2, BOOL):
+            got = bmm.multiply_cubic(a, b, bmm.Semiring(ring), kernel=2)
+            want = oracle.multiply_cubic(a.words, b.words, m, k, n, ring)
+            assert np.array_equal(got.words, want), (loader, m, k, n, ring)
