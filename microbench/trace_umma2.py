@@ -1,4 +1,5 @@
-"""Cross-CTA pipeline timestamps of the persistent tcgen05 kernel (BMMGPU_UMMA_TRACE=1)."""
+"""Pipeline timestamps of the persistent tcgen05 kernel, pair 0, stages 0..511
+(needs a -DBMMGPU_TRACE build; BMMGPU_UMMA_TRACE=1 is set here).  Global timer, ns."""
 import ctypes, os, sys
 from pathlib import Path
 import numpy as np, torch
@@ -7,6 +8,7 @@ os.environ["BMMGPU_UMMA_TRACE"] = "1"
 import paper_1909_01554_b200 as bmm
 lib = bmm.lib()
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+S = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 kw = n // 64
 dA = torch.randint(-2**62, 2**62, (n, kw), dtype=torch.int64, device="cuda")
 dB = torch.randint(-2**62, 2**62, (n, kw), dtype=torch.int64, device="cuda")
@@ -18,15 +20,17 @@ t = (ctypes.c_ulonglong * 6144)()
 assert lib.bmmgpu_debug_umma2_trace(t) == 0
 a = np.array(t, dtype=np.int64)
 full, commit = a[0:512], a[512:1024]
-e0, e1, r0, r1, r0w7, r1w7 = a[1024:1536], a[2048:2560], a[1536:2048], a[2560:3072], a[1536+3072:2048+3072], a[2560+3072:3072+3072]
-S = 6
+e0, e1, r0, r1 = a[1024:1536], a[2048:2560], a[1536:2048], a[2560:3072]
+t0 = full[0]
+print("it   full  commit  empty0 empty1 arrive0 arrive1  (ns from full[0])")
+for it in range(0, 80):
+    print(f"{it:3d} {full[it]-t0:6d} {commit[it]-t0:6d} {e0[it]-t0:6d} {e1[it]-t0:6d} {r0[it]-t0:6d} {r1[it]-t0:6d}")
 rows = []
-for it in range(100, 500):
-    rows.append([e0[it] - commit[it - S], e1[it] - commit[it - S], r0[it] - e0[it], r1[it] - e1[it],
-                 full[it] - max(r0[it], r0w7[it]), full[it] - max(r1[it], r1w7[it]), commit[it] - full[it],
-                 full[it] - full[it - 1]])
-m = np.median(np.array(rows), axis=0)
-names = ["commit(it-6)->empty CTA0", "commit(it-6)->empty CTA1", "empty->arrive CTA0 w0", "empty->arrive CTA1 w0",
-         "last CTA0 arrive->full", "last CTA1 arrive->full", "full->commit (MMA issue)", "full(it)-full(it-1)"]
-for k, v in zip(names, m):
-    print(f"{k:28s} {v:8.0f} ns")
+for it in range(S + 8, 500):
+    rows.append([e0[it] - commit[it - S], r0[it] - e0[it], r1[it] - e1[it], full[it] - max(r0[it], r1[it]),
+                 full[it] - full[it - 1], commit[it] - full[it]])
+r = np.array(rows)
+names = ["commit(it-S) issued -> empty seen CTA0", "empty -> arrive CTA0", "empty -> arrive CTA1",
+         "last arrive -> full seen", "full(it) - full(it-1)", "full -> commit issued"]
+for k, col in zip(names, r.T):
+    print(f"{k:40s} median {np.median(col):7.0f}  p90 {np.percentile(col, 90):7.0f} ns")

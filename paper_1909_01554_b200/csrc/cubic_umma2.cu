@@ -78,8 +78,8 @@ constexpr uint32_t P_MAX_PAIRS = 74;  // 148 SMs
 static_assert(P_SMEM <= 232448 - 1024, "stage ring exceeds shared memory");
 
 // Pipeline timestamps (global timer, ns) of pair 0 when launched with the trace flag
-// (BMMGPU_UMMA_TRACE=1; microbench/trace_umma2.py): 0 MMA full, 512 commit,
-// 1024/2048 empty seen (CTA 0/1), 1536/2560 arrive (warp 0), +3072 arrive (warp 7).
+// (BMMGPU_UMMA_TRACE=1; microbench/trace_umma2.py): 0 MMA full, 512 commit issued,
+// 1024/2048 empty seen (CTA 0/1), 1536/2560 full arrive (first warp of the stage's group).
 // Compiled in only with -DBMMGPU_TRACE (the build never sets it by default).
 __device__ unsigned long long g_trace[6144];
 __device__ __forceinline__ unsigned long long gtime() {
@@ -266,6 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                     const uint32_t s = uint32_t(it % P_STAGES);
                     if (it >= P_STAGES && !PROBE(128))
                         PWAIT(0, umma::mbar_wait(&empty_bar[s], uint32_t((it / P_STAGES - 1) & 1)));
+                    TRACE_AT(pair == 0 && (warp & 3) == 0 && lane == 0 && it < 512, (rank ? 2048 : 1024) + it);
                     uint8_t* sa = smem + size_t(s) * P_STAGE;
                     if (!PROBE(64 | 128)) {
                         expand_store_sw128(sa, r, 0, v[i][0]);
@@ -276,6 +277,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                     umma::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0 && !PROBE(128)) umma::mbar_arrive_cluster(full_leader0 + s * 8);
+                    TRACE_AT(pair == 0 && (warp & 3) == 0 && lane == 0 && it < 512, (rank ? 2560 : 1536) + it);
                 }
             }
         }
@@ -284,8 +286,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #endif
         PSTORE(0, 2, tid == 0);
     } else if (warp == P_MMA_WARP) {
-        // ------------------------------------------------ MMA issuer (leader CTA, one lane)
-        if (rank == 0 && lane == 0) {
+        // ------------------------------------------------ MMA issuer (leader CTA).  The whole warp
+        // runs the loop so ring slots and descriptors stay warp-uniform (uniform registers, no
+        // per-instruction R2UR waterfall); one elected lane issues the MMAs and commits.
+        if (rank == 0) {
             constexpr uint32_t idesc = umma::idesc_mxf4(P_BM, P_BN);
             const uint64_t desc_base = umma::smem_desc_sw128(smem_u32(smem), 1024);
             uint64_t it = 0;
@@ -302,28 +306,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                 umma::fence_after_sync();
                 for (uint64_t k = 0; k < (PROBE(128) ? 0 : n_stages); ++k, ++it, s = (s + 1 == P_STAGES) ? (full_parity ^= 1, 0) : s + 1) {
                     PWAIT(3, umma::mbar_wait(&full_bar[s], full_parity));
-                    TRACE_AT(pair == 0 && it < 512, it);
+                    TRACE_AT(pair == 0 && lane == 0 && it < 512, it);
                     umma::fence_after_sync();
                     // descriptors differ only in the start-address field (bytes >> 4)
                     const uint64_t da0 = desc_base + uint64_t((uint32_t(s) * P_STAGE) >> 4);
                     const uint64_t db0 = da0 + (P_REGION >> 4);
+                    if (umma::elect_one()) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint64_t da = da0 + 2 * j;  // + 32 bytes per K=64 step
-                        const uint64_t db = db0 + 2 * j;
-                        const uint32_t sf = tmem + ((j & 1) ? P_SF_ODD : P_SF_EVEN);
-                        if (PROBE(32)) continue;
-                        umma::mma_mxf4_pair(tmem, da, db, idesc, sf, sf, (k | j) ? 1u : 0u);
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t sf = tmem + ((j & 1) ? P_SF_ODD : P_SF_EVEN);
+                            if (PROBE(32)) continue;
+                            // + 32 bytes per K = 64 step
+                            umma::mma_mxf4_pair(tmem, da0 + 2 * j, db0 + 2 * j, idesc, sf, sf, (k | j) ? 1u : 0u);
+                        }
+                        umma::mma_commit_pair(&empty_bar[s], 0x3);
                     }
-                    umma::mma_commit_pair(&empty_bar[s], 0x3);
-                    TRACE_AT(pair == 0 && it < 512, 512 + it);
+                    __syncwarp();
+                    TRACE_AT(pair == 0 && lane == 0 && it < 512, 512 + it);
                 }
-                umma::mma_commit_pair(&acc_full_bar, 0x3);
+                if (umma::elect_one()) umma::mma_commit_pair(&acc_full_bar, 0x3);
+                __syncwarp();
             }
 #ifdef BMMGPU_PROBE
             pw[5] = clock64() - p_t0;
 #endif
-            PSTORE(3, 5, true);
+            PSTORE(3, 5, lane == 0);
         }
     } else if (kTma && warp >= P_LOADER_WARP0) {
         // ------------------------------------------------ loader: one thread issues two TMA boxes per superstage
