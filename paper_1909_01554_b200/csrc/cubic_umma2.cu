@@ -26,15 +26,29 @@
 // regions the rest, so there is one accumulator).  This is what makes the
 // short-K leaf products of the alternative-basis recursion efficient.
 //
-// Roles per CTA (416 threads, 128 registers each): warps 0-7 produce, two
-// threads per row of A and of Bt (LDG.128 three stages ahead -> expand ->
-// STS.128, fence.proxy.async, arrive on the leader's full barrier, remotely
-// from the peer CTA); warp 8 owns TMEM and, in the leader, one lane issues 4
-// MMAs per 256-bit stage, commits each stage back to both CTAs' empty
-// barriers and each finished tile to both CTAs' acc_full barriers; warps 9-12
-// drain the CTA's 128 accumulator rows 32 columns at a time, release the
-// accumulator to the leader (acc_empty) and store the bits.  (Eight producer
-// warps measured ~8% faster than four with one thread per row.)
+// Roles per CTA (480 threads, 115 registers):
+//   loader (warp 13, one lane; TMA): per superstage of 4 stages (1024 K bits) one
+//     3-D tensor-map box per operand, 128 rows x 128 bytes with the 128-byte swizzle,
+//     into a 2-slot packed ring (K tails zero-filled by the box bounds).  Without a
+//     tensor map (odd strides, K < 1024 bits) warps 13-14 do the same with cp.async
+//     and swizzled 16-byte destinations.  Keeping global loads out of the expander
+//     threads matters: their fence.proxy.async (MEMBAR.CTA) would wait for every load
+//     still in flight and serialise one L2 round trip per stage.
+//   expanders (warps 0-7): two groups of 4 warps take alternate stages, thread r of a
+//     group owns row r of A and of Bt; per superstage a warp reads its rows' bits for
+//     its two stages (conflict-free through the swizzle), frees the packed slot, then
+//     per stage expands 256 bits -> 128 bytes of e2m1 per row with STS.128 into the
+//     4-stage operand ring, fences and arrives on the leader's full barrier
+//     (remotely from the peer CTA).  While one group drains its stores through the
+//     proxy fence the other group's stores keep the shared-memory port busy.
+//   MMA (warp 8, leader CTA): the whole warp runs the loop so slots and descriptors
+//     stay warp-uniform (no per-instruction R2UR waterfall); an elected lane issues
+//     4 MMAs per stage, commits each stage to both CTAs' empty barriers and each tile
+//     to both CTAs' acc_full barriers.
+//   epilogue (warps 9-12): drain the CTA's 128 accumulator rows 32 columns at a time,
+//     release the accumulator (acc_empty), store the bits.
+// Measured (microbench/probe_waits.py, ncu): the tensor pipe is 94-99% active; long
+// runs are held at ~1.65-1.72 GHz by the board power cap, not by the pipeline.
 #include <cuda.h>
 
 #include "umma.cuh"
@@ -58,10 +72,6 @@ constexpr int P_MMA_WARP = P_PRODUCERS / 32;
 constexpr int P_LOADER_WARP0 = P_MMA_WARP + 1 + 4;  // after the MMA warp and 4 epilogue warps
 constexpr int P_LOADERS = 64;
 constexpr int P_THREADS = P_PRODUCERS + 32 + 128 + P_LOADERS;
-// Packed operand bits, copied global -> shared by the loader warps with cp.async
-// (A rows then Bt rows, 32 bytes per row per stage).  Keeping global loads out of
-// the expander threads matters: their fence.proxy.async (MEMBAR.CTA) would wait
-// for every load still in flight and serialise one L2 round trip per stage.
 #ifndef BMMGPU_SST_SLOTS
 #define BMMGPU_SST_SLOTS 2
 #endif
@@ -132,7 +142,7 @@ __device__ unsigned long long g_probe[2 * P_MAX_PAIRS * 8];
 #endif
 
 #ifndef BMMGPU_RASTER_GROUP
-#define BMMGPU_RASTER_GROUP 8
+#define BMMGPU_RASTER_GROUP 16
 #endif
 constexpr uint32_t kRasterGroup = BMMGPU_RASTER_GROUP;  // row panels per rasterisation group
 
@@ -140,8 +150,9 @@ struct TileMap {
     uint32_t m_tiles, n_tiles, per_prod;  // per_prod = m_tiles * n_tiles
     uint64_t sA, sB, sC;                  // batch strides (words)
 
-    // Linear tile id -> (product, row tile, column tile), grouped by 8 row
-    // panels within a product so concurrently running pairs share panels in L2.
+    // Linear tile id -> (product, row tile, column tile), grouped by kRasterGroup row
+    // panels within a product so concurrently running pairs share panels in L2
+    // (16 measured best at n=131072: least DRAM traffic, so the most power headroom).
     __device__ __forceinline__ void decode(uint32_t t, uint32_t& b, uint32_t& tm, uint32_t& tn) const {
         b = t / per_prod;
         const uint32_t r = t - b * per_prod;
@@ -469,6 +480,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 
 }  // namespace
 
+#ifndef BMMGPU_L2_PROMOTION
+#define BMMGPU_L2_PROMOTION 3  // CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -499,7 +514,7 @@ bool make_operand_map(CUtensorMap* m, const uint64_t* base, uint64_t kw, uint64_
     const cuuint32_t box[3] = {16, uint32_t(P_ROWS), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CUtensorMapL2promotion(BMMGPU_L2_PROMOTION),
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
