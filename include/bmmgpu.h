@@ -120,11 +120,21 @@ int bmmgpu_dev_cubic(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint
                      uint64_t m_pad, uint64_t n_pad, uint64_t kw, int32_t semiring, int32_t kernel,
                      int32_t accumulate, void* stream);
 
+/* `batch` independent panel products in one persistent launch: product b uses
+ * dA + b*sA, dBt + b*sB, dC + b*sC (strides in words), otherwise as
+ * bmmgpu_dev_cubic.  The leaf layer of the fast recursion is this call
+ * (reference parallel_leaf's 7^d kernel64 calls, engine.cpp:232-272). */
+int bmmgpu_dev_cubic_batched(const uint64_t* dA, uint64_t lda, uint64_t sA, const uint64_t* dBt, uint64_t ldbt,
+                             uint64_t sB, uint64_t* dC, uint64_t ldc, uint64_t sC, uint64_t batch, uint64_t m_pad,
+                             uint64_t n_pad, uint64_t kw, int32_t semiring, int32_t kernel, int32_t accumulate,
+                             void* stream);
+
 /* Fast GF(2) product on device, n = 64 * 2^depth: dA (n x n/64 words, stride
  * lda), dBt = Bt of B (n x n/64, stride ldbt; rows padded to 256 in memory),
- * dC (n x n/64, stride ldc).  dA and dBt are overwritten (basis-changed in
- * place).  leaf_log2 as in bmmgpu_opts.  Synchronises the stream between
- * recursion levels (it frees level buffers as it goes). */
+ * dC (n x n/64, stride ldc).  dA and dBt are only read: the scheme's basis
+ * changes are folded into the expand / compress coefficients.  leaf_log2 as in
+ * bmmgpu_opts.  Stream-ordered; level buffers come from and return to the
+ * device's memory pool as the recursion proceeds. */
 int bmmgpu_dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
                         uint64_t n, int32_t algo, int32_t leaf_log2, int32_t kernel, void* stream);
 

@@ -91,6 +91,8 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_dev_transpose.argtypes = [vp, u64, u64, u64, vp, u64, u64, vp]
         L.bmmgpu_dev_cubic.argtypes = [vp, u64, vp, u64, vp, u64, u64, u64, u64, i32, i32, i32, vp]
         L.bmmgpu_dev_multiply.argtypes = [vp, u64, vp, u64, vp, u64, u64, i32, i32, i32, vp]
+        L.bmmgpu_dev_cubic_batched.argtypes = [vp, u64, u64, vp, u64, u64, vp, u64, u64, u64, u64, u64, u64, i32,
+                                               i32, i32, vp]
         L.bmmgpu_slab_rows.argtypes = [u64, ctypes.c_uint32, ctypes.c_uint32, u64, _u64p, _u64p]
         L.bmmgpu_slab_rows.restype = ctypes.c_int
         L.bmmgpu_last_launch_count.restype = u64
@@ -98,7 +100,7 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_last_error.restype = ctypes.c_char_p
         L.bmmgpu_version.restype = ctypes.c_char_p
         for name in ("bmmgpu_cubic", "bmmgpu_multiply", "bmmgpu_basis_change", "bmmgpu_dev_granularity",
-                     "bmmgpu_dev_transpose", "bmmgpu_dev_cubic", "bmmgpu_dev_multiply"):
+                     "bmmgpu_dev_transpose", "bmmgpu_dev_cubic", "bmmgpu_dev_multiply", "bmmgpu_dev_cubic_batched"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib

@@ -54,89 +54,167 @@ struct Steps {
 
 // ---------------------------------------------------------------- kernels
 
-// In-place basis change on every (sub_rows x sub_cols) submatrix of size L:
-// quadrant q = 2*qi + qj at row offset qi*L/2, word offset qj*L/128; the
-// program is a list of x[t] ^= x[s] (reference yates.cpp:143-172).
-__global__ void basis_change_kernel(uint64_t* __restrict__ M, uint64_t ld, uint64_t sub, uint64_t L, Steps steps) {
-    const uint64_t half = L / 2, hw = L / 128;
-    const uint64_t per_sub = half * hw;
-    const uint64_t total = sub * sub * per_sub;
-    for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
-         idx += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t w = idx % hw;
-        const uint64_t r = (idx / hw) % half;
-        const uint64_t s = idx / per_sub;
-        const uint64_t sr = s / sub, sc = s % sub;
-        uint64_t* base = M + (sr * L + r) * ld + sc * (L / 64) + w;
-        uint64_t* p[4] = {base, base + hw, base + half * ld, base + half * ld + hw};
-        uint64_t x[4] = {*p[0], *p[1], *p[2], *p[3]};
-        uint32_t dirty = 0;
-        for (int i = 0; i < steps.n; ++i) {
-            x[steps.t[i]] ^= x[steps.s[i]];
-            dirty |= 1u << steps.t[i];
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (dirty & (1u << q)) *p[q] = x[q];
-    }
-}
+// ---- fused passes.  The basis changes are folded into the coefficient masks (an
+// e-level recursion over exact leaf products computes chi^(x)e gamma^(x)e [leaves of
+// (alpha phi)^(x)e A and (beta psi)^(x)e B], and Kronecker powers compose factor-wise), so
+// no separate phi / psi / chi pass exists; and one pass covers up to two recursion
+// levels (16 sub-blocks in, 49 grandchildren out, or the reverse), so the level-(l+1)
+// arrays are never written or read back.  HBM bytes per operand at n = 65536, e = 4:
+// 16.5 x (n^2/8) instead of 30.7 x (plus 2 x 4 x (n^2/8) of in-place basis change).
 
-// Expand: P parents of size L (row stride ld_in, batch stride bs_in) -> 7P
-// children of size L/2 (ld_out, bs_out), child h = XOR of the parent
-// quadrants in mask m[h] (reference yates.cpp:112-141 with the alpha / beta
-// programs; engine.cpp:284-285).
-__global__ void expand_kernel(const uint64_t* __restrict__ in, uint64_t ld_in, uint64_t bs_in, uint64_t P, uint64_t L,
-                              uint64_t* __restrict__ out, uint64_t ld_out, uint64_t bs_out, Masks7 masks) {
-    const uint64_t half = L / 2, hw = L / 128;
-    const uint64_t per_p = half * hw;
-    const uint64_t total = P * per_p;
+template <int V>
+struct Words;
+template <>
+struct Words<1> {
+    using T = uint64_t;
+    __device__ static T zero() { return 0; }
+    __device__ static T x(T a, T b) { return a ^ b; }
+};
+template <>
+struct Words<2> {
+    using T = ulonglong2;
+    __device__ static T zero() { return make_ulonglong2(0, 0); }
+    __device__ static T x(T a, T b) { return make_ulonglong2(a.x ^ b.x, a.y ^ b.y); }
+};
+
+// Position decode shared by the fused passes: sub-blocks of ls rows x (wv * V) words,
+// all extents powers of two (shifts only).
+struct PassGeom {
+    uint32_t sh_wv, sh_ls;  // log2(words / V per sub-block row), log2(sub-block rows)
+    uint64_t ls, ws;        // sub-block rows, sub-block words
+};
+
+// Expand D levels at once: P parents (L x L, row stride ld_in words, batch stride
+// bs_in) -> 7^D P descendants of size L / 2^D.  Descendant (h_1 .. h_D) of parent p
+// is index p 7^D + h_1 7^(D-1) + .. + h_D, and equals sum over quadrant digits
+// q_1 .. q_D of prod_i M[h_i][q_i] times the sub-block (q_1 .. q_D) of the parent
+// (reference yates::mode_step with the alpha / beta programs, yates.cpp:112-141,
+// engine.cpp:284-285, applied D times).
+template <int D, int V>
+__global__ void __launch_bounds__(256) expand_pass_kernel(const uint64_t* __restrict__ in, uint64_t ld_in,
+                                                          uint64_t bs_in, uint64_t total, PassGeom g,
+                                                          uint64_t* __restrict__ out, uint64_t ld_out,
+                                                          uint64_t bs_out, Masks7 m) {
+    using W = Words<V>;
+    using T = typename W::T;
     for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
          idx += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t w = idx % hw;
-        const uint64_t r = (idx / hw) % half;
-        const uint64_t p = idx / per_p;
+        const uint64_t w = (idx & ((1ull << g.sh_wv) - 1)) * V;
+        const uint64_t r = (idx >> g.sh_wv) & (g.ls - 1);
+        const uint64_t p = idx >> (g.sh_wv + g.sh_ls);
         const uint64_t* base = in + p * bs_in + r * ld_in + w;
-        const uint64_t x0 = base[0], x1 = base[hw], x2 = base[half * ld_in], x3 = base[half * ld_in + hw];
-        uint64_t* dst = out + (p * 7) * bs_out + r * ld_out + w;
+        if (D == 1) {
+            T x[4];
 #pragma unroll
-        for (int h = 0; h < 7; ++h) {
-            const uint32_t m = masks.m[h];
-            uint64_t v = 0;
-            if (m & 1) v ^= x0;
-            if (m & 2) v ^= x1;
-            if (m & 4) v ^= x2;
-            if (m & 8) v ^= x3;
-            dst[h * bs_out] = v;
+            for (int q = 0; q < 4; ++q)
+                x[q] = *reinterpret_cast<const T*>(base + (q >> 1) * g.ls * ld_in + (q & 1) * g.ws);
+            uint64_t* dst = out + (p * 7) * bs_out + r * ld_out + w;
+#pragma unroll
+            for (int h = 0; h < 7; ++h) {
+                T v = W::zero();
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (m.m[h] & (1u << q)) v = W::x(v, x[q]);
+                *reinterpret_cast<T*>(dst + h * bs_out) = v;
+            }
+        } else {
+            // x[4 q + q']: quadrant q of the parent, sub-quadrant q' of it
+            T x[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int q2 = 0; q2 < 4; ++q2)
+                    x[4 * q + q2] = *reinterpret_cast<const T*>(
+                        base + ((q >> 1) * 2 + (q2 >> 1)) * g.ls * ld_in + ((q & 1) * 2 + (q2 & 1)) * g.ws);
+            uint64_t* dst = out + (p * 49) * bs_out + r * ld_out + w;
+#pragma unroll
+            for (int h = 0; h < 7; ++h) {
+                T y[4];  // sub-quadrants of child h
+#pragma unroll
+                for (int q2 = 0; q2 < 4; ++q2) {
+                    T v = W::zero();
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (m.m[h] & (1u << q)) v = W::x(v, x[4 * q + q2]);
+                    y[q2] = v;
+                }
+#pragma unroll
+                for (int h2 = 0; h2 < 7; ++h2) {
+                    T v = W::zero();
+#pragma unroll
+                    for (int q2 = 0; q2 < 4; ++q2)
+                        if (m.m[h2] & (1u << q2)) v = W::x(v, y[q2]);
+                    *reinterpret_cast<T*>(dst + (h * 7 + h2) * bs_out) = v;
+                }
+            }
         }
     }
 }
 
-// Compress: 7P children of size L/2 -> P parents of size L, parent quadrant q
-// = XOR of the children in mask m[q] (gamma; reference engine.cpp:288).
-__global__ void compress_kernel(const uint64_t* __restrict__ in, uint64_t ld_in, uint64_t bs_in, uint64_t P,
-                                uint64_t L, uint64_t* __restrict__ out, uint64_t ld_out, uint64_t bs_out,
-                                Masks4 masks) {
-    const uint64_t half = L / 2, hw = L / 128;
-    const uint64_t per_p = half * hw;
-    const uint64_t total = P * per_p;
+// Compress D levels at once: 7^D P descendants (size L / 2^D, ld_in, bs_in) -> P
+// parents (L x L, ld_out, bs_out); sub-block (q_1 .. q_D) of parent p = sum over
+// (h_1 .. h_D) of prod_i G[q_i][h_i] times descendant (h_1 .. h_D) (gamma folded
+// with chi; reference engine.cpp:288 and the chi basis change 379-380).
+#ifndef BMMGPU_COMPRESS_MINB
+#define BMMGPU_COMPRESS_MINB 2  // resident CTAs per SM the compress pass is compiled for
+#endif
+template <int D, int V>
+__global__ void __launch_bounds__(256, BMMGPU_COMPRESS_MINB) compress_pass_kernel(const uint64_t* __restrict__ in, uint64_t ld_in,
+                                                            uint64_t bs_in, uint64_t total, PassGeom g,
+                                                            uint64_t* __restrict__ out, uint64_t ld_out,
+                                                            uint64_t bs_out, Masks4 m) {
+    using W = Words<V>;
+    using T = typename W::T;
     for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
          idx += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t w = idx % hw;
-        const uint64_t r = (idx / hw) % half;
-        const uint64_t p = idx / per_p;
-        const uint64_t* src = in + (p * 7) * bs_in + r * ld_in + w;
-        uint64_t y[7];
+        const uint64_t w = (idx & ((1ull << g.sh_wv) - 1)) * V;
+        const uint64_t r = (idx >> g.sh_wv) & (g.ls - 1);
+        const uint64_t p = idx >> (g.sh_wv + g.sh_ls);
+        uint64_t* base = out + p * bs_out + r * ld_out + w;
+        if (D == 1) {
+            const uint64_t* src = in + (p * 7) * bs_in + r * ld_in + w;
+            T y[7];
 #pragma unroll
-        for (int h = 0; h < 7; ++h) y[h] = src[h * bs_in];
-        uint64_t* dst = out + p * bs_out + r * ld_out + w;
+            for (int h = 0; h < 7; ++h) y[h] = *reinterpret_cast<const T*>(src + h * bs_in);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t m = masks.m[q];
-            uint64_t v = 0;
+            for (int q = 0; q < 4; ++q) {
+                T v = W::zero();
 #pragma unroll
-            for (int h = 0; h < 7; ++h)
-                if (m & (1u << h)) v ^= y[h];
-            dst[(q >> 1) * half * ld_out + (q & 1) * hw] = v;
+                for (int h = 0; h < 7; ++h)
+                    if (m.m[q] & (1u << h)) v = W::x(v, y[h]);
+                *reinterpret_cast<T*>(base + (q >> 1) * g.ls * ld_out + (q & 1) * g.ws) = v;
+            }
+        } else {
+            const uint64_t* src = in + (p * 49) * bs_in + r * ld_in + w;
+            T acc[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] = W::zero();
+#pragma unroll 1
+            for (int h = 0; h < 7; ++h) {  // rolled: 7 loads in flight per step, acc stays in registers
+                T y[7];
+#pragma unroll
+                for (int h2 = 0; h2 < 7; ++h2) y[h2] = *reinterpret_cast<const T*>(src + (h * 7 + h2) * bs_in);
+                T c[4];  // sub-quadrants of compressed child h
+#pragma unroll
+                for (int q2 = 0; q2 < 4; ++q2) {
+                    T v = W::zero();
+#pragma unroll
+                    for (int h2 = 0; h2 < 7; ++h2)
+                        if (m.m[q2] & (1u << h2)) v = W::x(v, y[h2]);
+                    c[q2] = v;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (m.m[q] & (1u << h))
+#pragma unroll
+                        for (int q2 = 0; q2 < 4; ++q2) acc[4 * q + q2] = W::x(acc[4 * q + q2], c[q2]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int q2 = 0; q2 < 4; ++q2)
+                    *reinterpret_cast<T*>(base + ((q >> 1) * 2 + (q2 >> 1)) * g.ls * ld_out +
+                                          ((q & 1) * 2 + (q2 & 1)) * g.ws) = acc[4 * q + q2];
         }
     }
 }
@@ -149,38 +227,103 @@ unsigned grid_for(uint64_t total) {
 // sigma: quadrant index of B (2j + k) <-> quadrant index of Bt (2k + j).
 inline int sigma(int q) { return ((q & 1) << 1) | (q >> 1); }
 
-Steps make_steps(const InPlaceStep* st, int n, bool transposed) {
-    Steps s{};
-    s.n = n;
-    for (int i = 0; i < n; ++i) {
-        s.t[i] = uint8_t(transposed ? sigma(st[i].target) : st[i].target);
-        s.s[i] = uint8_t(transposed ? sigma(st[i].source) : st[i].source);
-    }
-    return s;
+// Linear map of an in-place program (x[t] ^= x[s] in order): bit q2 of row q says
+// that the new x[q] contains the old x[q2].
+void program_map(const InPlaceStep* st, int n, uint32_t (&f)[4]) {
+    for (int q = 0; q < 4; ++q) f[q] = 1u << q;
+    for (int i = 0; i < n; ++i) f[st[i].target] ^= f[st[i].source];
 }
 
-Masks7 make_expand(const char* const rows[7], bool transposed) {
+// alpha . phi (or beta . psi): the expand coefficients with the operand's basis change
+// folded in; B's quadrant indices are mapped to Bt's through sigma when `transposed`.
+Masks7 fused_expand(const char* const rows[7], const InPlaceStep* st, int n_st, bool transposed) {
+    uint32_t f[4];
+    program_map(st, n_st, f);
     Masks7 m{};
     for (int h = 0; h < 7; ++h) {
         const uint32_t r = row_mask(rows[h]);
+        uint32_t comb = 0;
+        for (int q = 0; q < 4; ++q)
+            if (r & (1u << q)) comb ^= f[q];
         uint32_t out = 0;
         for (int t = 0; t < 4; ++t)
-            if (r & (1u << (transposed ? sigma(t) : t))) out |= 1u << t;
+            if (comb & (1u << (transposed ? sigma(t) : t))) out |= 1u << t;
         m.m[h] = uint8_t(out);
     }
     return m;
 }
 
-int launch_basis_change(uint64_t* M, uint64_t ld, uint64_t n, int levels, const Steps& steps, cudaStream_t s) {
-    if (steps.n == 0) return kOk;
-    for (int l = 0; l < levels; ++l) {
-        const uint64_t sub = 1ull << l, L = n >> l;
-        const uint64_t total = sub * sub * (L / 2) * (L / 128);
-        basis_change_kernel<<<grid_for(total), 256, 0, s>>>(M, ld, sub, L, steps);
-        count_launch();
-        BMMGPU_CUDA_TRY(cudaGetLastError());
+// chi . gamma: the compress coefficients with the output basis change folded in.
+Masks4 fused_compress(const Scheme* sc) {
+    uint32_t x[4];
+    program_map(sc->chi, sc->n_chi, x);
+    Masks4 m{};
+    for (int q = 0; q < 4; ++q) {
+        uint32_t g = 0;
+        for (int q2 = 0; q2 < 4; ++q2)
+            if (x[q] & (1u << q2)) g ^= row_mask(sc->gamma[q2]);
+        m.m[q] = uint8_t(g);
     }
+    return m;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+PassGeom pass_geom(uint64_t L, int D, int V) {
+    const uint64_t ls = L >> D, ws = ls / 64;
+    return PassGeom{uint32_t(__builtin_ctzll(ws / V)), uint32_t(__builtin_ctzll(ls)), ls, ws};
+}
+
+int launch_expand(int D, const uint64_t* in, uint64_t ld_in, uint64_t bs_in, uint64_t P, uint64_t L, uint64_t* out,
+                  uint64_t ld_out, uint64_t bs_out, const Masks7& m, cudaStream_t s) {
+    const uint64_t ws = (L >> D) / 64;
+    const int V = (ws % 2 == 0 && ld_in % 2 == 0 && ld_out % 2 == 0 && bs_in % 2 == 0 && bs_out % 2 == 0 &&
+                   aligned16(in) && aligned16(out))
+                      ? 2
+                      : 1;
+    const PassGeom g = pass_geom(L, D, V);
+    const uint64_t total = P * g.ls * (ws / V);
+    const unsigned grid = grid_for(total);
+    if (D == 1 && V == 1) expand_pass_kernel<1, 1><<<grid, 256, 0, s>>>(in, ld_in, bs_in, total, g, out, ld_out, bs_out, m);
+    if (D == 1 && V == 2) expand_pass_kernel<1, 2><<<grid, 256, 0, s>>>(in, ld_in, bs_in, total, g, out, ld_out, bs_out, m);
+    if (D == 2 && V == 1) expand_pass_kernel<2, 1><<<grid, 256, 0, s>>>(in, ld_in, bs_in, total, g, out, ld_out, bs_out, m);
+    if (D == 2 && V == 2) expand_pass_kernel<2, 2><<<grid, 256, 0, s>>>(in, ld_in, bs_in, total, g, out, ld_out, bs_out, m);
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaGetLastError());
     return kOk;
+}
+
+#ifndef BMMGPU_COMPRESS_V
+#define BMMGPU_COMPRESS_V 2
+#endif
+int launch_compress(int D, const uint64_t* in, uint64_t ld_in, uint64_t bs_in, uint64_t P, uint64_t L, uint64_t* out,
+                    uint64_t ld_out, uint64_t bs_out, const Masks4& m, cudaStream_t s) {
+    const uint64_t ws = (L >> D) / 64;
+    const int V = (BMMGPU_COMPRESS_V == 2 && ws % 2 == 0 && ld_in % 2 == 0 && ld_out % 2 == 0 && bs_in % 2 == 0 && bs_out % 2 == 0 &&
+                   aligned16(in) && aligned16(out))
+                      ? 2
+                      : 1;
+    const PassGeom g = pass_geom(L, D, V);
+    const uint64_t total = P * g.ls * (ws / V);
+    const unsigned grid = grid_for(total);
+    if (D == 1 && V == 1) compress_pass_kernel<1, 1><<<grid, 256, 0, s>>>(in, ld_in, bs_in, total, g, out, ld_out, bs_out, m);
+    if (D == 1 && V == 2) compress_pass_kernel<1, 2><<<grid, 256, 0, s>>>(in, ld_in, bs_in, total, g, out, ld_out, bs_out, m);
+    if (D == 2 && V == 1) compress_pass_kernel<2, 1><<<grid, 256, 0, s>>>(in, ld_in, bs_in, total, g, out, ld_out, bs_out, m);
+    if (D == 2 && V == 2) compress_pass_kernel<2, 2><<<grid, 256, 0, s>>>(in, ld_in, bs_in, total, g, out, ld_out, bs_out, m);
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaGetLastError());
+    return kOk;
+}
+
+// Levels at which the breadth-first part materialises arrays: 0, then (e odd) 1, then
+// every second level up to e.  The one single-level step sits at the top, where the
+// arrays are smallest.
+std::vector<int> pass_levels(int e) {
+    std::vector<int> lv{0};
+    int l = 0;
+    if (e % 2) lv.push_back(l = 1);
+    while (l < e) lv.push_back(l += 2);
+    return lv;
 }
 
 using DevMem = DeviceBuffer;  // stream-ordered, pool-cached (common.cuh)
@@ -195,9 +338,9 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
     int st;
     if (e == 0)
         return launch_cubic(kernel, dA, lda, dBt, ldbt, dC, ldc, n, n, n / 64, true, false, s, 1, 0, 0, 0);
-    const Masks7 ma = make_expand(sc->alpha, false), mb = make_expand(sc->beta, true);
-    Masks4 mg{};
-    for (int q = 0; q < 4; ++q) mg.m[q] = uint8_t(row_mask(sc->gamma[q]));
+    const Masks7 ma = fused_expand(sc->alpha, sc->phi, sc->n_phi, false);
+    const Masks7 mb = fused_expand(sc->beta, sc->psi, sc->n_psi, true);
+    const Masks4 mg = fused_compress(sc);
 
     uint64_t gm, gn, gk;
     if ((st = granularity(kernel, &gm, &gn, &gk))) return st;
@@ -208,14 +351,17 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
     const uint64_t cwl = s_rows / 64;
     uint64_t batch = 1;
     for (int l = 0; l < e; ++l) batch *= 7;
+    auto pow7 = [](int l) {
+        uint64_t p = 1;
+        while (l-- > 0) p *= 7;
+        return p;
+    };
 
-    // Level buffers: intermediate levels 1..e-1 are plain row-major (stride
-    // L_l/64), level e uses the padded leaf panels.
+    // Level arrays: level 0 is the operand itself, intermediate levels are plain
+    // row-major (stride L_l/64), level e uses the padded leaf panels.
     std::vector<DevMem> T(e + 1), S(e + 1);
     std::vector<uint64_t> t_ld(e + 1), s_ld(e + 1), t_bs(e + 1), s_bs(e + 1);
-    uint64_t P = 1;
     for (int l = 1; l <= e; ++l) {
-        P *= 7;
         const uint64_t Ll = n >> l;
         if (l < e) {
             t_ld[l] = s_ld[l] = Ll / 64;
@@ -229,36 +375,32 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
     t_ld[0] = lda;
     s_ld[0] = ldbt;
     t_bs[0] = s_bs[0] = 0;
+    const std::vector<int> lv = pass_levels(e);
 
-    // Expand level by level, freeing each parent level once consumed.
+    // Expand, one or two levels per pass, freeing each parent level once consumed.
     const uint64_t* tin = dA;
     const uint64_t* sin = dBt;
-    P = 1;
-    for (int l = 0; l < e; ++l) {
-        const uint64_t Ll = n >> l;
-        const uint64_t Pn = P * 7;
-        const size_t tb = size_t(Pn * t_bs[l + 1] * 8), sb = size_t(Pn * s_bs[l + 1] * 8);
-        if ((st = T[l + 1].alloc(tb, s)) || (st = S[l + 1].alloc(sb, s))) return st;
-        if (l + 1 == e && (t_rows != L || s_rows != L || kwl != L / 64)) {
-            BMMGPU_CUDA_TRY(cudaMemsetAsync(T[l + 1].p, 0, tb, s));
-            BMMGPU_CUDA_TRY(cudaMemsetAsync(S[l + 1].p, 0, sb, s));
+    for (size_t i = 0; i + 1 < lv.size(); ++i) {
+        const int l0 = lv[i], l1 = lv[i + 1];
+        const uint64_t Pn = pow7(l1);
+        const size_t tb = size_t(Pn * t_bs[l1] * 8), sb = size_t(Pn * s_bs[l1] * 8);
+        if ((st = T[l1].alloc(tb, s)) || (st = S[l1].alloc(sb, s))) return st;
+        if (l1 == e && (t_rows != L || s_rows != L || kwl != L / 64)) {
+            BMMGPU_CUDA_TRY(cudaMemsetAsync(T[l1].p, 0, tb, s));
+            BMMGPU_CUDA_TRY(cudaMemsetAsync(S[l1].p, 0, sb, s));
             count_launch(2);
         }
-        const uint64_t total = P * (Ll / 2) * (Ll / 128);
-        expand_kernel<<<grid_for(total), 256, 0, s>>>(tin, t_ld[l], t_bs[l], P, Ll, T[l + 1].u(), t_ld[l + 1],
-                                                      t_bs[l + 1], ma);
-        expand_kernel<<<grid_for(total), 256, 0, s>>>(sin, s_ld[l], s_bs[l], P, Ll, S[l + 1].u(), s_ld[l + 1],
-                                                      s_bs[l + 1], mb);
-        count_launch(2);
-        BMMGPU_CUDA_TRY(cudaGetLastError());
-        if (l > 0) {
+        const uint64_t Ll = n >> l0, P = pow7(l0);
+        if ((st = launch_expand(l1 - l0, tin, t_ld[l0], t_bs[l0], P, Ll, T[l1].u(), t_ld[l1], t_bs[l1], ma, s)) ||
+            (st = launch_expand(l1 - l0, sin, s_ld[l0], s_bs[l0], P, Ll, S[l1].u(), s_ld[l1], s_bs[l1], mb, s)))
+            return st;
+        if (l0 > 0) {
             // parents no longer needed (stream-ordered free: no host sync)
-            T[l].release();
-            S[l].release();
+            T[l0].release();
+            S[l0].release();
         }
-        tin = T[l + 1].u();
-        sin = S[l + 1].u();
-        P = Pn;
+        tin = T[l1].u();
+        sin = S[l1].u();
     }
 
     // Leaves: 7^e batched block products, Q row-major (t_rows x cwl words each).
@@ -275,16 +417,15 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
     T[e].release();
     S[e].release();
 
-    // Compress level by level back into dC.
+    // Compress back up the same levels into dC.
     DevMem cur = std::move(Q), nxt;
     uint64_t cur_ld = cwl, cur_bs = q_bs;
-    P = batch;
-    for (int l = e - 1; l >= 0; --l) {
-        const uint64_t Ll = n >> l;
-        const uint64_t Pp = P / 7;
+    for (size_t i = lv.size() - 1; i > 0; --i) {
+        const int l1 = lv[i], l0 = lv[i - 1];
+        const uint64_t Ll = n >> l0, Pp = pow7(l0);
         uint64_t* out;
         uint64_t out_ld, out_bs;
-        if (l == 0) {
+        if (l0 == 0) {
             out = dC;
             out_ld = ldc;
             out_bs = 0;
@@ -294,14 +435,10 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
             if ((st = nxt.alloc(size_t(Pp * out_bs * 8), s))) return st;
             out = nxt.u();
         }
-        const uint64_t total = Pp * (Ll / 2) * (Ll / 128);
-        compress_kernel<<<grid_for(total), 256, 0, s>>>(cur.u(), cur_ld, cur_bs, Pp, Ll, out, out_ld, out_bs, mg);
-        count_launch();
-        BMMGPU_CUDA_TRY(cudaGetLastError());
+        if ((st = launch_compress(l1 - l0, cur.u(), cur_ld, cur_bs, Pp, Ll, out, out_ld, out_bs, mg, s))) return st;
         cur = std::move(nxt);
         cur_ld = out_ld;
         cur_bs = out_bs;
-        P = Pp;
     }
     return kOk;
 }
@@ -355,7 +492,9 @@ int alt_serial(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t l
                uint64_t n, const Scheme* sc, int e_serial, int e_par, int kernel, cudaStream_t s) {
     if (e_serial == 0) return alt_breadth(dA, lda, dBt, ldbt, dC, ldc, n, sc, e_par, kernel, s);
     const uint64_t half = n / 2, hw = half / 64;
-    const Masks7 ma = make_expand(sc->alpha, false), mb = make_expand(sc->beta, true);
+    const Masks7 ma = fused_expand(sc->alpha, sc->phi, sc->n_phi, false);
+    const Masks7 mb = fused_expand(sc->beta, sc->psi, sc->n_psi, true);
+    const Masks4 mg = fused_compress(sc);
     int st;
     BMMGPU_CUDA_TRY(cudaMemset2DAsync(dC, ldc * 8, 0, (n / 64) * 8, n, s));
     count_launch();
@@ -371,7 +510,7 @@ int alt_serial(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t l
         if ((st = alt_serial(T.u(), hw, S.u(), hw, Q.u(), hw, half, sc, e_serial - 1, e_par, kernel, s))) return st;
         uint32_t cmask = 0;
         for (int q = 0; q < 4; ++q)
-            if (row_mask(sc->gamma[q]) & (1u << h)) cmask |= 1u << q;
+            if (mg.m[q] & (1u << h)) cmask |= 1u << q;
         scatter_xor_kernel<<<grid_for(total), 256, 0, s>>>(Q.u(), hw, n, dC, ldc, cmask);
         count_launch();
         BMMGPU_CUDA_TRY(cudaGetLastError());
@@ -380,27 +519,22 @@ int alt_serial(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t l
 }
 
 // Device-resident fast product: dA (n x n/64, stride lda), dBt (Bt of B, n x
-// n/64, stride ldbt), dC (n x n/64, stride ldc).  dA and dBt are CLOBBERED
-// (basis-changed in place).  e recursion levels (leaves of size n >> e), the
-// top e_serial of them depth-first.
-int alt_multiply_device(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
-                        uint64_t n, int algo, int e, int e_serial, int kernel, cudaStream_t s) {
+// n/64, stride ldbt), dC (n x n/64, stride ldc).  e recursion levels (leaves of
+// size n >> e), the top e_serial of them depth-first.  The reference's basis changes
+// (phi / psi on the operands, chi on the result, engine.cpp:371-380) are folded into
+// the expand / compress coefficients, so dA and dBt are only read.
+int alt_multiply_device(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
+                        uint64_t ldc, uint64_t n, int algo, int e, int e_serial, int kernel, cudaStream_t s) {
     const Scheme* sc = scheme_for(algo);
     if (!sc) {
         set_error("no bilinear scheme for this algorithm");
         return kEinval;
     }
-    int st;
     if (e < 1 || (n >> e) < 64 || e_serial < 0 || e_serial > e) {
         set_error("alt_multiply_device: need 1 <= e, 0 <= e_serial <= e and leaves of at least 64 bits");
         return kEinval;
     }
-    // phi on A, psi on B (seen through Bt) over the top e levels (reference engine.cpp:371-374).
-    if ((st = launch_basis_change(dA, lda, n, e, make_steps(sc->phi, sc->n_phi, false), s))) return st;
-    if ((st = launch_basis_change(dBt, ldbt, n, e, make_steps(sc->psi, sc->n_psi, true), s))) return st;
-    if ((st = alt_serial(dA, lda, dBt, ldbt, dC, ldc, n, sc, e_serial, e - e_serial, kernel, s))) return st;
-    // chi on C over the top e levels (reference engine.cpp:379-380).
-    return launch_basis_change(dC, ldc, n, e, make_steps(sc->chi, sc->n_chi, false), s);
+    return alt_serial(dA, lda, dBt, ldbt, dC, ldc, n, sc, e_serial, e - e_serial, kernel, s);
 }
 
 // Depth-first levels needed so the breadth-first part fits in `budget` bytes:

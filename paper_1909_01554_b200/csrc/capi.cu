@@ -276,6 +276,29 @@ int bmmgpu_dev_cubic(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint
                         accumulate != 0, static_cast<cudaStream_t>(stream), 1, 0, 0, 0);
 }
 
+int bmmgpu_dev_cubic_batched(const uint64_t* dA, uint64_t lda, uint64_t sA, const uint64_t* dBt, uint64_t ldbt,
+                             uint64_t sB, uint64_t* dC, uint64_t ldc, uint64_t sC, uint64_t batch, uint64_t m_pad,
+                             uint64_t n_pad, uint64_t kw, int32_t semiring, int32_t kernel, int32_t accumulate,
+                             void* stream) {
+    if (semiring != BMMGPU_BOOLEAN_OR_AND && semiring != BMMGPU_GF2_XOR_AND) {
+        set_error("unknown semiring");
+        return kEinval;
+    }
+    if (batch > 1 && (sA < m_pad * lda || sB < n_pad * ldbt || sC < m_pad * ldc)) {
+        set_error("batched product: batch strides smaller than one panel");
+        return kEinval;
+    }
+    // the kernels take at most 65535 products per launch (grid.y / tile-id range)
+    for (uint64_t b0 = 0; b0 < batch; b0 += 65535) {
+        const uint64_t nb = std::min<uint64_t>(65535, batch - b0);
+        const int st = launch_cubic(kernel, dA + b0 * sA, lda, dBt + b0 * sB, ldbt, dC + b0 * sC, ldc, m_pad, n_pad,
+                                    kw, semiring == BMMGPU_GF2_XOR_AND, accumulate != 0,
+                                    static_cast<cudaStream_t>(stream), nb, sA, sB, sC);
+        if (st) return st;
+    }
+    return kOk;
+}
+
 int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, uint64_t k, uint64_t n,
                  int32_t semiring, const bmmgpu_opts* opts) {
     g_launches.store(0);

@@ -138,7 +138,11 @@ __device__ unsigned long long g_probe[2 * P_MAX_PAIRS * 8];
 #endif
 
 #ifndef BMMGPU_EPI_SLEEP
-#define BMMGPU_EPI_SLEEP 512  // ns the epilogue warps sleep between polls of acc_full (0: spin)
+#define BMMGPU_EPI_SLEEP 512  // ns the epilogue warps sleep between polls of acc_full on long tiles
+#endif
+
+#ifndef BMMGPU_DRAIN_GROUP
+#define BMMGPU_DRAIN_GROUP 1  // x16 TMEM loads per drain phase
 #endif
 
 #ifndef BMMGPU_RASTER_GROUP
@@ -178,13 +182,87 @@ __device__ __forceinline__ void expand_store_sw128(uint8_t* region, int r, int g
     *reinterpret_cast<uint4*>(row + (((j0 + 3) ^ rr) << 4)) = make_uint4(y.x & M1, y.y & M1, y.z & M1, y.w & M1);
 }
 
+// 16 accumulator counts (fp32, exact integers) -> 16 output bits: the count's parity
+// (GF(2); adding 2^23 puts the integer's LSB at mantissa bit 0) or its non-zeroness.
+template <bool kGf2>
+__device__ __forceinline__ uint32_t pack_counts16(const uint32_t (&v)[16]) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (kGf2)
+            w |= (__float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 1u) << j;
+        else
+            w |= uint32_t(v[j] != 0u) << j;
+    }
+    return w;
+}
+
+// The epilogue warp's 32 lanes x 256 columns of the accumulator -> 8 words per lane,
+// 16 columns per TMEM load with two register buffers: chunk c + 1 is in flight while
+// chunk c is packed, and the accumulator is released to the leader's MMA lane as soon
+// as the last chunk has landed.  Short-K tiles (the 4096-bit leaves of the fast
+// recursion) wait on this drain.
+template <bool kGf2>
+__device__ __forceinline__ void drain_accumulator(uint32_t tbase, uint32_t (&words)[8], uint32_t acc_empty_leader,
+                                                  uint32_t lane) {
+#if BMMGPU_DRAIN_GROUP == 2
+    // two x16 loads (one 32-column word) per phase, the next word's loads in flight while
+    // this word is packed
+    uint32_t va[16], vb[16], vc[16], vd[16];
+    umma::tmem_ld16(tbase, va);
+    umma::tmem_ld16(tbase + 16, vb);
+    umma::tmem_ld_wait_regs16(va);
+    umma::tmem_ld_wait_regs16(vb);
+#pragma unroll
+    for (int c = 0; c < 8; c += 2) {
+        umma::tmem_ld16(tbase + 32 * (c + 1), vc);
+        umma::tmem_ld16(tbase + 32 * (c + 1) + 16, vd);
+        words[c] = pack_counts16<kGf2>(va) | (pack_counts16<kGf2>(vb) << 16);
+        umma::tmem_ld_wait_regs16(vc);
+        umma::tmem_ld_wait_regs16(vd);
+        if (c + 2 < 8) {
+            umma::tmem_ld16(tbase + 32 * (c + 2), va);
+            umma::tmem_ld16(tbase + 32 * (c + 2) + 16, vb);
+        } else {
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
+        }
+        words[c + 1] = pack_counts16<kGf2>(vc) | (pack_counts16<kGf2>(vd) << 16);
+        if (c + 2 < 8) {
+            umma::tmem_ld_wait_regs16(va);
+            umma::tmem_ld_wait_regs16(vb);
+        }
+    }
+#else
+    uint32_t va[16], vb[16];
+    umma::tmem_ld16(tbase, va);
+    umma::tmem_ld_wait_regs16(va);
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) {
+        umma::tmem_ld16(tbase + 16 * (c + 1), vb);
+        const uint32_t lo = pack_counts16<kGf2>(va);
+        umma::tmem_ld_wait_regs16(vb);
+        if (c + 2 < 16) {
+            umma::tmem_ld16(tbase + 16 * (c + 2), va);
+        } else {
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
+        }
+        words[c >> 1] = lo | (pack_counts16<kGf2>(vb) << 16);
+        if (c + 2 < 16) umma::tmem_ld_wait_regs16(va);
+    }
+#endif
+}
+
 // kTma: the packed superstages arrive by TMA (one 3-D tiled box per operand, 128-byte
 // swizzle, K tail zero-filled by the bounds check) instead of the cp.async loader warps.
 template <bool kTma>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     cubic_umma2_kernel(const uint64_t* __restrict__ A, uint64_t lda, const uint64_t* __restrict__ Bt, uint64_t ldbt,
                        uint64_t* __restrict__ C, uint64_t ldc, uint64_t kw, int flags, TileMap map,
-                       uint32_t total_tiles, const __grid_constant__ CUtensorMap tmA,
+                       uint32_t total_tiles, uint32_t epi_sleep_ns, const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB) {
     extern __shared__ uint8_t smem_raw[];
     // semiring as a runtime flag: one compiled main loop serves both (a template
@@ -424,30 +502,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             map.decode(t, b, tm, tn);
             uint32_t words[8];
             if (n_stages > 0) {
-                if (BMMGPU_EPI_SLEEP > 0)
-                    umma::mbar_wait_sleep(&acc_full_bar, local & 1, BMMGPU_EPI_SLEEP);
+                if (epi_sleep_ns > 0)
+                    umma::mbar_wait_sleep(&acc_full_bar, local & 1, epi_sleep_ns);
                 else
                     umma::mbar_wait(&acc_full_bar, local & 1);
                 umma::fence_after_sync();
-#pragma unroll 1
-                for (int c = 0; c < 8; ++c) {
-                    uint32_t v[32];
-                    umma::tmem_ld32(tmem + ((quarter * 32) << 16) + 32 * c, v);
-                    umma::tmem_ld_wait();
-                    uint32_t w = 0;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        if (kGf2)
-                            w |= (__float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 1u) << j;
-                        else
-                            w |= uint32_t(v[j] != 0u) << j;
-                    }
-                    words[c] = w;
-                }
-                // accumulator fully read: hand it back to the leader's MMA lane
-                umma::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
+                // Drain 8 chunks of 32 columns with two register buffers: chunk c + 1 is in
+                // flight while chunk c is packed, and the accumulator goes back to the MMA
+                // lane as soon as the last chunk has landed (before it is packed).  Short-K
+                // tiles (the 4096-bit leaves of the fast recursion) wait on this drain.
+                const uint32_t tbase = tmem + ((quarter * 32) << 16);
+                if (kGf2)
+                    drain_accumulator<true>(tbase, words, acc_empty_leader, lane);
+                else
+                    drain_accumulator<false>(tbase, words, acc_empty_leader, lane);
             } else {
 #pragma unroll
                 for (int c = 0; c < 8; ++c) words[c] = 0;
@@ -569,8 +637,14 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
     const char* probe = getenv("BMMGPU_UMMA_PROBE");
     const int flags = (accumulate ? 1 : 0) | (gf2 ? 2 : 0) | (getenv("BMMGPU_UMMA_TRACE") ? 16 : 0) |
                       (probe && *probe ? 32 * atoi(probe) : 0);
+    // Epilogue warps poll acc_full with this sleep between tries: long tiles (K of tens of
+    // thousands of bits) leave them idle for ~100 us and their spinning would steal issue
+    // slots from the expanders; for short tiles the sleep granularity is pure bubble.
+    const uint64_t n_stages = kw * 64 / P_KBITS;
+    uint32_t epi_sleep = n_stages >= 128 ? BMMGPU_EPI_SLEEP : n_stages >= 32 ? 64 : 0;
+    if (const char* es = getenv("BMMGPU_EPI_SLEEP_NS")) epi_sleep = uint32_t(atoi(es));
     kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw, flags, map,
-                                                             uint32_t(total), tmA, tmB);
+                                                             uint32_t(total), epi_sleep, tmA, tmB);
     count_launch();
     BMMGPU_CUDA_TRY(cudaGetLastError());
     return kOk;

@@ -4,54 +4,77 @@
 // "copy B and transpose_blocks64" step (engine.cpp:65-66, bitmatrix.cpp:97-110)
 // fused with the block-position transpose the dot-product form needs.
 //
-// HBM-bound: 16 B read + 16 B written per 128 bits... per 64x64 block 512 B in,
-// 512 B out.  A CTA stages a 256-row x 4-word tile through shared memory so
-// both the loads and the stores move whole 32-byte sectors.
+// HBM-bound: per 64x64 block 512 B in, 512 B out.  A CTA of 8 warps stages an
+// 8 x 8 grid of blocks (512 K rows x 8 words of B) through shared memory: warp w
+// loads K block w of the tile (64 B per row, 16-byte loads) and transposes each of
+// its 8 blocks with shuffles, then writes N block w of the tile as 64 contiguous
+// bytes per Bt row (16-byte stores).
 #include "common.cuh"
 
 namespace bmmgpu {
 
 namespace {
 
-constexpr int TB_K = 4;  // 64-row blocks of B (K direction) per CTA
-constexpr int TB_N = 4;  // 64-bit words of a B row (N direction) per CTA
+constexpr int TB = 8;  // blocks per tile side: 8 K blocks (512 rows) x 8 words (512 columns)
 
-__global__ void __launch_bounds__(128) transpose_kernel(const uint64_t* __restrict__ B, uint64_t ldb, uint64_t k,
-                                                        uint64_t n, uint64_t* __restrict__ Bt, uint64_t kw) {
-    __shared__ uint64_t tile[TB_N][TB_K][64];
+__global__ void __launch_bounds__(256) transpose_kernel(const uint64_t* __restrict__ B, uint64_t ldb, uint64_t k,
+                                                        uint64_t n, uint64_t* __restrict__ Bt, uint64_t n_pad,
+                                                        uint64_t kw) {
+    __shared__ uint64_t tile[TB][TB][64];  // [N block][K block][row of the transposed block]
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t nb_words = (n + 63) / 64;
-    const uint64_t bk = blockIdx.y * TB_K + warp;  // K block this warp loads
-    const uint64_t bj0 = blockIdx.x * TB_N;        // first N word of the tile
-    // Load rows bk*64 + lane (+32), words bj0..bj0+3, and transpose each block.
-    uint64_t x0[TB_N], x1[TB_N];
+    const uint64_t bk = blockIdx.y * uint64_t(TB) + warp;  // K block this warp loads
+    const uint64_t bj0 = blockIdx.x * uint64_t(TB);        // first N word of the tile
+    const uint64_t r0 = bk * 64 + lane, r1 = r0 + 32;
+    uint64_t x0[TB], x1[TB];
+    const bool fast = (ldb % 2 == 0) && bj0 + TB <= nb_words && r1 < k && (n & 63) == 0;
+    if (fast) {
+        const ulonglong2* p0 = reinterpret_cast<const ulonglong2*>(B + r0 * ldb + bj0);
+        const ulonglong2* p1 = reinterpret_cast<const ulonglong2*>(B + r1 * ldb + bj0);
 #pragma unroll
-    for (int b = 0; b < TB_N; ++b) {
-        const uint64_t bj = bj0 + b;
-        const uint64_t r0 = bk * 64 + lane, r1 = r0 + 32;
-        uint64_t mask = ~0ull;
-        if (bj == nb_words - 1 && (n & 63)) mask = (1ull << (n & 63)) - 1;
-        x0[b] = (bj < nb_words && r0 < k) ? (B[r0 * ldb + bj] & mask) : 0ull;
-        x1[b] = (bj < nb_words && r1 < k) ? (B[r1 * ldb + bj] & mask) : 0ull;
+        for (int b = 0; b < TB / 2; ++b) {
+            const ulonglong2 u = p0[b], v = p1[b];
+            x0[2 * b] = u.x;
+            x0[2 * b + 1] = u.y;
+            x1[2 * b] = v.x;
+            x1[2 * b + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int b = 0; b < TB; ++b) {
+            const uint64_t bj = bj0 + b;
+            uint64_t mask = ~0ull;
+            if (bj == nb_words - 1 && (n & 63)) mask = (1ull << (n & 63)) - 1;
+            x0[b] = (bj < nb_words && r0 < k) ? (B[r0 * ldb + bj] & mask) : 0ull;
+            x1[b] = (bj < nb_words && r1 < k) ? (B[r1 * ldb + bj] & mask) : 0ull;
+        }
     }
 #pragma unroll
-    for (int b = 0; b < TB_N; ++b) {
+    for (int b = 0; b < TB; ++b) {
         warp_transpose64(x0[b], x1[b], lane);
         tile[b][warp][lane] = x0[b];
         tile[b][warp][lane + 32] = x1[b];
     }
     __syncthreads();
-    // Warp w now writes N block bj0 + w: rows (bj0+w)*64 + lane (+32), K words
-    // blockIdx.y*4 .. +3 (32 contiguous bytes per row).
-    const uint64_t row0 = (bj0 + warp) * 64 + lane;
-    const uint64_t kw0 = blockIdx.y * TB_K;
+    // Warp w writes N block bj0 + w: rows (bj0+w)*64 + lane (+32), K words
+    // blockIdx.y*8 .. +7 (64 contiguous bytes per row).
+    const uint64_t kw0 = blockIdx.y * uint64_t(TB);
+    const bool vec = (kw % 2 == 0) && kw0 + TB <= kw;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        const uint64_t row = row0 + 32 * h;
+        const uint64_t row = (bj0 + warp) * 64 + lane + 32 * h;
+        if (row >= n_pad) continue;
         uint64_t* dst = Bt + row * kw + kw0;
+        if (vec) {
 #pragma unroll
-        for (int kb = 0; kb < TB_K; ++kb)
-            if (kw0 + kb < kw) dst[kb] = tile[warp][kb][lane + 32 * h];
+            for (int kb = 0; kb < TB; kb += 2)
+                *reinterpret_cast<ulonglong2*>(dst + kb) =
+                    make_ulonglong2(tile[warp][kb][lane + 32 * h], tile[warp][kb + 1][lane + 32 * h]);
+        } else {
+#pragma unroll
+            for (int kb = 0; kb < TB; ++kb)
+                if (kw0 + kb < kw) dst[kb] = tile[warp][kb][lane + 32 * h];
+        }
     }
 }
 
@@ -61,13 +84,13 @@ __global__ void __launch_bounds__(128) transpose_kernel(const uint64_t* __restri
 // ceil(k/64) come out zero.
 int launch_transpose(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
                      uint64_t kw, cudaStream_t stream) {
-    if (n_pad % (TB_N * 64) != 0 || n_pad < n || kw * 64 < k) {
+    if (n_pad % 256 != 0 || n_pad < n || kw * 64 < k) {
         set_error("bmmgpu_dev_transpose: n_pad must be a multiple of 256 covering n, kw*64 must cover k");
         return kEinval;
     }
     if (n_pad == 0 || kw == 0) return kOk;
-    dim3 grid(static_cast<unsigned>(n_pad / (TB_N * 64)), static_cast<unsigned>(ceil_div(kw, TB_K)));
-    transpose_kernel<<<grid, 128, 0, stream>>>(dB, ldb, k, n, dBt, kw);
+    dim3 grid(static_cast<unsigned>(ceil_div(n_pad, TB * 64)), static_cast<unsigned>(ceil_div(kw, TB)));
+    transpose_kernel<<<grid, 256, 0, stream>>>(dB, ldb, k, n, dBt, n_pad, kw);
     count_launch();
     BMMGPU_CUDA_TRY(cudaGetLastError());
     return kOk;

@@ -117,3 +117,34 @@ def test_depth_first_levels_match_reference(engine, oracle, golden, serial, monk
             got = bmm.multiply(a, b, bmm.Algo(c["algo"]), _plan(bmm, c["plan"]), bmm.Semiring.Gf2XorAnd,
                                leaf_log2=leaf)
             assert f"{oracle.fnv1a64(got.words):016x}" == c["fnv"], (c, leaf, serial)
+
+
+@pytest.mark.parametrize("leaf", [6, 7, 8])
+def test_device_fast_product_reads_operands_only(engine, oracle, leaf):
+    """bmmgpu_dev_multiply on torch-owned HBM: equal to the cubic product for every
+    scheme, and dA / dBt come back unchanged (the basis changes are folded into the
+    expand / compress coefficients, not applied in place)."""
+    import ctypes
+
+    import torch
+    bmm = engine
+    lib = bmm.lib()
+    n = 1024
+    a = oracle.random(n, n, 71)
+    b = oracle.random(n, n, 72)
+    want = oracle.multiply_cubic(a, b, n, n, n, GF2)
+    w = n // 64
+    dA = torch.from_numpy(a.view(np.int64).reshape(n, w).copy()).cuda()
+    dB = torch.from_numpy(b.view(np.int64).reshape(n, w).copy()).cuda()
+    dBt = torch.empty((n, w), dtype=torch.int64, device="cuda")
+    dC = torch.empty((n, w), dtype=torch.int64, device="cuda")
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.bmmgpu_dev_transpose(dB.data_ptr(), w, n, n, dBt.data_ptr(), n, w, stream) == 0
+    bt0 = dBt.clone()
+    for algo in (1, 2, 3):
+        assert lib.bmmgpu_dev_multiply(dA.data_ptr(), w, dBt.data_ptr(), w, dC.data_ptr(), w, n, algo, leaf, 0,
+                                       stream) == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(dC.cpu().numpy().view(np.uint64).ravel(), want), (algo, leaf)
+        assert np.array_equal(dA.cpu().numpy().view(np.uint64).ravel(), a)
+        assert torch.equal(dBt, bt0)

@@ -184,3 +184,34 @@ def test_umma_pair_loaders(engine, oracle, monkeypatch, loader):
             got = bmm.multiply_cubic(a, b, bmm.Semiring(ring), kernel=2)
             want = oracle.multiply_cubic(a.words, b.words, m, k, n, ring)
             assert np.array_equal(got.words, want), (loader, m, k, n, ring)
+
+
+def test_device_api_batched(engine, oracle):
+    """bmmgpu_dev_cubic_batched: independent products in one launch, each equal to the
+    oracle's product of its own panels (the leaf layer of the fast recursion)."""
+    import torch
+    bmm = engine
+    lib = bmm.lib()
+    for kernel in KERNELS:
+        gm, gn, gk = bmm.granularity(kernel)
+        batch, L = 5, 512
+        m_pad, n_pad, kw = -(-L // gm) * gm, -(-L // gn) * gn, -(-L // gk) * gk // 64
+        As = [oracle.random(L, L, 200 + i) for i in range(batch)]
+        Bs = [oracle.random(L, L, 300 + i) for i in range(batch)]
+        dA = torch.zeros((batch, m_pad, kw), dtype=torch.int64, device="cuda")
+        dBt = torch.zeros((batch, n_pad, kw), dtype=torch.int64, device="cuda")
+        dC = torch.zeros((batch, m_pad, n_pad // 64), dtype=torch.int64, device="cuda")
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for i in range(batch):
+            dA[i, :L, : L // 64] = torch.from_numpy(As[i].view(np.int64).reshape(L, -1)).cuda()
+            dB = torch.from_numpy(Bs[i].view(np.int64)).cuda()
+            assert lib.bmmgpu_dev_transpose(dB.data_ptr(), L // 64, L, L, dBt[i].data_ptr(), n_pad, kw,
+                                            stream) == 0
+        for ring in (GF2, BOOL):
+            assert lib.bmmgpu_dev_cubic_batched(dA.data_ptr(), kw, m_pad * kw, dBt.data_ptr(), kw, n_pad * kw,
+                                                dC.data_ptr(), n_pad // 64, m_pad * (n_pad // 64), batch, m_pad,
+                                                n_pad, kw, ring, kernel, 0, stream) == 0
+            torch.cuda.synchronize()
+            for i in range(batch):
+                got = dC[i].cpu().numpy().view(np.uint64)[:L, : L // 64].ravel()
+                assert np.array_equal(got, oracle.multiply_cubic(As[i], Bs[i], L, L, L, ring)), (kernel, ring, i)
