@@ -69,9 +69,15 @@ constexpr int P_REGION = P_ROWS * 128;    // bytes of one operand per stage (16 
 constexpr int P_STAGE = 2 * P_REGION;
 constexpr int P_PRODUCERS = 256;          // expanders: two threads per row of A and of Bt
 constexpr int P_MMA_WARP = P_PRODUCERS / 32;
-constexpr int P_LOADER_WARP0 = P_MMA_WARP + 1 + 4;  // after the MMA warp and 4 epilogue warps
-constexpr int P_LOADERS = 64;
-constexpr int P_THREADS = P_PRODUCERS + 32 + 128 + P_LOADERS;
+#ifndef BMMGPU_EPI_WARPS
+#define BMMGPU_EPI_WARPS 4  // 8 measured no faster: the drain is TMEM-read bound, not issue bound
+#endif
+constexpr int P_EPI_WARPS = BMMGPU_EPI_WARPS;     // 4: one per TMEM lane quarter; 8: two, 128 columns each
+constexpr int P_EPI_COLS = 256 * 4 / P_EPI_WARPS;  // accumulator columns one epilogue warp drains
+static_assert(P_EPI_WARPS == 4 || P_EPI_WARPS == 8, "epilogue warps cover the 4 lane quarters evenly");
+constexpr int P_LOADER_WARP0 = P_MMA_WARP + 1 + P_EPI_WARPS;  // after the MMA warp and the epilogue warps
+constexpr int P_LOADERS = P_EPI_WARPS == 8 ? 32 : 64;  // cp.async loader threads (TMA: one lane)
+constexpr int P_THREADS = P_PRODUCERS + 32 + 32 * P_EPI_WARPS + P_LOADERS;
 #ifndef BMMGPU_SST_SLOTS
 #define BMMGPU_SST_SLOTS 2
 #endif
@@ -182,78 +188,59 @@ __device__ __forceinline__ void expand_store_sw128(uint8_t* region, int r, int g
     *reinterpret_cast<uint4*>(row + (((j0 + 3) ^ rr) << 4)) = make_uint4(y.x & M1, y.y & M1, y.z & M1, y.w & M1);
 }
 
-// 16 accumulator counts (fp32, exact integers) -> 16 output bits: the count's parity
-// (GF(2); adding 2^23 puts the integer's LSB at mantissa bit 0) or its non-zeroness.
+// The accumulator never starts from zero: it is preset to a bias (all MMAs accumulate)
+// so each output bit is a single bit of the fp32 word.  Counts c < 2^23 are exact:
+//   GF(2):   2^23 + c      -> the integer sits at mantissa bit 0, parity = bit 0;
+//   Boolean: 2^23 - 1 + c  -> c == 0 gives 8388607.0 (exponent 149, bit 23 set), c >= 1
+//            gives [2^23, 2^24) (exponent 150, bit 23 clear): non-zero = !bit 23.
+// Two instructions per output bit in the drain (shift + merge) instead of three.
+constexpr uint32_t kBiasGf2 = 0x4B000000u;   // 8388608.0f
+constexpr uint32_t kBiasBool = 0x4AFFFFFEu;  // 8388607.0f
+
 template <bool kGf2>
 __device__ __forceinline__ uint32_t pack_counts16(const uint32_t (&v)[16]) {
     uint32_t w = 0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (kGf2)
-            w |= (__float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 1u) << j;
+            w |= (v[j] & 1u) << j;
         else
-            w |= uint32_t(v[j] != 0u) << j;
+            w |= ((~v[j] >> 23) & 1u) << j;
     }
     return w;
 }
 
-// The epilogue warp's 32 lanes x 256 columns of the accumulator -> 8 words per lane,
+// The epilogue warp's 32 lanes x P_EPI_COLS columns of the accumulator -> words per lane,
 // 16 columns per TMEM load with two register buffers: chunk c + 1 is in flight while
-// chunk c is packed, and the accumulator is released to the leader's MMA lane as soon
-// as the last chunk has landed.  Short-K tiles (the 4096-bit leaves of the fast
-// recursion) wait on this drain.
+// chunk c is packed.  Each chunk is re-biased behind its load, and the accumulator goes
+// back to the leader's MMA lane as soon as the last chunk has landed.  Short-K tiles
+// (the 4096-bit leaves of the fast recursion) wait on this drain.
 template <bool kGf2>
-__device__ __forceinline__ void drain_accumulator(uint32_t tbase, uint32_t (&words)[8], uint32_t acc_empty_leader,
-                                                  uint32_t lane) {
-#if BMMGPU_DRAIN_GROUP == 2
-    // two x16 loads (one 32-column word) per phase, the next word's loads in flight while
-    // this word is packed
-    uint32_t va[16], vb[16], vc[16], vd[16];
-    umma::tmem_ld16(tbase, va);
-    umma::tmem_ld16(tbase + 16, vb);
-    umma::tmem_ld_wait_regs16(va);
-    umma::tmem_ld_wait_regs16(vb);
-#pragma unroll
-    for (int c = 0; c < 8; c += 2) {
-        umma::tmem_ld16(tbase + 32 * (c + 1), vc);
-        umma::tmem_ld16(tbase + 32 * (c + 1) + 16, vd);
-        words[c] = pack_counts16<kGf2>(va) | (pack_counts16<kGf2>(vb) << 16);
-        umma::tmem_ld_wait_regs16(vc);
-        umma::tmem_ld_wait_regs16(vd);
-        if (c + 2 < 8) {
-            umma::tmem_ld16(tbase + 32 * (c + 2), va);
-            umma::tmem_ld16(tbase + 32 * (c + 2) + 16, vb);
-        } else {
-            umma::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
-        }
-        words[c + 1] = pack_counts16<kGf2>(vc) | (pack_counts16<kGf2>(vd) << 16);
-        if (c + 2 < 8) {
-            umma::tmem_ld_wait_regs16(va);
-            umma::tmem_ld_wait_regs16(vb);
-        }
-    }
-#else
+__device__ __forceinline__ void drain_accumulator(uint32_t tbase, uint32_t (&words)[P_EPI_COLS / 32],
+                                                  uint32_t acc_empty_leader, uint32_t lane) {
+    constexpr int kChunks = P_EPI_COLS / 16;
+    const uint32_t bias = kGf2 ? kBiasGf2 : kBiasBool;
     uint32_t va[16], vb[16];
     umma::tmem_ld16(tbase, va);
     umma::tmem_ld_wait_regs16(va);
 #pragma unroll
-    for (int c = 0; c < 16; c += 2) {
+    for (int c = 0; c < kChunks; c += 2) {
         umma::tmem_ld16(tbase + 16 * (c + 1), vb);
+        umma::tmem_st16_fill(tbase + 16 * c, bias);
         const uint32_t lo = pack_counts16<kGf2>(va);
         umma::tmem_ld_wait_regs16(vb);
-        if (c + 2 < 16) {
+        umma::tmem_st16_fill(tbase + 16 * (c + 1), bias);
+        if (c + 2 < kChunks) {
             umma::tmem_ld16(tbase + 16 * (c + 2), va);
         } else {
+            umma::tmem_st_wait();
             umma::fence_before_sync();
             __syncwarp();
             if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
         }
         words[c >> 1] = lo | (pack_counts16<kGf2>(vb) << 16);
-        if (c + 2 < 16) umma::tmem_ld_wait_regs16(va);
+        if (c + 2 < kChunks) umma::tmem_ld_wait_regs16(va);
     }
-#endif
 }
 
 // kTma: the packed superstages arrive by TMA (one 3-D tiled box per operand, 128-byte
@@ -294,7 +281,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             umma::mbar_init(&pk_empty_bar[s], P_PRODUCERS / 32);  // every expander warp, every superstage
         }
         umma::mbar_init(&acc_full_bar, 1);
-        umma::mbar_init(&acc_empty_bar, 2 * 4);
+        umma::mbar_init(&acc_empty_bar, 2 * P_EPI_WARPS);
         umma::mbar_fence_init();
     }
     umma::fence_before_sync();
@@ -307,6 +294,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         for (int c = 0; c < 4; ++c) umma::tmem_st32_fill(tmem + lane_base + P_SF_EVEN + 32 * c, 0x7F7F7F7Fu);
 #pragma unroll
         for (int c = 0; c < 4; ++c) umma::tmem_st32_fill(tmem + lane_base + P_SF_ODD + 32 * c, 0x80808080u);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) umma::tmem_st32_fill(tmem + lane_base + 32 * c, kGf2 ? kBiasGf2 : kBiasBool);
         umma::tmem_st_wait();
     }
     umma::fence_before_sync();
@@ -391,7 +380,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #endif
             for (uint32_t t = pair; t < total_tiles; t += n_pairs, ++local) {
                 // the accumulator must have been drained by both CTAs' epilogues
+                // the tile's first stage is usually staged long before the accumulator comes
+                // back: wait for it first so the MMAs issue right after acc_empty
+                if (local > 0 && n_stages > 0) umma::mbar_wait(&full_bar[s], full_parity);
                 if (local > 0) PWAIT(4, umma::mbar_wait(&acc_empty_bar, (local - 1) & 1));
+                TRACE_AT(pair == 0 && lane == 0 && local < 512, 3072 + 4 * local + 3);
                 umma::fence_after_sync();
                 for (uint64_t k = 0; k < (PROBE(128) ? 0 : n_stages); ++k, ++it, s = (s + 1 == P_STAGES) ? (full_parity ^= 1, 0) : s + 1) {
                     PWAIT(3, umma::mbar_wait(&full_bar[s], full_parity));
@@ -406,7 +399,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                             const uint32_t sf = tmem + ((j & 1) ? P_SF_ODD : P_SF_EVEN);
                             if (PROBE(32)) continue;
                             // + 32 bytes per K = 64 step
-                            umma::mma_mxf4_pair(tmem, da0 + 2 * j, db0 + 2 * j, idesc, sf, sf, (k | j) ? 1u : 0u);
+                            // always accumulate: the epilogue presets the accumulator to the bias
+                            umma::mma_mxf4_pair(tmem, da0 + 2 * j, db0 + 2 * j, idesc, sf, sf, 1u);
                         }
                         umma::mma_commit_pair(&empty_bar[s], 0x3);
                     }
@@ -414,6 +408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                     TRACE_AT(pair == 0 && lane == 0 && it < 512, 512 + it);
                 }
                 if (umma::elect_one()) umma::mma_commit_pair(&acc_full_bar, 0x3);
+                TRACE_AT(pair == 0 && lane == 0 && local < 512, 3072 + 4 * local + 0);
                 __syncwarp();
             }
 #ifdef BMMGPU_PROBE
@@ -450,10 +445,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     } else if (warp >= P_LOADER_WARP0) {
         // ------------------------------------------------ loaders: packed bits global -> shared (cp.async)
         // Superstage slot: [A, Bt][row][128 bytes = 4 stages], 16-byte chunk c of row r at
-        // c ^ (r & 7).  Loader thread lt always moves chunk c = lt & 7 of rows (lt >> 3) + 8 i,
-        // so a warp instruction covers four whole 128-byte rows.
+        // c ^ (r & 7).  Loader thread lt always moves chunk c = lt & 7 of rows r0 + kStep i
+        // (r0 = lt >> 3, kStep = P_LOADERS / 8), so a warp instruction covers four whole
+        // 128-byte rows; with kStep = 4 the swizzle alternates between two row phases.
+        constexpr int kStep = P_LOADERS / 8;
         const uint32_t lt = tid - P_LOADER_WARP0 * 32, c = lt & 7, r0 = lt >> 3;
         uint8_t* pk = smem + size_t(P_STAGES) * P_STAGE + r0 * 128 + ((c ^ (r0 & 7)) << 4);
+        // offset of row r0 + kStep (second phase) relative to the first, within an 8-row atom
+        const int phase2 = kStep == 4 ? 4 * 128 + (int((c ^ ((r0 + 4) & 7)) << 4) - int((c ^ (r0 & 7)) << 4)) : 0;
         int slot = 0;
         uint32_t pk_empty_parity = 0;
         uint64_t qn = 0;  // superstages issued
@@ -469,6 +468,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             const uint8_t* gb = reinterpret_cast<const uint8_t*>(
                                     Bt + b * map.sB + (uint64_t(tn) * P_BN + rank * P_ROWS + r0) * ldbt) + c * 16;
             const uint64_t sa8 = 8 * lda * 8, sb8 = 8 * ldbt * 8;  // 8 rows further
+            const uint64_t sa4 = 4 * lda * 8, sb4 = 4 * ldbt * 8;  // 4 rows further
             for (uint64_t k0 = 0; k0 < n_stages; k0 += 4, ++qn) {
                 if (qn >= P_SST_SLOTS) PWAIT(6, umma::mbar_wait(&pk_empty_bar[slot], pk_empty_parity));
                 if (k0 + (c >> 1) < n_stages) {  // this chunk's stage exists
@@ -479,6 +479,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                     for (int i = 0; i < P_ROWS / 8; ++i) {
                         cp_async16(dst + i * 1024, pa + i * sa8);
                         cp_async16(dst + P_SST_OP + i * 1024, pb + i * sb8);
+                        if (kStep == 4) {
+                            cp_async16(dst + i * 1024 + phase2, pa + i * sa8 + sa4);
+                            cp_async16(dst + P_SST_OP + i * 1024 + phase2, pb + i * sb8 + sb4);
+                        }
                     }
                 }
                 umma::cp_async_mbar_arrive_noinc(&pk_full_bar[slot]);
@@ -493,49 +497,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #endif
         PSTORE(6, 7, lt == 0);
     } else {
-        // ------------------------------------------------ epilogue (warps 9-12)
+        // ------------------------------------------------ epilogue (warps 9 .. 8 + P_EPI_WARPS):
+        // warp w may access TMEM lanes 32 (w % 4) ..; with 8 warps each lane quarter has two,
+        // draining columns [0, 128) and [128, 256), which halves the drain the next tile's
+        // MMAs wait on.
+        constexpr int kWords = P_EPI_COLS / 32;
         const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const uint32_t half = (warp - (P_MMA_WARP + 1)) / 4;
         const uint32_t acc_empty_leader = umma::mapa_shared(smem_u32(&acc_empty_bar), 0);
         uint32_t local = 0;
         for (uint32_t t = pair; t < total_tiles; t += n_pairs, ++local) {
             uint32_t b, tm, tn;
             map.decode(t, b, tm, tn);
-            uint32_t words[8];
+            uint32_t words[kWords];
             if (n_stages > 0) {
                 if (epi_sleep_ns > 0)
                     umma::mbar_wait_sleep(&acc_full_bar, local & 1, epi_sleep_ns);
                 else
                     umma::mbar_wait(&acc_full_bar, local & 1);
                 umma::fence_after_sync();
-                // Drain 8 chunks of 32 columns with two register buffers: chunk c + 1 is in
-                // flight while chunk c is packed, and the accumulator goes back to the MMA
-                // lane as soon as the last chunk has landed (before it is packed).  Short-K
-                // tiles (the 4096-bit leaves of the fast recursion) wait on this drain.
-                const uint32_t tbase = tmem + ((quarter * 32) << 16);
+                TRACE_AT(pair == 0 && rank == 0 && quarter == 0 && half == 0 && lane == 0 && local < 512,
+                         3072 + 4 * local + 1);
+                const uint32_t tbase = tmem + ((quarter * 32) << 16) + half * P_EPI_COLS;
                 if (kGf2)
                     drain_accumulator<true>(tbase, words, acc_empty_leader, lane);
                 else
                     drain_accumulator<false>(tbase, words, acc_empty_leader, lane);
+                TRACE_AT(pair == 0 && rank == 0 && quarter == 0 && half == 0 && lane == 0 && local < 512,
+                         3072 + 4 * local + 2);
             } else {
 #pragma unroll
-                for (int c = 0; c < 8; ++c) words[c] = 0;
+                for (int c = 0; c < kWords; ++c) words[c] = 0;
             }
             const uint64_t row = uint64_t(tm) * P_BM + rank * P_ROWS + quarter * 32 + lane;
-            uint4* dst = reinterpret_cast<uint4*>(C + b * map.sC + row * ldc + uint64_t(tn) * (P_BN / 64));
-            uint4 w0 = make_uint4(words[0], words[1], words[2], words[3]);
-            uint4 w1 = make_uint4(words[4], words[5], words[6], words[7]);
-            if (accumulate) {
-                const uint4 o0 = dst[0], o1 = dst[1];
-                if (kGf2) {
-                    w0 = make_uint4(w0.x ^ o0.x, w0.y ^ o0.y, w0.z ^ o0.z, w0.w ^ o0.w);
-                    w1 = make_uint4(w1.x ^ o1.x, w1.y ^ o1.y, w1.z ^ o1.z, w1.w ^ o1.w);
-                } else {
-                    w0 = make_uint4(w0.x | o0.x, w0.y | o0.y, w0.z | o0.z, w0.w | o0.w);
-                    w1 = make_uint4(w1.x | o1.x, w1.y | o1.y, w1.z | o1.z, w1.w | o1.w);
+            uint4* dst = reinterpret_cast<uint4*>(C + b * map.sC + row * ldc + uint64_t(tn) * (P_BN / 64)) +
+                         half * (kWords / 4);
+#pragma unroll
+            for (int i = 0; i < kWords / 4; ++i) {
+                uint4 w = make_uint4(words[4 * i], words[4 * i + 1], words[4 * i + 2], words[4 * i + 3]);
+                if (accumulate) {
+                    const uint4 o = dst[i];
+                    if (kGf2)
+                        w = make_uint4(w.x ^ o.x, w.y ^ o.y, w.z ^ o.z, w.w ^ o.w);
+                    else
+                        w = make_uint4(w.x | o.x, w.y | o.y, w.z | o.z, w.w | o.w);
                 }
+                dst[i] = w;
             }
-            dst[0] = w0;
-            dst[1] = w1;
         }
     }
     umma::fence_before_sync();
@@ -608,8 +616,8 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
             }
         return kOk;
     }
-    if (kw * 64 > (1ull << 24)) {
-        set_error("umma2 kernel: K above 2^24 bits would exceed exact fp32 accumulation");
+    if (kw * 64 > (1ull << 23)) {
+        set_error("umma2 kernel: K above 2^23 bits would exceed exact biased fp32 accumulation");
         return kEinval;
     }
     const uint64_t m_tiles = m_pad / P_BM, n_tiles = n_pad / P_BN;
