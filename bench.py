@@ -270,9 +270,6 @@ def run_ours(args, dist: Dist) -> None:
     dC = torch.empty((m_pad, n_pad // 64), dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
 
-    kt0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + args.warmup)]
-    kt1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + args.warmup)]
-
     def check(rc: int) -> None:
         if rc != 0:
             raise RuntimeError(lib.bmmgpu_last_error().decode())
@@ -284,20 +281,19 @@ def run_ours(args, dist: Dist) -> None:
         before = lib.bmmgpu_last_launch_count()
         check(lib.bmmgpu_dev_transpose(dB.data_ptr(), w, n, n, dBt.data_ptr(), n_pad, kw, sp))
         if algo == 0:
-            kt0[i].record(stream)
             check(lib.bmmgpu_dev_cubic(dA.data_ptr(), kw, dBt.data_ptr(), kw, dC.data_ptr(), n_pad // 64, m_pad,
                                        n_pad, kw, ring, kernel, 0, sp))
-            kt1[i].record(stream)
         else:
-            kt0[i].record(stream)
             check(lib.bmmgpu_dev_multiply(dA.data_ptr(), kw, dBt.data_ptr(), kw, dC.data_ptr(), n_pad // 64, n,
                                           algo, args.leaf_log2, kernel, sp))
-            kt1[i].record(stream)
         launches_per_step = lib.bmmgpu_last_launch_count() - before
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
+    # bracket every block-product launch of the timed steps with events (the dominant
+    # kernel's device time, also inside the fast pipeline)
+    check(lib.bmmgpu_block_timer(1))
     visible = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip().isdigit()]
     sampler = ClockSampler(int(visible[dev]) if dev < len(visible) else dev)
     sampler.start()
@@ -311,9 +307,11 @@ def run_ours(args, dist: Dist) -> None:
     torch.cuda.synchronize()
     dist.barrier()
     clocks = sampler.stop()
+    blk_ms, blk_launches = ctypes.c_double(0.0), ctypes.c_uint64(0)
+    check(lib.bmmgpu_block_timer_read(ctypes.byref(blk_ms), ctypes.byref(blk_launches)))
+    check(lib.bmmgpu_block_timer(0))
     local_ms = t0.elapsed_time(t1) / args.steps
     ms = dist.max(local_ms)
-    kms = statistics.mean(kt0[args.warmup + i].elapsed_time(kt1[args.warmup + i]) for i in range(args.steps))
     total_bops = eff_bops(n, n, n)
     value = total_bops / (ms * 1e-3) / 1e15
 
@@ -366,11 +364,15 @@ def run_ours(args, dist: Dist) -> None:
     if algo == 0:
         # algorithmic work of the one product launch: the slab's 2 m n k - m n
         launch_bops = eff_bops(m, n, n)
+        e_levels = 0
     else:
-        # the timed region is the whole fast pipeline; its algorithmic work is the
-        # effective count (the leaves execute 7^e/8^e of it)
-        launch_bops = eff_bops(n, n, n)
-        kname = f"alt pipeline ({kname} leaves + expand/compress passes)"
+        # the leaf layer: 7^e products of L = n >> e (the recursion's exact block products)
+        depth = (n // 64).bit_length() - 1
+        e_levels = max(0, min(depth, depth + 6 - (args.leaf_log2 or 12)))
+        leaf = n >> e_levels
+        launch_bops = 7**e_levels * eff_bops(leaf, leaf, leaf)
+        kname = f"{kname} (leaf layer: 7^{e_levels} products of {leaf}^3)"
+    kms = blk_ms.value / args.steps  # block-product device time per step
     achieved = launch_bops / (kms * 1e-3)
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
@@ -378,7 +380,8 @@ def run_ours(args, dist: Dist) -> None:
         traffic = json.loads(tf.read_text()).get(f"{args.workload}:{resolved}")
     roofline = {"bound": "alu" if resolved == 1 else "tensor", "achieved": achieved / 1e12,
                 "peak": peak / 1e12, "unit": "Tbop/s", "frac": achieved / peak, "traffic": traffic,
-                "kernel": kname, "kernel_ms": kms,
+                "kernel": kname, "kernel_ms": kms, "kernel_launches_per_step": blk_launches.value / args.steps,
+                "kernel_share_of_step": kms / ms,
                 "peak_source": "profiles/peaks.json (measured issue rate, microbench/ubench.cu; "
                                "MEASURED_PEAKS.json has no integer-ALU or fp4 figure)"}
 

@@ -121,8 +121,8 @@ int bmmgpu_dev_cubic(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint
                      int32_t accumulate, void* stream);
 
 /* `batch` independent panel products in one persistent launch: product b uses
- * dA + b*sA, dBt + b*sB, dC + b*sC (strides in words), otherwise as
- * bmmgpu_dev_cubic.  The leaf layer of the fast recursion is this call
+ * dA + b*sA, dBt + b*sB, dC + b*sC (strides in words; sA or sB = 0 broadcasts
+ * one panel to every product), otherwise as bmmgpu_dev_cubic.  The leaf layer of the fast recursion is this call
  * (reference parallel_leaf's 7^d kernel64 calls, engine.cpp:232-272). */
 int bmmgpu_dev_cubic_batched(const uint64_t* dA, uint64_t lda, uint64_t sA, const uint64_t* dBt, uint64_t ldbt,
                              uint64_t sB, uint64_t* dC, uint64_t ldc, uint64_t sC, uint64_t batch, uint64_t m_pad,
@@ -144,6 +144,15 @@ int bmmgpu_dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt
  * slabs are independent, so no exchange step exists.
  * Pure host arithmetic, no device needed. */
 int bmmgpu_slab_rows(uint64_t m, uint32_t parts, uint32_t index, uint64_t gran, uint64_t* begin, uint64_t* end);
+
+/* Block-product timer.  bmmgpu_block_timer(1) clears and starts bracketing every
+ * block-product launch (cubic, batched, the leaves of the fast recursion, the
+ * out-of-core drivers) with CUDA events on its stream; bmmgpu_block_timer(0) stops.
+ * bmmgpu_block_timer_read waits for the recorded launches and returns their summed
+ * device time and count: the dominant kernel's time inside a longer pipeline
+ * (bench.py's roofline).  Off by default. */
+int bmmgpu_block_timer(int32_t enable);
+int bmmgpu_block_timer_read(double* ms, uint64_t* launches);
 
 /* Number of kernel launches the last host-API call made on its devices. */
 uint64_t bmmgpu_last_launch_count(void);

@@ -95,6 +95,10 @@ def lib() -> ctypes.CDLL:
                                                i32, i32, vp]
         L.bmmgpu_slab_rows.argtypes = [u64, ctypes.c_uint32, ctypes.c_uint32, u64, _u64p, _u64p]
         L.bmmgpu_slab_rows.restype = ctypes.c_int
+        L.bmmgpu_block_timer.argtypes = [i32]
+        L.bmmgpu_block_timer.restype = ctypes.c_int
+        L.bmmgpu_block_timer_read.argtypes = [ctypes.POINTER(ctypes.c_double), _u64p]
+        L.bmmgpu_block_timer_read.restype = ctypes.c_int
         L.bmmgpu_last_launch_count.restype = u64
         L.bmmgpu_device_count.restype = ctypes.c_int
         L.bmmgpu_last_error.restype = ctypes.c_char_p

@@ -33,6 +33,8 @@ namespace bmmgpu {
 
 int launch_transpose(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
                      uint64_t kw, cudaStream_t stream);
+int launch_transpose_ld(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
+                        uint64_t kw, uint64_t ldbt, cudaStream_t stream);
 int launch_cubic(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
                  uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate,
                  cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
@@ -447,37 +449,78 @@ namespace {
 
 // child = XOR of the quadrants of an L x L matrix selected by a 4-bit mask
 // (one alpha / beta row of a depth-first level, reference engine.cpp:284-285).
-__global__ void select_kernel(const uint64_t* __restrict__ in, uint64_t ld_in, uint64_t L, uint64_t* __restrict__ out,
-                              uint64_t ld_out, uint32_t mask) {
-    const uint64_t half = L / 2, hw = L / 128, total = half * hw;
+template <int V>
+__global__ void __launch_bounds__(256) select_kernel(const uint64_t* __restrict__ in, uint64_t ld_in, uint64_t total,
+                                                     PassGeom g, uint64_t* __restrict__ out, uint64_t ld_out,
+                                                     uint32_t mask) {
+    using W = Words<V>;
+    using T = typename W::T;
     for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
          idx += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t w = idx % hw, r = idx / hw;
+        const uint64_t w = (idx & ((1ull << g.sh_wv) - 1)) * V;
+        const uint64_t r = idx >> g.sh_wv;
         const uint64_t* base = in + r * ld_in + w;
-        uint64_t v = 0;
-        if (mask & 1) v ^= base[0];
-        if (mask & 2) v ^= base[hw];
-        if (mask & 4) v ^= base[half * ld_in];
-        if (mask & 8) v ^= base[half * ld_in + hw];
-        out[r * ld_out + w] = v;
+        T v = W::zero();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (mask & (1u << q))
+                v = W::x(v, *reinterpret_cast<const T*>(base + (q >> 1) * g.ls * ld_in + (q & 1) * g.ws));
+        *reinterpret_cast<T*>(out + r * ld_out + w) = v;
     }
 }
 
 // quadrant q of C ^= child for every q in mask (one gamma column, folded as
 // each child product finishes; reference engine.cpp:288).
-__global__ void scatter_xor_kernel(const uint64_t* __restrict__ q_in, uint64_t ld_q, uint64_t L, uint64_t* C,
-                                   uint64_t ldc, uint32_t mask) {
-    const uint64_t half = L / 2, hw = L / 128, total = half * hw;
+template <int V>
+__global__ void __launch_bounds__(256) scatter_xor_kernel(const uint64_t* __restrict__ q_in, uint64_t ld_q,
+                                                          uint64_t total, PassGeom g, uint64_t* C, uint64_t ldc,
+                                                          uint32_t mask) {
+    using W = Words<V>;
+    using T = typename W::T;
     for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
          idx += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t w = idx % hw, r = idx / hw;
-        const uint64_t v = q_in[r * ld_q + w];
+        const uint64_t w = (idx & ((1ull << g.sh_wv) - 1)) * V;
+        const uint64_t r = idx >> g.sh_wv;
+        const T v = *reinterpret_cast<const T*>(q_in + r * ld_q + w);
         uint64_t* base = C + r * ldc + w;
-        if (mask & 1) base[0] ^= v;
-        if (mask & 2) base[hw] ^= v;
-        if (mask & 4) base[half * ldc] ^= v;
-        if (mask & 8) base[half * ldc + hw] ^= v;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (mask & (1u << q)) {
+                T* p = reinterpret_cast<T*>(base + (q >> 1) * g.ls * ldc + (q & 1) * g.ws);
+                *p = W::x(*p, v);
+            }
     }
+}
+
+int launch_select(const uint64_t* in, uint64_t ld_in, uint64_t L, uint64_t* out, uint64_t ld_out, uint32_t mask,
+                  cudaStream_t s) {
+    const uint64_t ws = L / 128;
+    const int V = (ws % 2 == 0 && ld_in % 2 == 0 && ld_out % 2 == 0 && aligned16(in) && aligned16(out)) ? 2 : 1;
+    const PassGeom g = pass_geom(L, 1, V);
+    const uint64_t total = g.ls * (ws / V);
+    if (V == 2)
+        select_kernel<2><<<grid_for(total), 256, 0, s>>>(in, ld_in, total, g, out, ld_out, mask);
+    else
+        select_kernel<1><<<grid_for(total), 256, 0, s>>>(in, ld_in, total, g, out, ld_out, mask);
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaGetLastError());
+    return kOk;
+}
+
+int launch_scatter(const uint64_t* q_in, uint64_t ld_q, uint64_t L, uint64_t* C, uint64_t ldc, uint32_t mask,
+                   cudaStream_t s) {
+    if (!mask) return kOk;
+    const uint64_t ws = L / 128;
+    const int V = (ws % 2 == 0 && ld_q % 2 == 0 && ldc % 2 == 0 && aligned16(q_in) && aligned16(C)) ? 2 : 1;
+    const PassGeom g = pass_geom(L, 1, V);
+    const uint64_t total = g.ls * (ws / V);
+    if (V == 2)
+        scatter_xor_kernel<2><<<grid_for(total), 256, 0, s>>>(q_in, ld_q, total, g, C, ldc, mask);
+    else
+        scatter_xor_kernel<1><<<grid_for(total), 256, 0, s>>>(q_in, ld_q, total, g, C, ldc, mask);
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaGetLastError());
+    return kOk;
 }
 
 }  // namespace
@@ -501,19 +544,15 @@ int alt_serial(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t l
     DevMem T, S, Q;
     if ((st = T.alloc(half * hw * 8, s)) || (st = S.alloc(half * hw * 8, s)) || (st = Q.alloc(half * hw * 8, s)))
         return st;
-    const uint64_t total = half * hw;
     for (int h = 0; h < 7; ++h) {
-        select_kernel<<<grid_for(total), 256, 0, s>>>(dA, lda, n, T.u(), hw, ma.m[h]);
-        select_kernel<<<grid_for(total), 256, 0, s>>>(dBt, ldbt, n, S.u(), hw, mb.m[h]);
-        count_launch(2);
-        BMMGPU_CUDA_TRY(cudaGetLastError());
+        if ((st = launch_select(dA, lda, n, T.u(), hw, ma.m[h], s)) ||
+            (st = launch_select(dBt, ldbt, n, S.u(), hw, mb.m[h], s)))
+            return st;
         if ((st = alt_serial(T.u(), hw, S.u(), hw, Q.u(), hw, half, sc, e_serial - 1, e_par, kernel, s))) return st;
         uint32_t cmask = 0;
         for (int q = 0; q < 4; ++q)
             if (mg.m[q] & (1u << h)) cmask |= 1u << q;
-        scatter_xor_kernel<<<grid_for(total), 256, 0, s>>>(Q.u(), hw, n, dC, ldc, cmask);
-        count_launch();
-        BMMGPU_CUDA_TRY(cudaGetLastError());
+        if ((st = launch_scatter(Q.u(), hw, n, dC, ldc, cmask, s))) return st;
     }
     return kOk;
 }
@@ -575,12 +614,183 @@ int alt_levels(uint64_t n, int leaf_log2) {
     return e;
 }
 
+namespace {
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+struct EventSet {
+    cudaEvent_t ev[12] = {};
+    ~EventSet() {
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace
+
+// Streamed host path of the fast product (e >= 2).  The top recursion level runs
+// depth-first: its 7 children are ordered so that the first ones read the fewest
+// operand quadrants, each child starts as soon as the quadrants it reads have been
+// uploaded (a copy stream uploads A and B quadrant by quadrant, Bt quadrants are
+// transposed as their B quadrant lands), and each quadrant of C goes back to the host
+// (second copy stream) as soon as the last child contributing to it has been folded
+// in.  The H2D of most of the operands and the D2H of most of C overlap the leaf
+// products.  With pageable host memory the copies are host-synchronous, so the
+// uploads are interleaved with the children and the downloads run at the end.
+int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, const Scheme* sc,
+                               int e, int kernel, double* timing_ms) {
+    const uint64_t w = n / 64, half = n / 2, hw = w / 2;
+    const Masks7 ma = fused_expand(sc->alpha, sc->phi, sc->n_phi, false);
+    const Masks7 mb = fused_expand(sc->beta, sc->psi, sc->n_psi, true);  // Bt quadrant indices
+    const Masks4 mg = fused_compress(sc);
+    // greedy child order: fewest quadrants not yet requested first
+    int order[7];
+    {
+        bool used[7] = {};
+        uint32_t hA = 0, hB = 0;
+        for (int i = 0; i < 7; ++i) {
+            int best = -1, bc = 99;
+            for (int h = 0; h < 7; ++h)
+                if (!used[h]) {
+                    const int c = __builtin_popcount(ma.m[h] & ~hA) + __builtin_popcount(mb.m[h] & ~hB);
+                    if (c < bc) bc = c, best = h;
+                }
+            used[best] = true;
+            order[i] = best;
+            hA |= ma.m[best];
+            hB |= mb.m[best];
+        }
+    }
+    int last_pos[4] = {-1, -1, -1, -1};  // position in `order` after which quadrant q of C is final
+    for (int i = 0; i < 7; ++i)
+        for (int q = 0; q < 4; ++q)
+            if (mg.m[q] & (1u << order[i])) last_pos[q] = i;
+
+    struct Streams {
+        cudaStream_t c = nullptr, h = nullptr, d = nullptr;
+        ~Streams() {
+            if (c) cudaStreamDestroy(c);
+            if (h) cudaStreamDestroy(h);
+            if (d) cudaStreamDestroy(d);
+        }
+    } st3;
+    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.c, cudaStreamNonBlocking));
+    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.h, cudaStreamNonBlocking));
+    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.d, cudaStreamNonBlocking));
+    const cudaStream_t s = st3.c;
+    EventSet evs;  // 0-3 A quadrants, 4-7 B quadrants, 8-11 C quadrants
+    for (auto& ev : evs.ev) BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaEvent_t t0, t1;
+    BMMGPU_CUDA_TRY(cudaEventCreate(&t0));
+    BMMGPU_CUDA_TRY(cudaEventCreate(&t1));
+    struct TE {
+        cudaEvent_t a, b;
+        ~TE() {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } te{t0, t1};
+
+    int rc;
+    DevMem dA, dB, dBt, dC, T, S, Q;
+    if ((rc = dA.alloc(n * w * 8, s)) || (rc = dB.alloc(n * w * 8, s)) || (rc = dBt.alloc(n * w * 8, s)) ||
+        (rc = dC.alloc(n * w * 8, s)) || (rc = T.alloc(half * hw * 8, s)) || (rc = S.alloc(half * hw * 8, s)) ||
+        (rc = Q.alloc(half * hw * 8, s)))
+        return rc;
+    // the allocations exist once s reaches this point: the copy streams start after it, and
+    // the depth-first split of the children below sees the memory they take
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
+    BMMGPU_CUDA_TRY(cudaMemsetAsync(dC.p, 0, n * w * 8, s));
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaEventRecord(t0, s));
+    const bool pinned_c = host_pinned(C);
+    auto quad = [&](uint64_t* base, int q) { return base + (q >> 1) * half * w + (q & 1) * hw; };
+    auto cquad = [&](const uint64_t* base, int q) { return base + (q >> 1) * half * w + (q & 1) * hw; };
+    uint32_t upA = 0, upB = 0, waitA = 0, doneBt = 0;
+    const int e_sub = e - 1;
+    const int es_sub = choose_serial_levels(half, e_sub);
+    for (int i = 0; i < 7; ++i) {
+        const int h = order[i];
+        // uploads this child needs (B quadrant p = sigma(t) for Bt quadrant t)
+        for (int q = 0; q < 4; ++q)
+            if ((ma.m[h] & (1u << q)) && !(upA & (1u << q))) {
+                BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(quad(dA.u(), q), w * 8, cquad(A, q), w * 8, hw * 8, half,
+                                                  cudaMemcpyHostToDevice, st3.h));
+                BMMGPU_CUDA_TRY(cudaEventRecord(evs.ev[q], st3.h));
+                upA |= 1u << q;
+            }
+        for (int t = 0; t < 4; ++t) {
+            const int p = sigma(t);
+            if ((mb.m[h] & (1u << t)) && !(upB & (1u << p))) {
+                BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(quad(dB.u(), p), w * 8, cquad(B, p), w * 8, hw * 8, half,
+                                                  cudaMemcpyHostToDevice, st3.h));
+                BMMGPU_CUDA_TRY(cudaEventRecord(evs.ev[4 + p], st3.h));
+                upB |= 1u << p;
+            }
+        }
+        for (int q = 0; q < 4; ++q)
+            if ((ma.m[h] & (1u << q)) && !(waitA & (1u << q))) {
+                BMMGPU_CUDA_TRY(cudaStreamWaitEvent(s, evs.ev[q]));
+                waitA |= 1u << q;
+            }
+        for (int t = 0; t < 4; ++t)
+            if ((mb.m[h] & (1u << t)) && !(doneBt & (1u << t))) {
+                const int p = sigma(t);
+                BMMGPU_CUDA_TRY(cudaStreamWaitEvent(s, evs.ev[4 + p]));
+                if ((rc = launch_transpose_ld(quad(dB.u(), p), w, half, half, quad(dBt.u(), t), half, hw, w, s)))
+                    return rc;
+                doneBt |= 1u << t;
+            }
+        if ((rc = launch_select(dA.u(), w, n, T.u(), hw, ma.m[h], s)) ||
+            (rc = launch_select(dBt.u(), w, n, S.u(), hw, mb.m[h], s)))
+            return rc;
+        if ((rc = alt_serial(T.u(), hw, S.u(), hw, Q.u(), hw, half, sc, es_sub, e_sub - es_sub, kernel, s)))
+            return rc;
+        uint32_t cmask = 0;
+        for (int q = 0; q < 4; ++q)
+            if (mg.m[q] & (1u << h)) cmask |= 1u << q;
+        if ((rc = launch_scatter(Q.u(), hw, n, dC.u(), w, cmask, s))) return rc;
+        if (pinned_c)
+            for (int q = 0; q < 4; ++q)
+                if (last_pos[q] == i) {
+                    BMMGPU_CUDA_TRY(cudaEventRecord(evs.ev[8 + q], s));
+                    BMMGPU_CUDA_TRY(cudaStreamWaitEvent(st3.d, evs.ev[8 + q]));
+                    BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(quad(C, q), w * 8, quad(dC.u(), q), w * 8, hw * 8, half,
+                                                      cudaMemcpyDeviceToHost, st3.d));
+                }
+    }
+    BMMGPU_CUDA_TRY(cudaEventRecord(t1, s));
+    if (!pinned_c)
+        BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(C, w * 8, dC.p, w * 8, w * 8, n, cudaMemcpyDeviceToHost, s));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(st3.d));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    if (timing_ms) *timing_ms = ms;
+    return kOk;
+}
+
 // Host entry: reference-layout host buffers in, C out.
 int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, const bmmgpu_plan* plan,
                       int kernel, int leaf_log2, double* timing_ms) {
     (void)plan;  // the plan's host/serial/parallel split is a CPU schedule; the GPU picks e from leaf_log2
     const int e = alt_levels(n, leaf_log2);
     kernel = resolve_kernel(kernel);
+    if (e >= 2 && n >= 512 && !getenv("BMMGPU_ALT_NO_STREAM")) {
+        const Scheme* sc = scheme_for(algo);
+        if (!sc) {
+            set_error("no bilinear scheme for this algorithm");
+            return kEinval;
+        }
+        return alt_multiply_host_streamed(A, B, C, n, sc, e, kernel, timing_ms);
+    }
     const uint64_t w = n / 64;
     cudaStream_t s;
     BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));

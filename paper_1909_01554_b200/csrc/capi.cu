@@ -87,9 +87,51 @@ int granularity(int kernel, uint64_t* gm, uint64_t* gn, uint64_t* gk) {
     }
 }
 
+// Block-product timer: while enabled, every block-product launch is bracketed by a
+// pair of CUDA events on its stream, so a caller (bench.py) can report the dominant
+// kernel's device time even when it runs inside a longer pipeline (the leaves of the
+// fast recursion).  Off by default: no events are recorded.
+namespace {
+struct BlockTimer {
+    std::mutex mu;
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans;
+};
+BlockTimer g_timer;
+}  // namespace
+
+int launch_cubic_dispatch(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt,
+                          uint64_t* dC, uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2,
+                          bool accumulate, cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch,
+                          uint64_t sC_batch);
+
 int launch_cubic(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
                  uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate,
                  cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch) {
+    bool timed;
+    {
+        std::lock_guard<std::mutex> lk(g_timer.mu);
+        timed = g_timer.on;
+    }
+    if (!timed)
+        return launch_cubic_dispatch(kernel, dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream,
+                                     batch, sA_batch, sB_batch, sC_batch);
+    cudaEvent_t e0, e1;
+    BMMGPU_CUDA_TRY(cudaEventCreate(&e0));
+    BMMGPU_CUDA_TRY(cudaEventCreate(&e1));
+    BMMGPU_CUDA_TRY(cudaEventRecord(e0, stream));
+    const int st = launch_cubic_dispatch(kernel, dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate,
+                                         stream, batch, sA_batch, sB_batch, sC_batch);
+    BMMGPU_CUDA_TRY(cudaEventRecord(e1, stream));
+    std::lock_guard<std::mutex> lk(g_timer.mu);
+    g_timer.spans.emplace_back(e0, e1);
+    return st;
+}
+
+int launch_cubic_dispatch(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt,
+                          uint64_t* dC, uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2,
+                          bool accumulate, cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch,
+                          uint64_t sC_batch) {
     switch (resolve_kernel(kernel)) {
         case BMMGPU_KERNEL_LOP3:
             return launch_cubic_lop3(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream, batch,
@@ -250,6 +292,31 @@ int bmmgpu_slab_rows(uint64_t m, uint32_t parts, uint32_t index, uint64_t gran, 
 const char* bmmgpu_version(void) { return "bmm-b200 0.1 (sm_100a)"; }
 uint64_t bmmgpu_last_launch_count(void) { return g_launches.load(); }
 
+int bmmgpu_block_timer(int32_t enable) {
+    std::lock_guard<std::mutex> lk(g_timer.mu);
+    for (auto& p : g_timer.spans) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    g_timer.spans.clear();
+    g_timer.on = enable != 0;
+    return kOk;
+}
+
+int bmmgpu_block_timer_read(double* ms, uint64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_timer.mu);
+    double total = 0.0;
+    for (auto& p : g_timer.spans) {
+        BMMGPU_CUDA_TRY(cudaEventSynchronize(p.second));
+        float t = 0.f;
+        BMMGPU_CUDA_TRY(cudaEventElapsedTime(&t, p.first, p.second));
+        total += t;
+    }
+    if (ms) *ms = total;
+    if (launches) *launches = g_timer.spans.size();
+    return kOk;
+}
+
 int bmmgpu_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
@@ -284,7 +351,8 @@ int bmmgpu_dev_cubic_batched(const uint64_t* dA, uint64_t lda, uint64_t sA, cons
         set_error("unknown semiring");
         return kEinval;
     }
-    if (batch > 1 && (sA < m_pad * lda || sB < n_pad * ldbt || sC < m_pad * ldc)) {
+    // sA / sB may be 0 (one panel broadcast to every product); outputs must not overlap
+    if (batch > 1 && ((sA && sA < m_pad * lda) || (sB && sB < n_pad * ldbt) || sC < m_pad * ldc)) {
         set_error("batched product: batch strides smaller than one panel");
         return kEinval;
     }

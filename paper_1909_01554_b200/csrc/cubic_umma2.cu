@@ -151,8 +151,13 @@ __device__ unsigned long long g_probe[2 * P_MAX_PAIRS * 8];
 #define BMMGPU_DRAIN_GROUP 1  // x16 TMEM loads per drain phase
 #endif
 
+#ifndef BMMGPU_L2_HINT
+#define BMMGPU_L2_HINT 1  // 0 normal / normal, 1 A evict_last + Bt evict_first (measured best), 2 A normal + Bt evict_first
+#endif
+constexpr uint32_t kWaveSpinLimit = 4096;  // x 64 ns: give up on wave alignment after ~0.3 ms
+
 #ifndef BMMGPU_RASTER_GROUP
-#define BMMGPU_RASTER_GROUP 16
+#define BMMGPU_RASTER_GROUP 12
 #endif
 constexpr uint32_t kRasterGroup = BMMGPU_RASTER_GROUP;  // row panels per rasterisation group
 
@@ -162,7 +167,9 @@ struct TileMap {
 
     // Linear tile id -> (product, row tile, column tile), grouped by kRasterGroup row
     // panels within a product so concurrently running pairs share panels in L2
-    // (16 measured best at n=131072: least DRAM traffic, so the most power headroom).
+    // (with the loaders wave-aligned and the group's row panels held in L2 by evict_last,
+    // 12 measured best at n=131072: 48 MiB of resident A panels, ~6 column panels streamed
+    // per wave; DRAM reads 112 GB per launch against 806 GB for unaligned waves of 16).
     __device__ __forceinline__ void decode(uint32_t t, uint32_t& b, uint32_t& tm, uint32_t& tn) const {
         b = t / per_prod;
         const uint32_t r = t - b * per_prod;
@@ -249,7 +256,8 @@ template <bool kTma>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     cubic_umma2_kernel(const uint64_t* __restrict__ A, uint64_t lda, const uint64_t* __restrict__ Bt, uint64_t ldbt,
                        uint64_t* __restrict__ C, uint64_t ldc, uint64_t kw, int flags, TileMap map,
-                       uint32_t total_tiles, uint32_t epi_sleep_ns, const __grid_constant__ CUtensorMap tmA,
+                       uint32_t total_tiles, uint32_t epi_sleep_ns, unsigned long long* wave_ctr,
+                       const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB) {
     extern __shared__ uint8_t smem_raw[];
     // semiring as a runtime flag: one compiled main loop serves both (a template
@@ -421,25 +429,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         if (tid == P_LOADER_WARP0 * 32) {
             umma::tma_prefetch_desc(&tmA);
             umma::tma_prefetch_desc(&tmB);
+            // L2 policy: the kRasterGroup row panels (A) are reused by every wave of the
+            // group's sweep over the column panels; a column panel (Bt) only within a wave.
+#if BMMGPU_L2_HINT == 1
+            const uint64_t polA = umma::createpolicy_evict_last(), polB = umma::createpolicy_evict_first();
+#elif BMMGPU_L2_HINT == 2
+            const uint64_t polA = umma::createpolicy_evict_normal(), polB = umma::createpolicy_evict_first();
+#else
+            const uint64_t polA = umma::createpolicy_evict_normal(), polB = umma::createpolicy_evict_normal();
+#endif
             uint8_t* pk = smem + size_t(P_STAGES) * P_STAGE;
             int slot = 0;
             uint32_t pk_empty_parity = 0;
             uint64_t qn = 0;
-            for (uint32_t t = pair; t < (PROBE(256) ? 0 : total_tiles); t += n_pairs) {
+            uint32_t local = 0;
+            for (uint32_t t = pair; t < (PROBE(256) ? 0 : total_tiles); t += n_pairs, ++local) {
                 uint32_t b, tm, tn;
                 map.decode(t, b, tm, tn);
                 const int32_t ra = int32_t(tm * P_BM + rank * P_ROWS), rb = int32_t(tn * P_BN + rank * P_ROWS);
+                // Wave alignment (long-K products): tile `local` of every pair shares row and
+                // column panels through L2 only if the pairs sweep K together.  Static round
+                // robin lets fast pairs drift whole waves ahead (the measured DRAM traffic was
+                // 200x the operands); so a loader starts its next tile only once every pair's
+                // loader has issued its previous one.  The loaders run two superstages ahead
+                // of the MMAs, so the wait hides behind buffered work.  Bounded: after
+                // kWaveSpinLimit polls it proceeds anyway (co-residency is not assumed).
+                if (wave_ctr && local > 0) {
+                    const unsigned long long target = (unsigned long long)n_pairs * local;
+                    for (uint32_t i = 0; i < kWaveSpinLimit && umma::ld_acquire_u64(wave_ctr) < target; ++i)
+                        __nanosleep(64);
+                }
                 for (uint64_t k0 = 0; k0 < n_stages; k0 += 4, ++qn) {
                     if (qn >= P_SST_SLOTS) umma::mbar_wait(&pk_empty_bar[slot], pk_empty_parity);
                     uint8_t* dst = pk + slot * P_SST;
                     umma::mbar_arrive_expect_tx(&pk_full_bar[slot], P_SST);
-                    umma::tma_load_3d(dst, &tmA, int32_t(k0 * 4), ra, int32_t(b), &pk_full_bar[slot]);
-                    umma::tma_load_3d(dst + P_SST_OP, &tmB, int32_t(k0 * 4), rb, int32_t(b), &pk_full_bar[slot]);
+                    // a zero batch stride broadcasts one panel (its map has a single batch entry)
+                    umma::tma_load_3d_hint(dst, &tmA, int32_t(k0 * 4), ra, map.sA ? int32_t(b) : 0,
+                                           &pk_full_bar[slot], polA);
+                    umma::tma_load_3d_hint(dst + P_SST_OP, &tmB, int32_t(k0 * 4), rb, map.sB ? int32_t(b) : 0,
+                                           &pk_full_bar[slot], polB);
                     if (++slot == P_SST_SLOTS) {
                         slot = 0;
                         if (qn + 1 > P_SST_SLOTS) pk_empty_parity ^= 1;
                     }
                 }
+                if (wave_ctr && rank == 0) umma::red_release_add_u64(wave_ctr, 1);
             }
         }
     } else if (warp >= P_LOADER_WARP0) {
@@ -582,9 +616,10 @@ EncodeTiledFn encode_tiled() {
 bool make_operand_map(CUtensorMap* m, const uint64_t* base, uint64_t kw, uint64_t rows, uint64_t ld, uint64_t batch,
                       uint64_t s_batch) {
     const EncodeTiledFn fn = encode_tiled();
-    if (!fn || kw < 16 || rows < uint64_t(P_ROWS) || ld % 2 || (batch > 1 && (s_batch == 0 || s_batch % 2)) ||
+    if (!fn || kw < 16 || rows < uint64_t(P_ROWS) || ld % 2 || (batch > 1 && s_batch % 2) ||
         (reinterpret_cast<uintptr_t>(base) & 15))
         return false;
+    if (s_batch == 0) batch = 1;  // broadcast panel
     const cuuint64_t dims[3] = {kw, rows, batch};
     const cuuint64_t strides[2] = {ld * 8, (batch > 1 ? s_batch : rows * ld) * 8};
     const cuuint32_t box[3] = {16, uint32_t(P_ROWS), 1};
@@ -651,8 +686,20 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
     const uint64_t n_stages = kw * 64 / P_KBITS;
     uint32_t epi_sleep = n_stages >= 128 ? BMMGPU_EPI_SLEEP : n_stages >= 32 ? 64 : 0;
     if (const char* es = getenv("BMMGPU_EPI_SLEEP_NS")) epi_sleep = uint32_t(atoi(es));
+    // Wave alignment of the TMA loaders for long-K products (see the loader): a zeroed
+    // 8-byte counter per launch from the stream-ordered pool.
+    DeviceBuffer ctr;
+    unsigned long long* wave_ctr = nullptr;
+    const char* wa = getenv("BMMGPU_WAVE_ALIGN");
+    if (tma && n_stages >= 64 && total > pairs && !(wa && *wa == '0')) {
+        int st;
+        if ((st = ctr.alloc(8, stream))) return st;
+        BMMGPU_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, 8, stream));
+        count_launch();
+        wave_ctr = static_cast<unsigned long long*>(ctr.p);
+    }
     kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw, flags, map,
-                                                             uint32_t(total), epi_sleep, tmA, tmB);
+                                                             uint32_t(total), epi_sleep, wave_ctr, tmA, tmB);
     count_launch();
     BMMGPU_CUDA_TRY(cudaGetLastError());
     return kOk;

@@ -19,7 +19,7 @@ constexpr int TB = 8;  // blocks per tile side: 8 K blocks (512 rows) x 8 words 
 
 __global__ void __launch_bounds__(256) transpose_kernel(const uint64_t* __restrict__ B, uint64_t ldb, uint64_t k,
                                                         uint64_t n, uint64_t* __restrict__ Bt, uint64_t n_pad,
-                                                        uint64_t kw) {
+                                                        uint64_t kw, uint64_t ldbt) {
     __shared__ uint64_t tile[TB][TB][64];  // [N block][K block][row of the transposed block]
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t nb_words = (n + 63) / 64;
@@ -59,12 +59,12 @@ __global__ void __launch_bounds__(256) transpose_kernel(const uint64_t* __restri
     // Warp w writes N block bj0 + w: rows (bj0+w)*64 + lane (+32), K words
     // blockIdx.y*8 .. +7 (64 contiguous bytes per row).
     const uint64_t kw0 = blockIdx.y * uint64_t(TB);
-    const bool vec = (kw % 2 == 0) && kw0 + TB <= kw;
+    const bool vec = (ldbt % 2 == 0) && (reinterpret_cast<uintptr_t>(Bt) & 15) == 0 && kw0 + TB <= kw;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const uint64_t row = (bj0 + warp) * 64 + lane + 32 * h;
         if (row >= n_pad) continue;
-        uint64_t* dst = Bt + row * kw + kw0;
+        uint64_t* dst = Bt + row * ldbt + kw0;
         if (vec) {
 #pragma unroll
             for (int kb = 0; kb < TB; kb += 2)
@@ -80,20 +80,26 @@ __global__ void __launch_bounds__(256) transpose_kernel(const uint64_t* __restri
 
 }  // namespace
 
-// n_pad must be a multiple of 256 (TB_N * 64).  Rows j >= n and K words past
-// ceil(k/64) come out zero.
-int launch_transpose(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
-                     uint64_t kw, cudaStream_t stream) {
-    if (n_pad % 256 != 0 || n_pad < n || kw * 64 < k) {
+// n_pad must be a multiple of 256.  Rows j >= n and K words past ceil(k/64) come
+// out zero.  Bt rows are ldbt words apart (kw for a dense panel; larger when Bt is
+// a quadrant of a bigger matrix, as in the streamed fast path).
+int launch_transpose_ld(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
+                        uint64_t kw, uint64_t ldbt, cudaStream_t stream) {
+    if (n_pad % 256 != 0 || n_pad < n || kw * 64 < k || ldbt < kw) {
         set_error("bmmgpu_dev_transpose: n_pad must be a multiple of 256 covering n, kw*64 must cover k");
         return kEinval;
     }
     if (n_pad == 0 || kw == 0) return kOk;
     dim3 grid(static_cast<unsigned>(ceil_div(n_pad, TB * 64)), static_cast<unsigned>(ceil_div(kw, TB)));
-    transpose_kernel<<<grid, 256, 0, stream>>>(dB, ldb, k, n, dBt, n_pad, kw);
+    transpose_kernel<<<grid, 256, 0, stream>>>(dB, ldb, k, n, dBt, n_pad, kw, ldbt);
     count_launch();
     BMMGPU_CUDA_TRY(cudaGetLastError());
     return kOk;
+}
+
+int launch_transpose(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
+                     uint64_t kw, cudaStream_t stream) {
+    return launch_transpose_ld(dB, ldb, k, n, dBt, n_pad, kw, kw, stream);
 }
 
 }  // namespace bmmgpu

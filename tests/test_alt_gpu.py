@@ -148,3 +148,25 @@ def test_device_fast_product_reads_operands_only(engine, oracle, leaf):
         assert np.array_equal(dC.cpu().numpy().view(np.uint64).ravel(), want), (algo, leaf)
         assert np.array_equal(dA.cpu().numpy().view(np.uint64).ravel(), a)
         assert torch.equal(dBt, bt0)
+
+
+@pytest.mark.parametrize("leaf", [6, 8])
+def test_streamed_host_path_pinned_buffers(engine, oracle, leaf):
+    """bmmgpu_multiply from page-locked host buffers: the streamed driver uploads A / B
+    quadrant by quadrant behind the first children and downloads each C quadrant as
+    soon as it is final; same bits as the cubic product for every scheme."""
+    import torch
+    bmm = engine
+    n = 1024
+    a = oracle.random(n, n, 81)
+    b = oracle.random(n, n, 82)
+    want = oracle.multiply_cubic(a, b, n, n, n, GF2)
+    ha = torch.from_numpy(a.view(np.int64)).pin_memory()
+    hb = torch.from_numpy(b.view(np.int64)).pin_memory()
+    hc = torch.zeros(n * n // 64, dtype=torch.int64).pin_memory()
+    for algo in (bmm.Algo.StrassenWinograd, bmm.Algo.AltSelfInverse, bmm.Algo.AltChaining):
+        out = bmm.BitMatrix(n, n, hc.numpy().view(np.uint64))
+        got = bmm.multiply(bmm.BitMatrix(n, n, ha.numpy().view(np.uint64)),
+                           bmm.BitMatrix(n, n, hb.numpy().view(np.uint64)), algo, bmm.LayerPlan.auto_plan(n, 1),
+                           bmm.Semiring.Gf2XorAnd, leaf_log2=leaf, out=out)
+        assert np.array_equal(got.words, want), (algo, leaf)
