@@ -48,7 +48,14 @@ WORKLOADS = {
     "c2-gf2-altsi-65536": (65536, GF2, 2, "GF(2) product n=65536 alternative-basis Strassen (BASELINE configs[1])"),
     "c4-gf2-cubic-262144": (262144, GF2, 0, "GF(2) product n=262144, output row slabs (BASELINE configs[3])"),
     "c4-gf2-altsi-262144": (262144, GF2, 2, "GF(2) product n=262144 alternative-basis Strassen"),
+    # configs[4] (n = 2^20 on 8 GPUs needs 384 GiB of host memory for A, B, C; one box has
+    # 196 GB), scaled to one GPU: n = 2^19 from pinned host memory through the out-of-core
+    # driver with a device budget below the operands (A row panels resident, B streamed in
+    # K-chunks, partial products XOR/OR-folded on device, C tiles back to host).
+    "c5-bool-ooc-524288": (524288, BOOL, 0, "Boolean n=2^19 out-of-core from host (configs[4] scaled to 1 GPU)"),
+    "c5-gf2-ooc-524288": (524288, GF2, 0, "GF(2) n=2^19 out-of-core from host (configs[4] scaled to 1 GPU)"),
 }
+OOC_BUDGET = 40 << 30  # device bytes the out-of-core workloads may use (operands are 3 x 32 GiB)
 DEFAULT_WORKLOAD = "c3-bool-cubic-131072"
 # Paper V100 numbers for the same metric/config at 1 GPU, Pbop/s.
 PUBLISHED_1GPU = {"c3-bool-cubic-131072": 0.15127, "c3-gf2-cubic-131072": 0.17014, "c1-gf2-cubic-8192": 0.13283,
@@ -232,11 +239,140 @@ def run_reference(args, dist: Dist) -> None:
 
 
 # ------------------------------------------------------------------ our arm
+def spot_check(hA: np.ndarray, hB: np.ndarray, hC: np.ndarray, n: int, ring: int, rows: list[int],
+               col: int) -> bool:
+    """Independent CPU check of full rows and one full column of C (numpy, no GPU,
+    no oracle): row i = fold over k with A[i,k] = 1 of B row k; column j = per-row
+    parity / OR of A[i,:] & B[:, j]."""
+    w = n // 64
+    A = hA.reshape(n, w)
+    B = hB.reshape(n, w)
+    C = hC.reshape(n, w)
+    for i in rows:
+        bits = np.unpackbits(A[i].view(np.uint8), bitorder="little")[:n]
+        ks = np.flatnonzero(bits)
+        acc = np.zeros(w, dtype=np.uint64)
+        for c0 in range(0, ks.size, 4096):
+            blk = B[ks[c0:c0 + 4096]]
+            if ring == GF2:
+                acc ^= np.bitwise_xor.reduce(blk, axis=0)
+            else:
+                acc |= np.bitwise_or.reduce(blk, axis=0)
+        if not np.array_equal(acc, C[i]):
+            return False
+    bcol = ((B[:, col // 64] >> np.uint64(col % 64)) & np.uint64(1)).astype(np.uint8)
+    bw = np.packbits(bcol, bitorder="little").view(np.uint64)
+    got = ((C[:, col // 64] >> np.uint64(col % 64)) & np.uint64(1)).astype(np.uint8)
+    for r0 in range(0, n, 8192):
+        x = A[r0:r0 + 8192] & bw
+        if ring == GF2:
+            v = np.bitwise_xor.reduce(x, axis=1)
+            v ^= v >> np.uint64(32)
+            v ^= v >> np.uint64(16)
+            v ^= v >> np.uint64(8)
+            v ^= v >> np.uint64(4)
+            v ^= v >> np.uint64(2)
+            v ^= v >> np.uint64(1)
+            want = (v & np.uint64(1)).astype(np.uint8)
+        else:
+            want = (np.bitwise_or.reduce(x, axis=1) != 0).astype(np.uint8)
+        if not np.array_equal(want, got[r0:r0 + 8192]):
+            return False
+    return True
+
+
+def run_ooc(args, dist: Dist) -> None:
+    """Out-of-core workloads: the inputs live in (pinned) host memory by definition, so
+    the measured number is the end-to-end one through bmmgpu_cubic; value = e2e."""
+    import torch
+    import paper_1909_01554_b200 as bmm
+
+    n, ring, algo, desc = WORKLOADS[args.workload]
+    lib = bmm.lib()
+    dev = dist.local_rank
+    torch.cuda.set_device(dev)
+    w = n // 64
+    r0, r1 = shard_rows(n, dist.rank, dist.world, 256)
+    m = r1 - r0
+    t_gen = time.perf_counter()
+    hA = torch.empty(max(m, 1) * w, dtype=torch.int64, pin_memory=True)
+    hB = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
+    hC = torch.empty(max(m, 1) * w, dtype=torch.int64, pin_memory=True)
+    hA_np, hB_np, hC_np = (t.numpy().view(np.uint64) for t in (hA, hB, hC))
+    bmm.random_rows_into(hA_np, n, 1, r0, r1)
+    bmm.random_rows_into(hB_np, n, 2, 0, n)
+    t_gen = time.perf_counter() - t_gen
+    budget = args.device_budget or OOC_BUDGET
+    opts = bmm._opts(0 if args.kernel == "auto" else KERNEL_IDS[args.kernel], device_mask=1 << dev,
+                     device_budget=budget, force_streaming=1)
+
+    def check(rc: int) -> None:
+        if rc != 0:
+            raise RuntimeError(lib.bmmgpu_last_error().decode())
+
+    def step() -> float:
+        dist.barrier()
+        s0 = time.perf_counter()
+        check(lib.bmmgpu_cubic(hA.data_ptr(), hB.data_ptr(), hC.data_ptr(), m, n, n, ring, ctypes.byref(opts)))
+        return time.perf_counter() - s0
+
+    for _ in range(args.warmup):
+        step()
+    visible = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip().isdigit()]
+    sampler = ClockSampler(int(visible[dev]) if dev < len(visible) else dev)
+    sampler.start()
+    check(lib.bmmgpu_block_timer(1))
+    times = [step() for _ in range(args.steps)]
+    clocks = sampler.stop()
+    blk_ms, blk_launches = ctypes.c_double(0.0), ctypes.c_uint64(0)
+    check(lib.bmmgpu_block_timer_read(ctypes.byref(blk_ms), ctypes.byref(blk_launches)))
+    check(lib.bmmgpu_block_timer(0))
+    launches = lib.bmmgpu_last_launch_count()
+    h2d, d2h = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    check(lib.bmmgpu_last_copy_bytes(ctypes.byref(h2d), ctypes.byref(d2h)))
+    t = dist.max(statistics.median(times))
+    total_bops = eff_bops(n, n, n)
+    value = total_bops / t / 1e15
+    ok = None
+    if args.check and dist.rank == 0:
+        ok = spot_check(hA_np, hB_np, hC_np, n, ring, [0, m // 2 + 1, m - 1], n // 3)
+    peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())
+    kms = blk_ms.value / args.steps
+    achieved = eff_bops(m, n, n) / (kms * 1e-3)
+    if dist.rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "e2m1",
+                "data": "synthetic (BitMatrix::random seeds 1, 2, mt19937_64), pinned host memory",
+                "config": {"workload": args.workload, "desc": desc, "n": n, "ring": "gf2" if ring else "boolean",
+                           "algo": "cubic", "rows_per_rank": m, "device_budget_bytes": budget,
+                           "driver": "out-of-core tiles (force_streaming=1)",
+                           "value_is": "end to end from pinned host buffers (the operands exceed the budget)",
+                           "input_generation_s": t_gen,
+                           "parallelism": f"output row slabs x{dist.world}, no exchange"},
+                "roofline": {"bound": "tensor", "achieved": achieved / 1e12,
+                             "peak": peaks["umma_mxf4_bops"] / 1e12, "unit": "Tbop/s",
+                             "frac": achieved / peaks["umma_mxf4_bops"], "traffic": None,
+                             "kernel": "cubic_umma2_kernel (K-chunk products of the tile driver)",
+                             "kernel_ms": kms, "kernel_launches_per_step": blk_launches.value / args.steps,
+                             "kernel_share_of_step": kms / (t * 1e3)},
+                "cpu_baseline": None,
+                "e2e": {"value": value, "unit": UNIT, "ms_per_step": t * 1e3,
+                        "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value),
+                        "h2d_note": "counted by the library (bmmgpu_last_copy_bytes): A once, B once per "
+                                    "resident row panel of the plan",
+                        "path": "bmmgpu_cubic (include/bmmgpu.h) from pinned host buffers, per rank"},
+                "spot_check": ok, "clocks": clocks, "gpu_launches": int(launches * args.steps)}
+        print(json.dumps(line), flush=True)
+
+
 def run_ours(args, dist: Dist) -> None:
     import torch
     import paper_1909_01554_b200 as bmm
 
     n, ring, algo, desc = WORKLOADS[args.workload]
+    if args.workload.startswith("c5-"):
+        return run_ooc(args, dist)
     kernel = KERNEL_IDS[args.kernel]
     lib = bmm.lib()
     dev = dist.local_rank
@@ -443,7 +579,9 @@ def main() -> None:
                     help="e2e driver: 0 auto, 1 out-of-core tiles (A panels resident, B streamed in K-chunks), "
                          "2 K-outer pipeline (C resident, A/B K-chunks uploaded behind the product)")
     ap.add_argument("--device-budget", dest="device_budget", type=int, default=0,
-                    help="HBM bytes the e2e call may use (0 = free memory)")
+                    help="HBM bytes the e2e call may use (0 = free memory; the c5 workloads default to 40 GiB)")
+    ap.add_argument("--check", action="store_true",
+                    help="c5 workloads: verify full rows and a full column of C on the CPU (numpy)")
     args = ap.parse_args()
     dist = Dist()
     try:

@@ -157,6 +157,10 @@ int bmmgpu_block_timer_read(double* ms, uint64_t* launches);
 /* Number of kernel launches the last host-API call made on its devices. */
 uint64_t bmmgpu_last_launch_count(void);
 
+/* Host->device and device->host bytes the last host-API call copied (operands,
+ * re-streamed panels, results). */
+int bmmgpu_last_copy_bytes(uint64_t* h2d, uint64_t* d2h);
+
 int bmmgpu_device_count(void);
 const char* bmmgpu_last_error(void);
 const char* bmmgpu_version(void);

@@ -721,7 +721,7 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
         // uploads this child needs (B quadrant p = sigma(t) for Bt quadrant t)
         for (int q = 0; q < 4; ++q)
             if ((ma.m[h] & (1u << q)) && !(upA & (1u << q))) {
-                BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(quad(dA.u(), q), w * 8, cquad(A, q), w * 8, hw * 8, half,
+                BMMGPU_CUDA_TRY(memcpy2d_counted(quad(dA.u(), q), w * 8, cquad(A, q), w * 8, hw * 8, half,
                                                   cudaMemcpyHostToDevice, st3.h));
                 BMMGPU_CUDA_TRY(cudaEventRecord(evs.ev[q], st3.h));
                 upA |= 1u << q;
@@ -729,7 +729,7 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
         for (int t = 0; t < 4; ++t) {
             const int p = sigma(t);
             if ((mb.m[h] & (1u << t)) && !(upB & (1u << p))) {
-                BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(quad(dB.u(), p), w * 8, cquad(B, p), w * 8, hw * 8, half,
+                BMMGPU_CUDA_TRY(memcpy2d_counted(quad(dB.u(), p), w * 8, cquad(B, p), w * 8, hw * 8, half,
                                                   cudaMemcpyHostToDevice, st3.h));
                 BMMGPU_CUDA_TRY(cudaEventRecord(evs.ev[4 + p], st3.h));
                 upB |= 1u << p;
@@ -762,13 +762,13 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
                 if (last_pos[q] == i) {
                     BMMGPU_CUDA_TRY(cudaEventRecord(evs.ev[8 + q], s));
                     BMMGPU_CUDA_TRY(cudaStreamWaitEvent(st3.d, evs.ev[8 + q]));
-                    BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(quad(C, q), w * 8, quad(dC.u(), q), w * 8, hw * 8, half,
+                    BMMGPU_CUDA_TRY(memcpy2d_counted(quad(C, q), w * 8, quad(dC.u(), q), w * 8, hw * 8, half,
                                                       cudaMemcpyDeviceToHost, st3.d));
                 }
     }
     BMMGPU_CUDA_TRY(cudaEventRecord(t1, s));
     if (!pinned_c)
-        BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(C, w * 8, dC.p, w * 8, w * 8, n, cudaMemcpyDeviceToHost, s));
+        BMMGPU_CUDA_TRY(memcpy2d_counted(C, w * 8, dC.p, w * 8, w * 8, n, cudaMemcpyDeviceToHost, s));
     BMMGPU_CUDA_TRY(cudaStreamSynchronize(st3.d));
     BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
     float ms = 0.f;
@@ -814,8 +814,8 @@ int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_
         BMMGPU_CUDA_TRY(cudaMemsetAsync(dA.p, 0, rows_a * kw * 8, s));
         count_launch();
     }
-    BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dA.p, kw * 8, A, w * 8, w * 8, n, cudaMemcpyHostToDevice, s));
-    BMMGPU_CUDA_TRY(cudaMemcpyAsync(dB.p, B, n * w * 8, cudaMemcpyHostToDevice, s));
+    BMMGPU_CUDA_TRY(memcpy2d_counted(dA.p, kw * 8, A, w * 8, w * 8, n, cudaMemcpyHostToDevice, s));
+    BMMGPU_CUDA_TRY(memcpy_counted(dB.p, B, n * w * 8, cudaMemcpyHostToDevice, s));
     cudaEvent_t e0, e1;
     BMMGPU_CUDA_TRY(cudaEventCreate(&e0));
     BMMGPU_CUDA_TRY(cudaEventCreate(&e1));
@@ -828,7 +828,7 @@ int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_
         st = alt_multiply_device(dA.u(), w, dBt.u(), w, dC.u(), w, n, algo, e, choose_serial_levels(n, e), kernel, s);
     if (st) return st;
     BMMGPU_CUDA_TRY(cudaEventRecord(e1, s));
-    BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(C, w * 8, dC.p, cw * 8, w * 8, n, cudaMemcpyDeviceToHost, s));
+    BMMGPU_CUDA_TRY(memcpy2d_counted(C, w * 8, dC.p, cw * 8, w * 8, n, cudaMemcpyDeviceToHost, s));
     BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);

@@ -69,6 +69,11 @@ void enable_pool_caching() {
     done_mask |= 1u << dev;
 }
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
+void count_copy(cudaMemcpyKind kind, uint64_t bytes) {
+    if (kind == cudaMemcpyHostToDevice) g_h2d.fetch_add(bytes, std::memory_order_relaxed);
+    if (kind == cudaMemcpyDeviceToHost) g_d2h.fetch_add(bytes, std::memory_order_relaxed);
+}
 
 int resolve_kernel(int kernel) {
     // The tcgen05 kind::mxf4 kernel beats the LOP3 kernel 3.4-3.8x in bop/s on
@@ -207,12 +212,12 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
     BMMGPU_CUDA_TRY(cudaMemsetAsync(dA.p, 0, m_pad * kw * 8, s));
     count_launch();
     if (ka > 0)
-        BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dA.p, kw * 8, A + job.row_begin * ka, ka * 8, ka * 8, m,
+        BMMGPU_CUDA_TRY(memcpy2d_counted(dA.p, kw * 8, A + job.row_begin * ka, ka * 8, ka * 8, m,
                                           cudaMemcpyHostToDevice, s));
     // B, then Bt on device.
     if (k > 0 && nb > 0) {
         if ((st = dB.alloc(k * nb * 8, s))) return st;
-        BMMGPU_CUDA_TRY(cudaMemcpyAsync(dB.p, B, k * nb * 8, cudaMemcpyHostToDevice, s));
+        BMMGPU_CUDA_TRY(memcpy_counted(dB.p, B, k * nb * 8, cudaMemcpyHostToDevice, s));
         if ((st = launch_transpose(dB.u(), nb, k, n, dBt.u(), n_pad, kw, s))) return st;
     } else {
         BMMGPU_CUDA_TRY(cudaMemsetAsync(dBt.p, 0, n_pad * kw * 8, s));
@@ -221,7 +226,7 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
     if (accumulate && nb > 0) {
         BMMGPU_CUDA_TRY(cudaMemsetAsync(dC.p, 0, m_pad * cw * 8, s));
         count_launch();
-        BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dC.p, cw * 8, C + job.row_begin * nb, nb * 8, nb * 8, m,
+        BMMGPU_CUDA_TRY(memcpy2d_counted(dC.p, cw * 8, C + job.row_begin * nb, nb * 8, nb * 8, m,
                                           cudaMemcpyHostToDevice, s));
     }
     cudaEvent_t e0, e1;
@@ -237,7 +242,7 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
     }
     BMMGPU_CUDA_TRY(cudaEventRecord(e1, s));
     if (nb > 0)
-        BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(C + job.row_begin * nb, nb * 8, dC.p, cw * 8, nb * 8, m,
+        BMMGPU_CUDA_TRY(memcpy2d_counted(C + job.row_begin * nb, nb * 8, dC.p, cw * 8, nb * 8, m,
                                           cudaMemcpyDeviceToHost, s));
     BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
     cudaEventElapsedTime(&job.ms, e0, e1);
@@ -291,6 +296,12 @@ int bmmgpu_slab_rows(uint64_t m, uint32_t parts, uint32_t index, uint64_t gran, 
 }
 const char* bmmgpu_version(void) { return "bmm-b200 0.1 (sm_100a)"; }
 uint64_t bmmgpu_last_launch_count(void) { return g_launches.load(); }
+
+int bmmgpu_last_copy_bytes(uint64_t* h2d, uint64_t* d2h) {
+    if (h2d) *h2d = g_h2d.load();
+    if (d2h) *d2h = g_d2h.load();
+    return kOk;
+}
 
 int bmmgpu_block_timer(int32_t enable) {
     std::lock_guard<std::mutex> lk(g_timer.mu);
@@ -370,6 +381,8 @@ int bmmgpu_dev_cubic_batched(const uint64_t* dA, uint64_t lda, uint64_t sA, cons
 int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, uint64_t k, uint64_t n,
                  int32_t semiring, const bmmgpu_opts* opts) {
     g_launches.store(0);
+    g_h2d.store(0);
+    g_d2h.store(0);
     if (semiring != BMMGPU_BOOLEAN_OR_AND && semiring != BMMGPU_GF2_XOR_AND) {
         set_error("unknown semiring");
         return kEinval;
@@ -420,6 +433,8 @@ int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, 
 int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int32_t algo,
                     const bmmgpu_plan* plan, int32_t semiring, const bmmgpu_opts* opts) {
     g_launches.store(0);
+    g_h2d.store(0);
+    g_d2h.store(0);
     const bmmgpu_opts defaults{};
     const bmmgpu_opts& o = opts ? *opts : defaults;
     if (algo == BMMGPU_ALGO_CUBIC) return bmmgpu_cubic(A, B, C, n, n, n, semiring, opts);

@@ -11,6 +11,17 @@ constexpr int kOk = 0, kEinval = 1, kEshape = 3, kEcuda = 5, kEnodev = 6;
 
 void set_error(const std::string& msg);
 void count_launch(uint64_t n = 1);
+// Host<->device bytes moved by the host-API drivers (bmmgpu_last_copy_bytes).
+void count_copy(cudaMemcpyKind kind, uint64_t bytes);
+inline cudaError_t memcpy2d_counted(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                                    size_t height, cudaMemcpyKind kind, cudaStream_t s) {
+    count_copy(kind, uint64_t(width) * height);
+    return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, s);
+}
+inline cudaError_t memcpy_counted(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+    count_copy(kind, bytes);
+    return cudaMemcpyAsync(dst, src, bytes, kind, s);
+}
 
 #define BMMGPU_CUDA_TRY(expr)                                                                     \
     do {                                                                                          \

@@ -40,7 +40,8 @@ struct Plan {
 
 Plan plan_tiles(uint64_t m, uint64_t n, uint64_t kw, uint64_t gm, uint64_t gn, uint64_t gkw, uint64_t budget) {
     Plan p{};
-    p.TM = std::min<uint64_t>(round_up(m, gm), 32768);
+    // tall A panels: B is re-streamed once per row tile, so fewer, taller panels cut H2D
+    p.TM = std::min<uint64_t>(round_up(m, gm), 131072);
     p.TN = std::min<uint64_t>(round_up(std::max<uint64_t>(n, 1), gn), 32768);
     p.KCw = std::min<uint64_t>(kw, round_up(2048, gkw));  // 128 Ki bits of K per chunk
     auto need = [&](const Plan& q) {
@@ -139,7 +140,7 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
         BMMGPU_CUDA_TRY(cudaMemsetAsync(dA.p, 0, P.TM * kwc * 8, xs));
         count_launch();
         if (ka > 0)
-            BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dA.p, kwc * 8, A + (row_begin + r0) * ka, ka * 8, ka * 8, rows,
+            BMMGPU_CUDA_TRY(memcpy2d_counted(dA.p, kwc * 8, A + (row_begin + r0) * ka, ka * 8, ka * 8, rows,
                                               cudaMemcpyHostToDevice, xs));
         BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[4], xs));
         BMMGPU_CUDA_TRY(cudaStreamWaitEvent(cs, ev.e[4], 0));
@@ -148,7 +149,7 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
             const uint64_t cw0 = c0 / 64, cwn = ceil_div(cols, 64);
             if (accumulate) {
                 BMMGPU_CUDA_TRY(cudaMemsetAsync(dC.p, 0, P.TM * TNw * 8, cs));
-                BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dC.p, TNw * 8, C + (row_begin + r0) * nb + cw0, nb * 8, cwn * 8,
+                BMMGPU_CUDA_TRY(memcpy2d_counted(dC.p, TNw * 8, C + (row_begin + r0) * nb + cw0, nb * 8, cwn * 8,
                                                   rows, cudaMemcpyHostToDevice, cs));
                 count_launch();
             }
@@ -160,7 +161,7 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
                 // copy stream: wait until compute released this buffer, then fetch B[k0.., c0..]
                 BMMGPU_CUDA_TRY(cudaStreamWaitEvent(xs, ev.e[2 + buf], 0));
                 if (krows > 0)
-                    BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dB[buf].p, TNw * 8, B + k0 * nb + cw0, nb * 8, cwn * 8, krows,
+                    BMMGPU_CUDA_TRY(memcpy2d_counted(dB[buf].p, TNw * 8, B + k0 * nb + cw0, nb * 8, cwn * 8, krows,
                                                       cudaMemcpyHostToDevice, xs));
                 BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[buf], xs));
                 // compute stream: transpose the chunk and fold its product into the C tile
@@ -171,7 +172,7 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
                     return st;
                 BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[2 + buf], cs));
             }
-            BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(C + (row_begin + r0) * nb + cw0, nb * 8, dC.p, TNw * 8, cwn * 8, rows,
+            BMMGPU_CUDA_TRY(memcpy2d_counted(C + (row_begin + r0) * nb + cw0, nb * 8, dC.p, TNw * 8, cwn * 8, rows,
                                               cudaMemcpyDeviceToHost, cs));
         }
         BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[7], cs));  // the A panel may be replaced
@@ -235,7 +236,7 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
     BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[3], cs));
     if (accumulate) {
         BMMGPU_CUDA_TRY(cudaMemsetAsync(dC.p, 0, m_pad * cw * 8, cs));
-        BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dC.p, cw * 8, C + row_begin * nb, nb * 8, nb * 8, m,
+        BMMGPU_CUDA_TRY(memcpy2d_counted(dC.p, cw * 8, C + row_begin * nb, nb * 8, nb * 8, m,
                                           cudaMemcpyHostToDevice, cs));
         count_launch();
     }
@@ -249,10 +250,10 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
         BMMGPU_CUDA_TRY(cudaMemsetAsync(dA[buf].p, 0, m_pad * KCw * 8, xs));
         count_launch();
         if (aw > 0)
-            BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(dA[buf].p, KCw * 8, A + row_begin * ka + w0, ka * 8, aw * 8, m,
+            BMMGPU_CUDA_TRY(memcpy2d_counted(dA[buf].p, KCw * 8, A + row_begin * ka + w0, ka * 8, aw * 8, m,
                                               cudaMemcpyHostToDevice, xs));
         if (krows > 0)
-            BMMGPU_CUDA_TRY(cudaMemcpyAsync(dB[buf].p, B + k0 * nb, krows * nb * 8, cudaMemcpyHostToDevice, xs));
+            BMMGPU_CUDA_TRY(memcpy_counted(dB[buf].p, B + k0 * nb, krows * nb * 8, cudaMemcpyHostToDevice, xs));
         BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[buf], xs));
         BMMGPU_CUDA_TRY(cudaStreamWaitEvent(cs, ev.e[buf], 0));
         if ((st = launch_transpose(dB[buf].u(), nb, krows, n, dBt[buf].u(), n_pad, KCw, cs))) return st;
@@ -261,7 +262,7 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
             return st;
         BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[2 + buf], cs));
     }
-    BMMGPU_CUDA_TRY(cudaMemcpy2DAsync(C + row_begin * nb, nb * 8, dC.p, cw * 8, nb * 8, m, cudaMemcpyDeviceToHost,
+    BMMGPU_CUDA_TRY(memcpy2d_counted(C + row_begin * nb, nb * 8, dC.p, cw * 8, nb * 8, m, cudaMemcpyDeviceToHost,
                                       cs));
     BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[6], cs));
     BMMGPU_CUDA_TRY(cudaStreamSynchronize(cs));
