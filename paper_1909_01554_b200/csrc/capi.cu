@@ -196,7 +196,9 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
         if (force_streaming == 2 || (force_streaming == 0 && k >= 32768 && 3 * c_slab <= limit) ||
             in_core > limit)
             return stream_kouter_slab(job.device, job.row_begin, job.row_end, A, B, C, k, n, gf2, kernel,
-                                      accumulate, limit, &job.ms, 4);
+                                      accumulate, limit, &job.ms, getenv("BMMGPU_KOUTER_CHUNKS")
+                                                                       ? atoi(getenv("BMMGPU_KOUTER_CHUNKS"))
+                                                                       : 0);
     }
     cudaStream_t s;
     BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));

@@ -431,10 +431,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             umma::tma_prefetch_desc(&tmB);
             // L2 policy: the kRasterGroup row panels (A) are reused by every wave of the
             // group's sweep over the column panels; a column panel (Bt) only within a wave.
+            // Only for long-K products (flag 4): in a batch of short leaf products the
+            // evict_last lines of finished products would crowd out the live ones.
+            const bool hint = (flags & 4) != 0;
 #if BMMGPU_L2_HINT == 1
-            const uint64_t polA = umma::createpolicy_evict_last(), polB = umma::createpolicy_evict_first();
+            const uint64_t polA = hint ? umma::createpolicy_evict_last() : umma::createpolicy_evict_normal();
+            const uint64_t polB = hint ? umma::createpolicy_evict_first() : umma::createpolicy_evict_normal();
 #elif BMMGPU_L2_HINT == 2
-            const uint64_t polA = umma::createpolicy_evict_normal(), polB = umma::createpolicy_evict_first();
+            const uint64_t polA = umma::createpolicy_evict_normal();
+            const uint64_t polB = hint ? umma::createpolicy_evict_first() : umma::createpolicy_evict_normal();
 #else
             const uint64_t polA = umma::createpolicy_evict_normal(), polB = umma::createpolicy_evict_normal();
 #endif
@@ -678,8 +683,9 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
     auto kern = tma ? cubic_umma2_kernel<true> : cubic_umma2_kernel<false>;
     BMMGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P_SMEM)));
     const char* probe = getenv("BMMGPU_UMMA_PROBE");
-    const int flags = (accumulate ? 1 : 0) | (gf2 ? 2 : 0) | (getenv("BMMGPU_UMMA_TRACE") ? 16 : 0) |
-                      (probe && *probe ? 32 * atoi(probe) : 0);
+    const uint64_t n_stages_l = kw * 64 / P_KBITS;
+    const int flags = (accumulate ? 1 : 0) | (gf2 ? 2 : 0) | (n_stages_l >= 64 ? 4 : 0) |
+                      (getenv("BMMGPU_UMMA_TRACE") ? 16 : 0) | (probe && *probe ? 32 * atoi(probe) : 0);
     // Epilogue warps poll acc_full with this sleep between tries: long tiles (K of tens of
     // thousands of bits) leave them idle for ~100 us and their spinning would steal issue
     // slots from the expanders; for short tiles the sleep granularity is pure bubble.
