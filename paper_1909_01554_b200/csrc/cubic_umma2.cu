@@ -85,10 +85,15 @@ constexpr int P_SST_SLOTS = BMMGPU_SST_SLOTS;  // packed ring slots, one superst
 constexpr int P_SST_OP = P_ROWS * 128;         // one operand of a superstage: 128 rows x 128 bytes
 constexpr int P_SST = 2 * P_SST_OP;            // 32 KB
 static_assert(P_STAGES % 2 == 0, "the two expander groups alternate ring slots");
-constexpr size_t P_SMEM = size_t(P_STAGES) * P_STAGE + size_t(P_SST_SLOTS) * P_SST + 1024;  // + alignment slack
+// One K = 64 operand region of constants for the bias MMA (rows of 32 e2m1 ones, then
+// zeros); A and Bt of the bias MMA both read it.
+constexpr int P_CONST = P_REGION;
+constexpr size_t P_SMEM =
+    size_t(P_STAGES) * P_STAGE + size_t(P_SST_SLOTS) * P_SST + P_CONST + 1024;  // + alignment slack
 constexpr uint32_t P_TMEM_COLS = 512;
 constexpr uint32_t P_SF_EVEN = 256;
 constexpr uint32_t P_SF_ODD = 384;
+constexpr uint32_t P_SF_BIAS = 480;  // 2^9 block scales of the bias MMA
 constexpr uint32_t P_MAX_PAIRS = 74;  // 148 SMs
 
 static_assert(P_SMEM <= 232448 - 1024, "stage ring exceeds shared memory");
@@ -195,57 +200,65 @@ __device__ __forceinline__ void expand_store_sw128(uint8_t* region, int r, int g
     *reinterpret_cast<uint4*>(row + (((j0 + 3) ^ rr) << 4)) = make_uint4(y.x & M1, y.y & M1, y.z & M1, y.w & M1);
 }
 
-// The accumulator never starts from zero: it is preset to a bias (all MMAs accumulate)
-// so each output bit is a single bit of the fp32 word.  Counts c < 2^23 are exact:
-//   GF(2):   2^23 + c      -> the integer sits at mantissa bit 0, parity = bit 0;
-//   Boolean: 2^23 - 1 + c  -> c == 0 gives 8388607.0 (exponent 149, bit 23 set), c >= 1
-//            gives [2^23, 2^24) (exponent 150, bit 23 clear): non-zero = !bit 23.
-// Two instructions per output bit in the drain (shift + merge) instead of three.
-constexpr uint32_t kBiasGf2 = 0x4B000000u;   // 8388608.0f
-constexpr uint32_t kBiasBool = 0x4AFFFFFEu;  // 8388607.0f
-
+// The accumulator never starts from zero: each tile's first MMA (accumulate = 0)
+// multiplies a constant region of 32 e2m1 ones per row by itself with 2^9 x 2^9 block
+// scales, writing 32 * 2^18 = 2^23 into every element; the real MMAs then accumulate
+// on top.  Counts c < 2^23 stay exact at the bottom of the mantissa, so an output bit
+// is bit 0 of a 32-bit quantity:
+//   GF(2):   v = 2^23 + c, parity = bit 0 of v;
+//   Boolean: (v + 0x7FFFFF) >> 23 has bit 0 set iff c != 0.
+// The drain is issue-bound (measured: 640 ns per tile with two ops per bit, 224 ns with
+// the packing removed), so each bit is pushed into its word with one funnel shift:
+// w = (x:w) >> 1 moves bit 0 of x into bit 31 and the earlier bits down; after 8
+// pushes column j of a group sits in byte 3; byte permutes assemble the word.  About
+// one op per bit (GF(2)), three (Boolean).
+#ifndef BMMGPU_DRAIN_PROBE
+#define BMMGPU_DRAIN_PROBE 0  // dev: 1 = trivial packing (results wrong), isolates the drain's ALU cost
+#endif
+template <bool kGf2>
+__device__ __forceinline__ uint32_t bit_of(uint32_t v) {
+    return kGf2 ? v : (v + 0x7FFFFFu) >> 23;
+}
+// 16 columns -> 16 bits in the low half of the result, as two independent 8-deep
+// funnel-shift chains (each leaves its 8 bits in byte 3) merged with one byte permute:
+// the chain latency, not the op count, is what the drain waits on.
 template <bool kGf2>
 __device__ __forceinline__ uint32_t pack_counts16(const uint32_t (&v)[16]) {
-    uint32_t w = 0;
+    if (BMMGPU_DRAIN_PROBE == 1) return v[0] ^ v[15];
+    uint32_t a = 0, b = 0;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if (kGf2)
-            w |= (v[j] & 1u) << j;
-        else
-            w |= ((~v[j] >> 23) & 1u) << j;
+    for (int j = 0; j < 8; ++j) {
+        a = __funnelshift_r(a, bit_of<kGf2>(v[j]), 1);
+        b = __funnelshift_r(b, bit_of<kGf2>(v[8 + j]), 1);
     }
-    return w;
+    return __byte_perm(a, b, 0x0073);  // [a.byte3, b.byte3, -, -]
 }
 
 // The epilogue warp's 32 lanes x P_EPI_COLS columns of the accumulator -> words per lane,
 // 16 columns per TMEM load with two register buffers: chunk c + 1 is in flight while
-// chunk c is packed.  Each chunk is re-biased behind its load, and the accumulator goes
-// back to the leader's MMA lane as soon as the last chunk has landed.  Short-K tiles
-// (the 4096-bit leaves of the fast recursion) wait on this drain.
+// chunk c is packed, and the accumulator goes back to the leader's MMA lane as soon as
+// the last chunk has landed.  Short-K tiles (the 4096-bit leaves of the fast recursion)
+// wait on this drain.
 template <bool kGf2>
 __device__ __forceinline__ void drain_accumulator(uint32_t tbase, uint32_t (&words)[P_EPI_COLS / 32],
                                                   uint32_t acc_empty_leader, uint32_t lane) {
     constexpr int kChunks = P_EPI_COLS / 16;
-    const uint32_t bias = kGf2 ? kBiasGf2 : kBiasBool;
     uint32_t va[16], vb[16];
     umma::tmem_ld16(tbase, va);
     umma::tmem_ld_wait_regs16(va);
 #pragma unroll
     for (int c = 0; c < kChunks; c += 2) {
         umma::tmem_ld16(tbase + 16 * (c + 1), vb);
-        umma::tmem_st16_fill(tbase + 16 * c, bias);
         const uint32_t lo = pack_counts16<kGf2>(va);
         umma::tmem_ld_wait_regs16(vb);
-        umma::tmem_st16_fill(tbase + 16 * (c + 1), bias);
         if (c + 2 < kChunks) {
             umma::tmem_ld16(tbase + 16 * (c + 2), va);
         } else {
-            umma::tmem_st_wait();
             umma::fence_before_sync();
             __syncwarp();
             if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
         }
-        words[c >> 1] = lo | (pack_counts16<kGf2>(vb) << 16);
+        words[c >> 1] = __byte_perm(lo, pack_counts16<kGf2>(vb), 0x5410);
         if (c + 2 < kChunks) umma::tmem_ld_wait_regs16(va);
     }
 }
@@ -301,10 +314,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) umma::tmem_st32_fill(tmem + lane_base + P_SF_EVEN + 32 * c, 0x7F7F7F7Fu);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) umma::tmem_st32_fill(tmem + lane_base + P_SF_ODD + 32 * c, 0x80808080u);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) umma::tmem_st32_fill(tmem + lane_base + 32 * c, kGf2 ? kBiasGf2 : kBiasBool);
+        for (int c = 0; c < 3; ++c) umma::tmem_st32_fill(tmem + lane_base + P_SF_ODD + 32 * c, 0x80808080u);
+        umma::tmem_st32_fill(tmem + lane_base + P_SF_BIAS, 0x88888888u);  // 2^9
         umma::tmem_st_wait();
+    }
+    {
+        // bias operand: row r holds 32 e2m1 ones (0x22 bytes) in its logical 16-byte chunk 0
+        // (physical chunk 0 ^ (r & 7) of the 128-byte swizzle), zeros elsewhere
+        uint8_t* cst = smem + size_t(P_STAGES) * P_STAGE + size_t(P_SST_SLOTS) * P_SST;
+        for (uint32_t i = tid; i < uint32_t(P_CONST / 16); i += blockDim.x) {
+            const uint32_t r = i >> 3, phys = i & 7;
+            const uint32_t v = (phys ^ (r & 7)) == 0 ? 0x22222222u : 0u;
+            *reinterpret_cast<uint4*>(cst + size_t(i) * 16) = make_uint4(v, v, v, v);
+        }
+        umma::fence_proxy_async_smem();
     }
     umma::fence_before_sync();
     umma::cluster_sync();  // barriers of both CTAs initialised, TMEM of both allocated and scaled
@@ -378,6 +401,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         if (rank == 0) {
             constexpr uint32_t idesc = umma::idesc_mxf4(P_BM, P_BN);
             const uint64_t desc_base = umma::smem_desc_sw128(smem_u32(smem), 1024);
+            const uint64_t desc_const = umma::smem_desc_sw128(
+                smem_u32(smem + size_t(P_STAGES) * P_STAGE + size_t(P_SST_SLOTS) * P_SST), 1024);
             uint64_t it = 0;
             int s = 0;
             uint32_t full_parity = 0;
@@ -394,6 +419,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                 if (local > 0) PWAIT(4, umma::mbar_wait(&acc_empty_bar, (local - 1) & 1));
                 TRACE_AT(pair == 0 && lane == 0 && local < 512, 3072 + 4 * local + 3);
                 umma::fence_after_sync();
+                if (umma::elect_one() && !PROBE(32))  // preset the accumulator to 2^23
+                    umma::mma_mxf4_pair(tmem, desc_const, desc_const, idesc, tmem + P_SF_BIAS, tmem + P_SF_BIAS, 0u);
+                __syncwarp();
                 for (uint64_t k = 0; k < (PROBE(128) ? 0 : n_stages); ++k, ++it, s = (s + 1 == P_STAGES) ? (full_parity ^= 1, 0) : s + 1) {
                     PWAIT(3, umma::mbar_wait(&full_bar[s], full_parity));
                     TRACE_AT(pair == 0 && lane == 0 && it < 512, it);
@@ -407,7 +435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                             const uint32_t sf = tmem + ((j & 1) ? P_SF_ODD : P_SF_EVEN);
                             if (PROBE(32)) continue;
                             // + 32 bytes per K = 64 step
-                            // always accumulate: the epilogue presets the accumulator to the bias
+                            // always accumulate onto the bias
                             umma::mma_mxf4_pair(tmem, da0 + 2 * j, db0 + 2 * j, idesc, sf, sf, 1u);
                         }
                         umma::mma_commit_pair(&empty_bar[s], 0x3);
@@ -656,8 +684,8 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
             }
         return kOk;
     }
-    if (kw * 64 > (1ull << 23)) {
-        set_error("umma2 kernel: K above 2^23 bits would exceed exact biased fp32 accumulation");
+    if (kw * 64 >= (1ull << 23)) {
+        set_error("umma2 kernel: K of 2^23 bits or more would exceed exact biased fp32 accumulation");
         return kEinval;
     }
     const uint64_t m_tiles = m_pad / P_BM, n_tiles = n_pad / P_BN;
