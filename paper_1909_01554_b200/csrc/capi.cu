@@ -8,6 +8,7 @@
 // slab and all of Bt: output tiles are independent, so there is no exchange
 // step (the paper's "one host thread per output
 // segment").
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -133,10 +134,37 @@ int launch_cubic(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* d
     return st;
 }
 
+int launch_cubic_kernel(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt,
+                        uint64_t* dC, uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2,
+                        bool accumulate, cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch,
+                        uint64_t sC_batch);
+
+// The tensor-core kernels count in fp32 (exact below 2^23 terms): longer inner
+// dimensions run as K-chunks folded into C with the accumulate flag -- the
+// reference's XOR / OR fold of partial block products (engine.cpp:81-84).
+constexpr uint64_t kMaxTensorKWords = (uint64_t(1) << 22) / 64;  // 2^22 bits per launch
+
 int launch_cubic_dispatch(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt,
                           uint64_t* dC, uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2,
                           bool accumulate, cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch,
                           uint64_t sC_batch) {
+    if (resolve_kernel(kernel) != BMMGPU_KERNEL_LOP3 && kw > kMaxTensorKWords) {
+        for (uint64_t w0 = 0; w0 < kw; w0 += kMaxTensorKWords) {
+            const int st = launch_cubic_kernel(kernel, dA + w0, lda, dBt + w0, ldbt, dC, ldc, m_pad, n_pad,
+                                               std::min(kMaxTensorKWords, kw - w0), gf2, accumulate || w0 > 0,
+                                               stream, batch, sA_batch, sB_batch, sC_batch);
+            if (st) return st;
+        }
+        return kOk;
+    }
+    return launch_cubic_kernel(kernel, dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream, batch,
+                               sA_batch, sB_batch, sC_batch);
+}
+
+int launch_cubic_kernel(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt,
+                        uint64_t* dC, uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2,
+                        bool accumulate, cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch,
+                        uint64_t sC_batch) {
     switch (resolve_kernel(kernel)) {
         case BMMGPU_KERNEL_LOP3:
             return launch_cubic_lop3(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream, batch,

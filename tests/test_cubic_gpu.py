@@ -215,3 +215,37 @@ def test_device_api_batched(engine, oracle):
             for i in range(batch):
                 got = dC[i].cpu().numpy().view(np.uint64)[:L, : L // 64].ravel()
                 assert np.array_equal(got, oracle.multiply_cubic(As[i], Bs[i], L, L, L, ring)), (kernel, ring, i)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_inner_dimension_beyond_fp32_exact_range(engine, kernel):
+    """K = 2^23 + 2^20 bits: counts up to ~9.4e6 exceed the 2^23 the tensor-core kernels
+    keep exact in fp32, so the dispatcher folds K-chunks of 2^22 bits (the reference's
+    XOR / OR fold of partial products).  A row i = ones on [0, K - 3i), B column j =
+    ones on [0, K - 37j): count = K - max(3i, 37j), parity known in closed form; the
+    last row of A is zero (Boolean zeros)."""
+    bmm = engine
+    m = n = 256
+    K = (1 << 23) + (1 << 20)
+    W = K // 64
+    A = np.full((m, W), np.uint64(0xFFFFFFFFFFFFFFFF), dtype=np.uint64)
+    for i in range(m):
+        L = K - 3 * i if i < m - 1 else 0
+        A[i, L // 64 + 1:] = 0
+        if L // 64 < W:
+            A[i, L // 64] = np.uint64((1 << (L % 64)) - 1)
+    B = np.full((K, n // 64), np.uint64(0xFFFFFFFFFFFFFFFF), dtype=np.uint64)
+    tail = 37 * n
+    ks = np.arange(K - tail, K)
+    cols = np.minimum(n, -(-(K - ks) // 37))  # columns j with 37 j < K - k
+    bits = (np.arange(n)[None, :] < cols[:, None])
+    B[K - tail:] = np.packbits(bits, axis=1, bitorder="little").view(np.uint64)
+    i = np.arange(m)[:, None]
+    j = np.arange(n)[None, :]
+    count = np.where(i == m - 1, 0, K - np.maximum(3 * i, 37 * j))
+    for ring in (GF2, BOOL):
+        want_bits = (count % 2 == 1) if ring == GF2 else (count > 0)
+        want = np.packbits(want_bits, axis=1, bitorder="little").view(np.uint64).ravel()
+        got = bmm.multiply_cubic(bmm.BitMatrix(m, K, A.ravel()), bmm.BitMatrix(K, n, B.ravel()),
+                                 bmm.Semiring(ring), kernel=kernel)
+        assert np.array_equal(got.words, want), (kernel, ring)
