@@ -89,6 +89,15 @@ int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, 
 int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int32_t algo,
                     const bmmgpu_plan* plan, int32_t semiring, const bmmgpu_opts* opts);
 
+/* bmm::multiply_alt on interleaved vectors already in the scheme's basis (host
+ * buffers of 4^depth * 64 words laid out [4]*depth [4096]; right operand blocks
+ * stored transposed, reference bitmatrix.cpp:112-173): c_hat =
+ * chi^-1(phi^-1 a_hat . psi^-1 b_hat), computed on one device (the lowest bit of
+ * opts->device_mask).  Replaces bmm::multiply_alt (reference engine.cpp:293-349) and
+ * is the solve stage of the host pipeline (pipeline.cpp:310). */
+int bmmgpu_multiply_alt(const uint64_t* a_hat, const uint64_t* b_hat, uint64_t* c_hat, int32_t depth, int32_t algo,
+                        const bmmgpu_opts* opts);
+
 /* In-place basis change of an interleaved vector (host buffer of total_words
  * words laid out [4]*levels ... [inner]): factor 0 phi, 1 psi, 2 chi of the
  * scheme of `algo`; inverse != 0 applies the factor's inverse.  Each level is
@@ -156,6 +165,12 @@ int bmmgpu_block_timer_read(double* ms, uint64_t* launches);
 
 /* Number of kernel launches the last host-API call made on its devices. */
 uint64_t bmmgpu_last_launch_count(void);
+
+/* Page-locked host memory (cudaHostAlloc, portable across devices) for buffers
+ * the host-API calls copy from / into at full link speed: the host pipeline's
+ * per-worker sub-instance buffers, callers' operand staging. */
+int bmmgpu_host_alloc(uint64_t bytes, void** ptr);
+int bmmgpu_host_free(void* ptr);
 
 /* Host->device and device->host bytes the last host-API call copied (operands,
  * re-streamed panels, results). */

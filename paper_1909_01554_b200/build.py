@@ -22,7 +22,7 @@ CUDA_HOME = Path(NVCC).resolve().parent.parent
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CUDA_SOURCES = ["capi.cu", "transpose.cu", "cubic_lop3.cu", "cubic_umma.cu", "cubic_umma2.cu", "cubic_umma2np.cu", "alt.cu", "stream.cu"]
-HOST_SOURCES = ["host/bitmatrix.cpp", "host/engine.cpp"]
+HOST_SOURCES = ["host/bitmatrix.cpp", "host/engine.cpp", "host/pipeline.cpp"]
 
 LIB_GPU = HERE / "libbmmgpu.so"
 LIB_HOST = HERE / "libbmm_b200.so"

@@ -874,7 +874,10 @@ __global__ void mode_step_in_place_kernel(uint64_t* __restrict__ v, uint64_t out
 
 }  // namespace
 
-int interleaved_basis_change(uint64_t* words, uint64_t total_words, int levels, int algo, int factor, int inverse) {
+// In-place basis change of an interleaved vector already on the device: factor 0 phi,
+// 1 psi, 2 chi of the scheme; one pass per level (reference yates.cpp:143-172).
+int interleaved_basis_change_dev(uint64_t* d, uint64_t total_words, int levels, int algo, int factor, int inverse,
+                                 cudaStream_t stream) {
     const Scheme* sc = scheme_for(algo);
     if (!sc || factor < 0 || factor > 2 || levels < 0) {
         set_error("basis change: unknown scheme or factor");
@@ -891,19 +894,140 @@ int interleaved_basis_change(uint64_t* words, uint64_t total_words, int levels, 
         s.t[i] = p.target;
         s.s[i] = p.source;
     }
-    DevMem d;
-    int rc;
-    if ((rc = d.alloc(total_words * 8, nullptr))) return rc;
-    BMMGPU_CUDA_TRY(cudaMemcpy(d.p, words, total_words * 8, cudaMemcpyHostToDevice));
     uint64_t outer = 1;
     for (int l = 0; l < levels; ++l) {
         const uint64_t inner = total_words / (outer * 4);
-        mode_step_in_place_kernel<<<grid_for(outer * inner), 256>>>(d.u(), outer, inner, s);
+        mode_step_in_place_kernel<<<grid_for(outer * inner), 256, 0, stream>>>(d, outer, inner, s);
         count_launch();
         BMMGPU_CUDA_TRY(cudaGetLastError());
         outer *= 4;
     }
-    BMMGPU_CUDA_TRY(cudaMemcpy(words, d.p, total_words * 8, cudaMemcpyDeviceToHost));
+    return kOk;
+}
+
+int interleaved_basis_change(uint64_t* words, uint64_t total_words, int levels, int algo, int factor, int inverse) {
+    DevMem d;
+    int rc;
+    if ((rc = d.alloc(total_words * 8, nullptr))) return rc;
+    BMMGPU_CUDA_TRY(memcpy_counted(d.p, words, total_words * 8, cudaMemcpyHostToDevice, nullptr));
+    if ((rc = interleaved_basis_change_dev(d.u(), total_words, levels, algo, factor, inverse, nullptr))) return rc;
+    BMMGPU_CUDA_TRY(memcpy_counted(words, d.p, total_words * 8, cudaMemcpyDeviceToHost, nullptr));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(nullptr));
+    return kOk;
+}
+
+namespace {
+
+// Interleave bit spread: bit i of x -> bit 2i.
+__device__ __forceinline__ uint64_t spread_bits(uint64_t x) {
+    x &= 0xFFFFFFFFull;
+    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
+}
+
+// Block permutation between the interleaved vector (64-word blocks in Morton order:
+// level-l row digit at bit 2l+1, column digit at bit 2l, reference bitmatrix.cpp
+// interleaved_bit_index / to_interleaved / from_interleaved 112-173) and a row-major
+// matrix of nb x nb blocks (row stride ld words).  One thread per (block row, row,
+// block column) word, block column fastest: the row-major side is coalesced.
+//   swap = 0: row-major block (bi, bj) <-> vector block morton(bi, bj)  (left operand, result)
+//   swap = 1: row-major block (bi, bj) <-> vector block morton(bj, bi)  (right operand
+//             straight into Bt: Bt block (p, q) = B block (q, p) transposed = the stored
+//             block, since the vector holds right-operand blocks transposed)
+__global__ void block_permute_kernel(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, uint64_t nb,
+                                     uint64_t ld, int to_rowmajor, int swap) {
+    const uint64_t total = nb * 64 * nb;
+    for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t bj = idx % nb;
+        const uint64_t R = idx / nb;  // row of the row-major matrix
+        const uint64_t bi = R >> 6, r = R & 63;
+        const uint64_t mb = swap ? (spread_bits(bj) << 1) | spread_bits(bi) : (spread_bits(bi) << 1) | spread_bits(bj);
+        const uint64_t vi = mb * 64 + r, mi = R * ld + bj;
+        if (to_rowmajor)
+            dst[mi] = src[vi];
+        else
+            dst[vi] = src[mi];
+    }
+}
+
+int launch_block_permute(const uint64_t* src, uint64_t* dst, uint64_t nb, uint64_t ld, bool to_rowmajor, bool swap,
+                         cudaStream_t s) {
+    const uint64_t total = nb * 64 * nb;
+    block_permute_kernel<<<grid_for(total), 256, 0, s>>>(src, dst, nb, ld, to_rowmajor ? 1 : 0, swap ? 1 : 0);
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaGetLastError());
+    return kOk;
+}
+
+}  // namespace
+
+// bmm::multiply_alt on interleaved host vectors, entirely on one device
+// (reference engine.cpp:293-349): c_hat = chi^-1( phi^-1 a_hat . psi^-1 b_hat ).
+// Upload, inverse basis changes (K4), Morton -> row-major / Bt block permutes, the
+// fast product (folded coefficients), permute back, inverse chi, download.
+int multiply_alt_interleaved(const uint64_t* a_hat, const uint64_t* b_hat, uint64_t* c_hat, int depth, int algo,
+                             int kernel, int leaf_log2, int device, double* timing_ms) {
+    BMMGPU_CUDA_TRY(cudaSetDevice(device));
+    const uint64_t n = 64ull << depth, w = n / 64, nb = n / 64, total = n * w;
+    kernel = resolve_kernel(kernel);
+    uint64_t gm, gn, gk;
+    int st;
+    if ((st = granularity(kernel, &gm, &gn, &gk))) return st;
+    const int e = alt_levels(n, leaf_log2);
+    const uint64_t rows_pad = round_up(n, std::max(gm, gn)), kw = round_up(w, gk / 64), cw = rows_pad / 64;
+    cudaStream_t s;
+    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct G {
+        cudaStream_t s;
+        ~G() { cudaStreamDestroy(s); }
+    } guard{s};
+    DevMem dV, dA, dBt, dC;
+    if ((st = dV.alloc(total * 8, s)) || (st = dA.alloc(rows_pad * kw * 8, s)) ||
+        (st = dBt.alloc(round_up(rows_pad, 256) * kw * 8, s)) || (st = dC.alloc(rows_pad * cw * 8, s)))
+        return st;
+    BMMGPU_CUDA_TRY(cudaMemsetAsync(dA.p, 0, rows_pad * kw * 8, s));
+    BMMGPU_CUDA_TRY(cudaMemsetAsync(dBt.p, 0, round_up(rows_pad, 256) * kw * 8, s));
+    count_launch(2);
+    cudaEvent_t e0, e1;
+    BMMGPU_CUDA_TRY(cudaEventCreate(&e0));
+    BMMGPU_CUDA_TRY(cudaEventCreate(&e1));
+    struct TE {
+        cudaEvent_t a, b;
+        ~TE() {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } te{e0, e1};
+    BMMGPU_CUDA_TRY(cudaEventRecord(e0, s));
+    BMMGPU_CUDA_TRY(memcpy_counted(dV.p, a_hat, total * 8, cudaMemcpyHostToDevice, s));
+    if ((st = interleaved_basis_change_dev(dV.u(), total, depth, algo, 0, 1, s)) ||
+        (st = launch_block_permute(dV.u(), dA.u(), nb, kw, true, false, s)))
+        return st;
+    BMMGPU_CUDA_TRY(memcpy_counted(dV.p, b_hat, total * 8, cudaMemcpyHostToDevice, s));
+    float ms_a = 0.f;
+    if ((st = interleaved_basis_change_dev(dV.u(), total, depth, algo, 1, 1, s)) ||
+        (st = launch_block_permute(dV.u(), dBt.u(), nb, kw, true, true, s)))
+        return st;
+    if (e == 0)
+        st = launch_cubic(kernel, dA.u(), kw, dBt.u(), kw, dC.u(), cw, rows_pad, rows_pad, kw, true, false, s, 1, 0, 0,
+                          0);
+    else
+        st = alt_multiply_device(dA.u(), kw, dBt.u(), kw, dC.u(), cw, n, algo, e, choose_serial_levels(n, e), kernel,
+                                 s);
+    if (st) return st;
+    if ((st = launch_block_permute(dC.u(), dV.u(), nb, cw, false, false, s)) ||
+        (st = interleaved_basis_change_dev(dV.u(), total, depth, algo, 2, 1, s)))
+        return st;
+    BMMGPU_CUDA_TRY(memcpy_counted(c_hat, dV.p, total * 8, cudaMemcpyDeviceToHost, s));
+    BMMGPU_CUDA_TRY(cudaEventRecord(e1, s));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaEventElapsedTime(&ms_a, e0, e1);
+    if (timing_ms) *timing_ms = ms_a;
     return kOk;
 }
 
@@ -914,6 +1038,32 @@ extern "C" int bmmgpu_dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, ui
                                    void* stream) {
     return bmmgpu::dev_multiply(dA, lda, dBt, ldbt, dC, ldc, n, algo, leaf_log2, kernel,
                                 static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int bmmgpu_multiply_alt(const uint64_t* a_hat, const uint64_t* b_hat, uint64_t* c_hat, int32_t depth,
+                                   int32_t algo, const bmmgpu_opts* opts) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        bmmgpu::set_error("no CUDA device available; the bit-matrix engine has no CPU fallback");
+        return bmmgpu::kEnodev;
+    }
+    if (!bmmgpu::scheme_for(algo)) {
+        bmmgpu::set_error("no bilinear scheme for this algorithm");
+        return bmmgpu::kEinval;
+    }
+    if (depth < 0 || depth > 16) {
+        bmmgpu::set_error("multiply_alt: depth out of range");
+        return bmmgpu::kEinval;
+    }
+    int device = 0;
+    const uint32_t mask = opts ? opts->device_mask : 0u;
+    if (mask) device = __builtin_ctz(mask);
+    if (device >= count) {
+        bmmgpu::set_error("device_mask names a missing device");
+        return bmmgpu::kEinval;
+    }
+    return bmmgpu::multiply_alt_interleaved(a_hat, b_hat, c_hat, depth, algo, opts ? opts->kernel : 0,
+                                            opts ? opts->leaf_log2 : 0, device, opts ? opts->timing_ms : nullptr);
 }
 
 extern "C" int bmmgpu_basis_change(uint64_t* words, uint64_t total_words, int32_t levels, int32_t algo,

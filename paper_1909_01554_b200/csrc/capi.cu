@@ -76,6 +76,112 @@ void count_copy(cudaMemcpyKind kind, uint64_t bytes) {
     if (kind == cudaMemcpyDeviceToHost) g_d2h.fetch_add(bytes, std::memory_order_relaxed);
 }
 
+namespace {
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Two 64 MiB page-locked slots per device, allocated on first use and kept.
+struct Stager {
+    static constexpr size_t kSlot = size_t(64) << 20;
+    std::mutex mu;
+    void* slot[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    bool ready = false;
+    bool init() {
+        if (ready) return true;
+        for (int i = 0; i < 2; ++i) {
+            if (cudaHostAlloc(&slot[i], kSlot, cudaHostAllocPortable) != cudaSuccess) return false;
+            if (cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming) != cudaSuccess) return false;
+        }
+        ready = true;
+        return true;
+    }
+};
+Stager g_stagers[16];
+
+// `rows` rows of `width` bytes from src (pitch spitch) to dst (pitch dpitch), split
+// across host threads (8 MiB per thread, at most 4)
+void copy_rows(char* dst, size_t dpitch, const char* src, size_t spitch, size_t width, size_t rows) {
+    const size_t bytes = rows * width;
+    const unsigned n_thr = unsigned(std::min<size_t>(4, std::max<size_t>(1, bytes >> 23)));
+    auto part = [&](size_t a, size_t b) {
+        for (size_t r = a; r < b; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, width);
+    };
+    if (n_thr == 1) {
+        part(0, rows);
+        return;
+    }
+    std::vector<std::thread> thr;
+    const size_t step = (rows + n_thr - 1) / n_thr;
+    for (unsigned i = 0; i < n_thr; ++i) thr.emplace_back(part, std::min(rows, i * step), std::min(rows, (i + 1) * step));
+    for (auto& t : thr) t.join();
+}
+
+}  // namespace
+
+cudaError_t memcpy2d_counted(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                             cudaMemcpyKind kind, cudaStream_t s) {
+    count_copy(kind, uint64_t(width) * height);
+    const bool h2d = kind == cudaMemcpyHostToDevice, d2h = kind == cudaMemcpyDeviceToHost;
+    const void* host = h2d ? src : d2h ? static_cast<const void*>(dst) : nullptr;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static const bool disabled = getenv("BMMGPU_NO_STAGING") != nullptr;
+    if (disabled || !host || width * height < (size_t(16) << 20) || width > Stager::kSlot || dev < 0 || dev >= 16 ||
+        is_pinned(host))
+        return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, s);
+    Stager& st = g_stagers[dev];
+    std::lock_guard<std::mutex> lk(st.mu);
+    if (!st.init()) return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, s);
+    const size_t rows_per = std::max<size_t>(1, Stager::kSlot / width);
+    cudaError_t e = cudaSuccess;
+    int k = 0;
+    if (h2d) {
+        for (size_t r0 = 0; r0 < height; r0 += rows_per, k ^= 1) {
+            const size_t r1 = std::min(height, r0 + rows_per);
+            if ((e = cudaEventSynchronize(st.done[k])) != cudaSuccess) return e;  // slot's last DMA finished
+            copy_rows(static_cast<char*>(st.slot[k]), width, static_cast<const char*>(src) + r0 * spitch, spitch, width,
+                      r1 - r0);
+            if ((e = cudaMemcpy2DAsync(static_cast<char*>(dst) + r0 * dpitch, dpitch, st.slot[k], width, width,
+                                       r1 - r0, kind, s)) != cudaSuccess ||
+                (e = cudaEventRecord(st.done[k], s)) != cudaSuccess)
+                return e;
+        }
+        return cudaSuccess;
+    }
+    // D2H: DMA chunk i + 1 into one slot while host threads drain chunk i from the other
+    size_t pending_r0 = 0, pending_r1 = 0;
+    int pending = -1;
+    for (size_t r0 = 0; r0 < height; r0 += rows_per, k ^= 1) {
+        const size_t r1 = std::min(height, r0 + rows_per);
+        if ((e = cudaMemcpy2DAsync(st.slot[k], width, static_cast<const char*>(src) + r0 * spitch, spitch, width,
+                                   r1 - r0, kind, s)) != cudaSuccess ||
+            (e = cudaEventRecord(st.done[k], s)) != cudaSuccess)
+            return e;
+        if (pending >= 0) {
+            if ((e = cudaEventSynchronize(st.done[pending])) != cudaSuccess) return e;
+            copy_rows(static_cast<char*>(dst) + pending_r0 * dpitch, dpitch,
+                      static_cast<const char*>(st.slot[pending]), width, width, pending_r1 - pending_r0);
+        }
+        pending = k;
+        pending_r0 = r0;
+        pending_r1 = r1;
+    }
+    if (pending >= 0) {
+        if ((e = cudaEventSynchronize(st.done[pending])) != cudaSuccess) return e;
+        copy_rows(static_cast<char*>(dst) + pending_r0 * dpitch, dpitch, static_cast<const char*>(st.slot[pending]),
+                  width, width, pending_r1 - pending_r0);
+    }
+    return cudaSuccess;
+}
+
 int resolve_kernel(int kernel) {
     // The tcgen05 kind::mxf4 kernel beats the LOP3 kernel 3.4-3.8x in bop/s on
     // B200 (profiles/r01), so it is the default block product.
@@ -326,6 +432,29 @@ int bmmgpu_slab_rows(uint64_t m, uint32_t parts, uint32_t index, uint64_t gran, 
 }
 const char* bmmgpu_version(void) { return "bmm-b200 0.1 (sm_100a)"; }
 uint64_t bmmgpu_last_launch_count(void) { return g_launches.load(); }
+
+int bmmgpu_host_alloc(uint64_t bytes, void** ptr) {
+    if (!ptr) {
+        set_error("bmmgpu_host_alloc: null output pointer");
+        return kEinval;
+    }
+    *ptr = nullptr;
+    const cudaError_t e = cudaHostAlloc(ptr, bytes ? bytes : 8, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+        *ptr = nullptr;
+        return kEcuda;
+    }
+    return kOk;
+}
+
+int bmmgpu_host_free(void* ptr) {
+    if (ptr && cudaFreeHost(ptr) != cudaSuccess) {
+        set_error("cudaFreeHost failed");
+        return kEcuda;
+    }
+    return kOk;
+}
 
 int bmmgpu_last_copy_bytes(uint64_t* h2d, uint64_t* d2h) {
     if (h2d) *h2d = g_h2d.load();

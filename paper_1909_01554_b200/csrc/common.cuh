@@ -13,16 +13,17 @@ void set_error(const std::string& msg);
 void count_launch(uint64_t n = 1);
 // Host<->device bytes moved by the host-API drivers (bmmgpu_last_copy_bytes).
 void count_copy(cudaMemcpyKind kind, uint64_t bytes);
-inline cudaError_t memcpy2d_counted(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
-                                    size_t height, cudaMemcpyKind kind, cudaStream_t s) {
-    count_copy(kind, uint64_t(width) * height);
-    return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, s);
-}
+// Host<->device copies of the host-API drivers.  Page-locked host buffers go straight
+// to the DMA engines (asynchronous on `s`); large pageable ones (the reference API's
+// std::vector storage) are staged through pinned double buffers, with host threads
+// filling / draining one slot while the DMA engine moves the other -- host-synchronous
+// for the pageable side, like the runtime's own pageable copies, but at a multiple of
+// their bandwidth.
+cudaError_t memcpy2d_counted(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                             cudaMemcpyKind kind, cudaStream_t s);
 inline cudaError_t memcpy_counted(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
-    count_copy(kind, bytes);
-    return cudaMemcpyAsync(dst, src, bytes, kind, s);
+    return memcpy2d_counted(dst, bytes, src, bytes, bytes, 1, kind, s);
 }
-
 #define BMMGPU_CUDA_TRY(expr)                                                                     \
     do {                                                                                          \
         cudaError_t _e = (expr);                                                                  \

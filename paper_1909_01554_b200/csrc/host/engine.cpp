@@ -160,6 +160,30 @@ void basis_change(BitVectorTensor& v, const Decomposition& d, BasisFactor which,
     }
 }
 
+namespace detail {
+
+// The device solve of multiply_alt on raw interleaved buffers of depth `depth` (4^depth
+// blocks of 64 words), on CUDA device `device`, with the reference's tallies: the
+// whole sub-product runs on the GPU (inverse basis changes, Morton block permutes, the
+// fast product, permute back, inverse chi).  Shared by multiply_alt and the pipeline's
+// solve stage (reference pipeline.cpp:310).
+void solve_alt(const std::uint64_t* a_hat, const std::uint64_t* b_hat, std::uint64_t* c_hat, int depth,
+               const Decomposition& d, OpCounter* counter, int device) {
+    bmmgpu_opts o{};
+    o.device_mask = 1u << device;
+    check(bmmgpu_multiply_alt(a_hat, b_hat, c_hat, depth, algo_id(d.which), &o));
+    if (counter) {
+        const std::uint64_t kernels = ipow(7, depth);
+        counter->add_kernels(kernels);
+        counter->add_ands(kernels * kBlockBits);
+        counter->add_xors(predicted_additions(d, depth, CostPart::LinearCombinations) * kBlockWords);
+    }
+}
+
+}  // namespace detail
+
+// multiply_alt is the bilinear map (a_hat, b_hat) -> chi^-1( phi^-1 a_hat . psi^-1 b_hat )
+// in interleaved form (reference engine.cpp:293-349).
 BitVectorTensor multiply_alt(const BitVectorTensor& a_hat, const BitVectorTensor& b_hat, const Decomposition& d,
                              const LayerPlan& plan, OpCounter* counter) {
     if (plan.d_serial < 0 || plan.d_parallel < 0 || plan.d_inner != 1 || plan.workers < 1)
@@ -171,32 +195,10 @@ BitVectorTensor multiply_alt(const BitVectorTensor& a_hat, const BitVectorTensor
         throw std::invalid_argument("operands are not interleaved for this plan");
     if (a_hat.words.size() * kWordBits != a_hat.bit_length() || b_hat.words.size() * kWordBits != b_hat.bit_length())
         throw std::invalid_argument("operand storage does not match its modes");
-    const int algo = algo_id(d.which);
-    // multiply_alt is the bilinear map (a_hat, b_hat) -> chi^-1( phi^-1 a_hat . psi^-1 b_hat )
-    // in interleaved form; the GPU computes the standard-basis product in between.
-    LayerPlan p;
-    p.d_serial = depth;
-    BitVectorTensor a = a_hat, b = b_hat;
-    if (!factor_identity(d, BasisFactor::Phi))
-        check(bmmgpu_basis_change(a.words.data(), a.words.size(), depth, algo, 0, 1));
-    if (!factor_identity(d, BasisFactor::Psi))
-        check(bmmgpu_basis_change(b.words.data(), b.words.size(), depth, algo, 1, 1));
-    const BitMatrix am = from_interleaved(a, p, Operand::Left);
-    const BitMatrix bm = from_interleaved(b, p, Operand::Right);
-    const std::uint64_t n = p.matrix_dim();
-    BitMatrix cm = BitMatrix::zeros(n, n);
-    bmmgpu_plan gp{0, depth, 0, 1, 1};
-    check(bmmgpu_multiply(am.words.data(), bm.words.data(), cm.words.data(), n, algo, &gp, BMMGPU_GF2_XOR_AND,
-                          nullptr));
-    BitVectorTensor c = to_interleaved(cm, p, Operand::Result);
-    if (!factor_identity(d, BasisFactor::Chi))
-        check(bmmgpu_basis_change(c.words.data(), c.words.size(), depth, algo, 2, 1));
-    if (counter) {
-        const std::uint64_t kernels = ipow(7, depth);
-        counter->add_kernels(kernels);
-        counter->add_ands(kernels * kBlockBits);
-        counter->add_xors(predicted_additions(d, depth, CostPart::LinearCombinations) * kBlockWords);
-    }
+    BitVectorTensor c;
+    c.mode_lengths = a_hat.mode_lengths;
+    c.words.assign(a_hat.words.size(), 0);
+    detail::solve_alt(a_hat.words.data(), b_hat.words.data(), c.words.data(), depth, d, counter, 0);
     return c;
 }
 

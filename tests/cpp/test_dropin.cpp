@@ -16,9 +16,12 @@
 #include "bmm/counter.hpp"
 #include "bmm/decomposition.hpp"
 #include "bmm/engine.hpp"
+#include "bmm/pipeline.hpp"
 #include "bmm/plan.hpp"
 
 using namespace bmm;
+using pipeline::SubInstanceIndex;
+using pipeline::SubvectorLocks;
 
 namespace {
 
@@ -95,6 +98,191 @@ void run(const char* name, const std::function<void()>& f) {
 }
 
 // ------------------------------------------------------------------ host cases
+// Coefficient rows of the schemes as the reference writes them (decomposition.cpp
+// 104-142 alt-si, 144-183 alt-chain): rows of alpha / beta = products, columns =
+// quadrants 00,01,10,11; rows of gamma = quadrants, columns = products.
+struct Coeffs {
+    const char* alpha[7];
+    const char* beta[7];
+    const char* gamma[4];
+};
+const Coeffs kAltSi = {{"1000", "0100", "0010", "0001", "1001", "0101", "0011"},
+                       {"1000", "0010", "1001", "0001", "0100", "0101", "0011"},
+                       {"1100000", "0000101", "0010010", "0101011"}};
+const Coeffs kAltChain = {{"1000", "0100", "0010", "0001", "1010", "0110", "0011"},
+                          {"1000", "0011", "0010", "0001", "0100", "0110", "1010"},
+                          {"1100000", "0110110", "0110101", "0001100"}};
+
+// Dense Kronecker power of a coefficient matrix (rows x cols strings), built by
+// explicit products of 0/1 matrices -- independent of the pipeline's digit walk.
+std::vector<std::vector<int>> kron_power(const char* const* rows, int r, int c, int levels) {
+    std::vector<std::vector<int>> k = {{1}};
+    for (int l = 0; l < levels; ++l) {
+        std::vector<std::vector<int>> nk(k.size() * r, std::vector<int>(k[0].size() * c));
+        for (std::size_t i = 0; i < k.size(); ++i)
+            for (std::size_t j = 0; j < k[0].size(); ++j)
+                for (int a = 0; a < r; ++a)
+                    for (int b = 0; b < c; ++b) nk[i * r + a][j * c + b] = k[i][j] & (rows[a][b] == '1');
+        k = std::move(nk);
+    }
+    return k;
+}
+
+std::vector<std::uint64_t> dense_combination(const BitVectorTensor& src, const std::vector<int>& coeff_row,
+                                             std::uint64_t inner) {
+    std::vector<std::uint64_t> out(inner, 0);
+    for (std::size_t g = 0; g < coeff_row.size(); ++g)
+        if (coeff_row[g])
+            for (std::uint64_t w = 0; w < inner; ++w) out[w] ^= src.words[g * inner + w];
+    return out;
+}
+
+void pipeline_host_cases() {
+    run("pipeline: sub-instance indexing and ownership", [] {
+        SubInstanceIndex h;
+        h.digits = {4, 4};
+        CHECK(h.flat() == 32 && SubInstanceIndex::from_flat(32, 2).digits == h.digits);
+        bool ok = true;
+        for (std::uint64_t f = 0; f < 343; ++f) {
+            const SubInstanceIndex x = SubInstanceIndex::from_flat(f, 3);
+            ok = ok && x.digits.size() == 3 && x.flat() == f && x.owner(5) == int(f % 5);
+        }
+        CHECK(ok);
+        CHECK(pipeline::sub_instance_count(plan_for(0, 0, 0)) == 1);
+        CHECK(pipeline::sub_instance_count(plan_for(1, 1, 2)) == 49);
+        std::vector<int> owned(8, 0);
+        for (std::uint64_t f = 0; f < 2401; ++f) ++owned[SubInstanceIndex::from_flat(f, 4).owner(8)];
+        CHECK(owned[0] == 301);
+        for (int l = 1; l < 8; ++l) CHECK(owned[l] == 300);
+        CHECK(throws<std::invalid_argument>([&] { (void)h.owner(0); }));
+    });
+    run("pipeline: generation is the Kronecker row of alpha / beta", [] {
+        for (auto [which, co] : {std::pair{Builtin::AltSelfInverse, &kAltSi}, std::pair{Builtin::AltChaining, &kAltChain}}) {
+            const Decomposition& d = builtin(which);
+            const LayerPlan plan = plan_for(0, 0, 2);
+            const BitVectorTensor a_hat = random_hat({4, 4, kBlockBits}, 201), b_hat = random_hat({4, 4, kBlockBits}, 202);
+            const std::uint64_t inner = a_hat.words.size() / 16;
+            const auto ka = kron_power(co->alpha, 7, 4, 2), kb = kron_power(co->beta, 7, 4, 2);
+            bool ok = true;
+            for (std::uint64_t f = 0; f < 49; ++f) {
+                const SubInstanceIndex h = SubInstanceIndex::from_flat(f, 2);
+                ok = ok && pipeline::generate_left(a_hat, h, d, plan) == dense_combination(a_hat, ka[f], inner);
+                ok = ok && pipeline::generate_right(b_hat, h, d, plan) == dense_combination(b_hat, kb[f], inner);
+            }
+            CHECK(ok);
+        }
+        const Decomposition& asi = builtin(Builtin::AltSelfInverse);
+        const BitVectorTensor a_hat = random_hat({4, 4, kBlockBits}, 203);
+        OpCounter c;
+        (void)pipeline::generate_left(a_hat, SubInstanceIndex::from_flat(4, 1), asi, plan_for(1, 0, 1), &c);
+        CHECK(c.word_xors == a_hat.words.size() / 4);  // alpha row 4 = 1001: one fold
+        SubInstanceIndex wrong;
+        wrong.digits = {1};
+        CHECK(throws<std::invalid_argument>([&] { (void)pipeline::generate_left(a_hat, wrong, asi, plan_for(0, 0, 2)); }));
+        wrong.digits = {9};
+        CHECK(throws<std::invalid_argument>([&] { (void)pipeline::generate_left(a_hat, wrong, asi, plan_for(1, 0, 1)); }));
+    });
+    run("pipeline: aggregation folds into gamma-selected outputs under locks", [] {
+        for (auto [which, co] : {std::pair{Builtin::AltSelfInverse, &kAltSi}, std::pair{Builtin::AltChaining, &kAltChain}}) {
+            const Decomposition& d = builtin(which);
+            const LayerPlan plan = plan_for(0, 0, 1);
+            const BitVectorTensor base = random_hat({4, kBlockBits}, 211);
+            const std::uint64_t inner = base.words.size() / 4;
+            std::mt19937_64 rng(212);
+            std::vector<std::uint64_t> q(inner);
+            for (auto& w : q) w = rng();
+            bool ok = true;
+            for (std::uint64_t f = 0; f < 7; ++f) {
+                BitVectorTensor c = base;
+                SubvectorLocks locks(1);
+                pipeline::aggregate(c, SubInstanceIndex::from_flat(f, 1), q, d, plan, locks);
+                ok = ok && locks.violations() == 0;
+                for (std::uint64_t m = 0; m < 4; ++m)
+                    for (std::uint64_t w = 0; w < inner; ++w)
+                        ok = ok && c.words[m * inner + w] ==
+                                       (base.words[m * inner + w] ^ (co->gamma[m][f] == '1' ? q[w] : 0));
+            }
+            CHECK(ok);
+            BitVectorTensor c = base;
+            SubvectorLocks locks(1), small(0);
+            std::vector<std::uint64_t> short_q(inner - 1, 0);
+            CHECK(throws<std::invalid_argument>(
+                [&] { pipeline::aggregate(c, SubInstanceIndex::from_flat(0, 1), short_q, d, plan, locks); }));
+            CHECK(throws<std::invalid_argument>(
+                [&] { pipeline::aggregate(c, SubInstanceIndex::from_flat(0, 1), q, d, plan, small); }));
+        }
+    });
+}
+
+void pipeline_gpu_cases() {
+    run("pipeline: sequential host layer equals the single call", [] {
+        for (Builtin which : {Builtin::AltSelfInverse, Builtin::AltChaining}) {
+            const Decomposition& d = builtin(which);
+            const BitVectorTensor a_hat = random_hat({4, 4, kBlockBits}, 221), b_hat = random_hat({4, 4, kBlockBits}, 222);
+            const LayerPlan host_plan = plan_for(0, 1, 1), sub_plan = plan_for(0, 1);
+            BitVectorTensor c_hat;
+            c_hat.mode_lengths = a_hat.mode_lengths;
+            c_hat.words.assign(a_hat.words.size(), 0);
+            SubvectorLocks locks(1);
+            for (std::uint64_t f = 0; f < 7; ++f) {
+                const SubInstanceIndex h = SubInstanceIndex::from_flat(f, 1);
+                BitVectorTensor t, s;
+                t.mode_lengths = s.mode_lengths = {4, kBlockBits};
+                t.words = pipeline::generate_left(a_hat, h, d, host_plan);
+                s.words = pipeline::generate_right(b_hat, h, d, host_plan);
+                pipeline::aggregate(c_hat, h, multiply_alt(t, s, d, sub_plan).words, d, host_plan, locks);
+            }
+            CHECK(locks.violations() == 0);
+            CHECK(c_hat == multiply_alt(a_hat, b_hat, d, plan_for(1, 1)));
+        }
+    });
+    run("pipeline: coordinate equals the single call, counts kernels", [] {
+        const Decomposition& asi = builtin(Builtin::AltSelfInverse);
+        const BitVectorTensor a2 = random_hat({4, 4, kBlockBits}, 231), b2 = random_hat({4, 4, kBlockBits}, 232);
+        const BitVectorTensor want2 = multiply_alt(a2, b2, asi, plan_for(2, 0));
+        for (int workers : {1, 3}) {
+            CHECK(pipeline::coordinate(a2, b2, asi, plan_for(0, 1, 1), workers) == want2);
+            CHECK(pipeline::coordinate(a2, b2, asi, plan_for(0, 0, 2), workers) == want2);
+        }
+        const BitVectorTensor a0 = random_hat({4, kBlockBits}, 233), b0 = random_hat({4, kBlockBits}, 234);
+        CHECK(pipeline::coordinate(a0, b0, asi, plan_for(1, 0, 0), 2) == multiply_alt(a0, b0, asi, plan_for(1, 0)));
+        OpCounter counter;
+        pipeline::coordinate(a2, b2, asi, plan_for(0, 1, 1), 2, &counter);
+        CHECK(counter.kernel_invocations == 49 && counter.word_ands == 49 * kBlockBits);
+    });
+    run("pipeline: deterministic across workers and runs, exactly once, no lock overlap", [] {
+        const Decomposition& ach = builtin(Builtin::AltChaining);
+        const BitVectorTensor a = random_hat({4, 4, 4, kBlockBits}, 241), b = random_hat({4, 4, 4, kBlockBits}, 242);
+        const BitVectorTensor want = multiply_alt(a, b, ach, plan_for(2, 1));
+        for (int workers : {1, 2, 4, 8}) CHECK(pipeline::coordinate(a, b, ach, plan_for(0, 1, 2), workers) == want);
+        for (int run = 0; run < 5; ++run) {
+            pipeline::PipelineStats st;
+            CHECK(pipeline::coordinate(a, b, ach, plan_for(0, 1, 2), 4, nullptr, &st) == want);
+            CHECK(st.lock_violations == 0);
+        }
+        const Decomposition& asi = builtin(Builtin::AltSelfInverse);
+        pipeline::PipelineStats st;
+        pipeline::coordinate(a, b, asi, plan_for(1, 0, 2), 3, nullptr, &st);
+        bool once = st.prepared_left.size() == 49 && st.prepared_right.size() == 49 && st.aggregated.size() == 49;
+        for (std::size_t f = 0; once && f < 49; ++f)
+            once = st.prepared_left[f] == 1 && st.prepared_right[f] == 1 && st.aggregated[f] == 1;
+        CHECK(once && st.lock_violations == 0);
+        CHECK(throws<std::invalid_argument>([&] { (void)pipeline::coordinate(a, b, asi, plan_for(1, 0, 2), 0); }));
+        CHECK(throws<std::invalid_argument>([&] { (void)pipeline::coordinate(a, b, asi, plan_for(1, 1, 2), 2); }));
+    });
+    run("pipeline: full multiply with host levels", [] {
+        const BitMatrix a = BitMatrix::random(256, 256, 261), b = BitMatrix::random(256, 256, 262);
+        const BitMatrix want = multiply_cubic(a, b, Semiring::Gf2XorAnd);
+        LayerPlan p1 = plan_for(0, 1, 1), p2 = plan_for(0, 0, 2), p3 = plan_for(1, 0, 1);
+        p1.workers = 2;
+        p2.workers = 3;
+        p3.workers = 2;
+        CHECK(multiply(a, b, Algo::AltSelfInverse, p1, Semiring::Gf2XorAnd) == want);
+        CHECK(multiply(a, b, Algo::AltChaining, p2, Semiring::Gf2XorAnd) == want);
+        CHECK(multiply(a, b, Algo::StrassenWinograd, p3, Semiring::Gf2XorAnd) == want);
+    });
+}
+
 void host_cases() {
     run("zeros and padding", [] {
         BitMatrix m = BitMatrix::zeros(130, 130);
@@ -210,6 +398,7 @@ void host_cases() {
         CHECK(builtin(Builtin::AltChaining).traits.supports_chaining);
         CHECK(!builtin(Builtin::AltSelfInverse).traits.supports_chaining);
     });
+    pipeline_host_cases();
 }
 
 // ------------------------------------------------------------------ gpu cases
@@ -347,6 +536,7 @@ void gpu_cases() {
         CHECK(from_interleaved(ch, p, Operand::Result) == want);
         CHECK(throws<std::invalid_argument>([&] { (void)chain_multiply(ops, builtin(Builtin::AltSelfInverse), p); }));
     });
+    pipeline_gpu_cases();
 }
 
 }  // namespace

@@ -249,3 +249,29 @@ def test_inner_dimension_beyond_fp32_exact_range(engine, kernel):
         got = bmm.multiply_cubic(bmm.BitMatrix(m, K, A.ravel()), bmm.BitMatrix(K, n, B.ravel()),
                                  bmm.Semiring(ring), kernel=kernel)
         assert np.array_equal(got.words, want), (kernel, ring)
+
+
+def test_pageable_host_buffers_are_staged(engine, oracle):
+    """Large pageable operands (the reference API's std::vector storage) go through the
+    library's pinned staging slots: same bits as the call on page-locked buffers, and
+    rows checked independently."""
+    import torch
+    bmm = engine
+    m, k, n = 2048, 8192, 131072  # B 128 MiB and C 32 MiB: both directions staged
+    a = oracle.random(m, k, 301)
+    b = oracle.random(k, n, 302)
+    for ring in (GF2, BOOL):
+        got = bmm.multiply_cubic(bmm.BitMatrix(m, k, a), bmm.BitMatrix(k, n, b), bmm.Semiring(ring))
+        ha = torch.from_numpy(a.view(np.int64)).pin_memory()
+        hb = torch.from_numpy(b.view(np.int64)).pin_memory()
+        hc = torch.zeros(m * n // 64, dtype=torch.int64).pin_memory()
+        pinned = bmm.multiply_cubic(bmm.BitMatrix(m, k, ha.numpy().view(np.uint64)),
+                                    bmm.BitMatrix(k, n, hb.numpy().view(np.uint64)), bmm.Semiring(ring),
+                                    out=bmm.BitMatrix(m, n, hc.numpy().view(np.uint64)))
+        assert np.array_equal(got.words, pinned.words), ring
+        B = b.reshape(k, n // 64)
+        for i in (0, 777, m - 1):
+            bits = np.unpackbits(a.reshape(m, k // 64)[i].view(np.uint8), bitorder="little")[:k]
+            sel = B[np.flatnonzero(bits)]
+            want = np.bitwise_xor.reduce(sel, axis=0) if ring == GF2 else np.bitwise_or.reduce(sel, axis=0)
+            assert np.array_equal(got.words.reshape(m, n // 64)[i], want), (ring, i)
