@@ -3,12 +3,12 @@
 // kind::mxf4, M256 x N256 x K64 per instruction, f32 accumulators in TMEM),
 // persistent over all output tiles of all products of a batch.
 //
-// Contract and bit -> fp4 expansion exactly as cubic_umma.cu (reference
-// kernel64 + cubic_blocked, engine.cpp:34-100): each bit becomes one e2m1
-// element (x & 0x22222222 / (x>>2) & 0x22222222 -> 1.0, x & 0x11111111 /
-// (x>>2) & 0x11111111 -> 0.5, uniform UE8M0 block scales 1.0 / 2.0 per MMA),
-// exact 0/1 dot products accumulate in fp32, the epilogue takes the count's
-// parity (GF(2)) or non-zeroness (Boolean).
+// Contract and bit -> fp4 expansion as cubic_umma.cu (reference kernel64 +
+// cubic_blocked, engine.cpp:34-100): each bit becomes one e2m1 element
+// (x & 0x22222222 / (x>>2) & 0x22222222 -> 1.0, x & 0x11111111 / (x>>2) &
+// 0x11111111 -> 0.5, uniform UE8M0 block scales 1.0 / 2.0 per MMA), exact 0/1 dot
+// products accumulate in fp32 on top of a 2^23 bias written by one MMA per tile, and
+// the epilogue takes bit 0 (GF(2) parity) or the low 23 bits (Boolean non-zero).
 //
 // Why the pair: the single-CTA form is shared-memory bound -- producers write
 // the expanded operands with STS while the tensor core reads them back.  With
@@ -19,21 +19,25 @@
 // reads stay 128-B aligned and the producers' STS.128 are conflict free.
 //
 // Why persistent: one launch walks every tile (static round robin over the
-// 74 SM pairs), so TMEM allocation, barrier setup and scale-factor fill happen
-// once, the producers stream the next tile's stages while the current tile's
-// accumulator drains, and the MMA pauses only for the TMEM drain (the
-// accumulator takes 256 of the 512 TMEM columns and the constant scale
-// regions the rest, so there is one accumulator).  This is what makes the
-// short-K leaf products of the alternative-basis recursion efficient.
+// 74 SM pairs, raster groups of 12 row tiles), so TMEM allocation, barrier setup
+// and scale-factor fill happen once, the producers stream the next tile's stages
+// while the current tile's accumulator drains, and the MMA pauses only for the
+// drain (the accumulator takes 256 of the 512 TMEM columns and the constant scale
+// regions the rest, so there is one accumulator).  This is what makes the short-K
+// leaf products of the alternative-basis recursion efficient.
 //
-// Roles per CTA (480 threads, 115 registers):
+// Roles per CTA (480 threads):
 //   loader (warp 13, one lane; TMA): per superstage of 4 stages (1024 K bits) one
 //     3-D tensor-map box per operand, 128 rows x 128 bytes with the 128-byte swizzle,
-//     into a 2-slot packed ring (K tails zero-filled by the box bounds).  Without a
-//     tensor map (odd strides, K < 1024 bits) warps 13-14 do the same with cp.async
-//     and swizzled 16-byte destinations.  Keeping global loads out of the expander
-//     threads matters: their fence.proxy.async (MEMBAR.CTA) would wait for every load
-//     still in flight and serialise one L2 round trip per stage.
+//     into a 2-slot packed ring (K tails zero-filled by the box bounds).  Long-K
+//     launches wave-align the pairs (a loader starts tile j once every pair's loader
+//     has issued tile j - 1, global counter, bounded spin) and tag the loads with an
+//     L2 policy (the raster group's A panels evict_last, Bt panels evict_first): DRAM
+//     reads per n = 131072 launch 806 -> 112 GB, which buys SM clock under the power
+//     cap.  Without a tensor map (odd strides, K < 1024 bits) warps 13-14 load with
+//     cp.async and swizzled 16-byte destinations.  Keeping global loads out of the
+//     expander threads matters: their fence.proxy.async (MEMBAR.CTA) would wait for
+//     every load still in flight and serialise one L2 round trip per stage.
 //   expanders (warps 0-7): two groups of 4 warps take alternate stages, thread r of a
 //     group owns row r of A and of Bt; per superstage a warp reads its rows' bits for
 //     its two stages (conflict-free through the swizzle), frees the packed slot, then
@@ -42,13 +46,15 @@
 //     (remotely from the peer CTA).  While one group drains its stores through the
 //     proxy fence the other group's stores keep the shared-memory port busy.
 //   MMA (warp 8, leader CTA): the whole warp runs the loop so slots and descriptors
-//     stay warp-uniform (no per-instruction R2UR waterfall); an elected lane issues
-//     4 MMAs per stage, commits each stage to both CTAs' empty barriers and each tile
-//     to both CTAs' acc_full barriers.
-//   epilogue (warps 9-12): drain the CTA's 128 accumulator rows 32 columns at a time,
-//     release the accumulator (acc_empty), store the bits.
-// Measured (microbench/probe_waits.py, ncu): the tensor pipe is 94-99% active; long
-// runs are held at ~1.65-1.72 GHz by the board power cap, not by the pipeline.
+//     stay warp-uniform (no per-instruction R2UR waterfall); an elected lane issues the
+//     bias MMA and then 4 MMAs per stage, commits each stage to both CTAs' empty
+//     barriers and each tile to both CTAs' acc_full barriers.
+//   epilogue (warps 9-12): drain the CTA's 128 accumulator rows with double-buffered
+//     16-column TMEM loads, release the accumulator (acc_empty) as soon as the last
+//     load lands, pack the bits with funnel-shift chains, store.
+// Measured (ncu, microbench/trace_tiles.py): the tensor pipe is 98-99% active on long
+// K, held at ~1.8 GHz by the board power cap; on 4096-bit leaves each tile boundary
+// costs ~0.9 us (drain ~450 ns plus commit / restart latency) against a ~4.3 us tile.
 #include <cuda.h>
 
 #include "umma.cuh"
