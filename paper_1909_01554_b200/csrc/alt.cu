@@ -895,6 +895,36 @@ __global__ void mode_step_in_place_kernel(uint64_t* __restrict__ v, uint64_t out
 
 }  // namespace
 
+Steps basis_steps(const Scheme* sc, int factor, int inverse) {
+    const InPlaceStep* st = factor == 0 ? sc->phi : factor == 1 ? sc->psi : sc->chi;
+    const int n = factor == 0 ? sc->n_phi : factor == 1 ? sc->n_psi : sc->n_chi;
+    Steps s{};
+    s.n = n;
+    for (int i = 0; i < n; ++i) {
+        // the inverse of a sequence of x[t] ^= x[s] is the reversed sequence
+        const InPlaceStep& p = inverse ? st[n - 1 - i] : st[i];
+        s.t[i] = p.target;
+        s.s[i] = p.source;
+    }
+    return s;
+}
+
+// One level of a basis change on [outer][4][inner] words on the device.
+int interleaved_basis_change_level_dev(uint64_t* d, uint64_t outer, uint64_t inner, int algo, int factor, int inverse,
+                                       cudaStream_t stream) {
+    const Scheme* sc = scheme_for(algo);
+    if (!sc || factor < 0 || factor > 2) {
+        set_error("basis change: unknown scheme or factor");
+        return kEinval;
+    }
+    const Steps s = basis_steps(sc, factor, inverse);
+    if (s.n == 0 || outer * inner == 0) return kOk;
+    mode_step_in_place_kernel<<<grid_for(outer * inner), 256, 0, stream>>>(d, outer, inner, s);
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaGetLastError());
+    return kOk;
+}
+
 // In-place basis change of an interleaved vector already on the device: factor 0 phi,
 // 1 psi, 2 chi of the scheme; one pass per level (reference yates.cpp:143-172).
 int interleaved_basis_change_dev(uint64_t* d, uint64_t total_words, int levels, int algo, int factor, int inverse,
@@ -926,13 +956,68 @@ int interleaved_basis_change_dev(uint64_t* d, uint64_t total_words, int levels, 
     return kOk;
 }
 
+// Host-vector basis change (bmm::basis_change, reference engine.cpp:146-172; the
+// standalone `transform` of bmm_cli.cpp:210-234).  Vectors that fit the device budget
+// go up once, get every level, come back.  Larger ones (a 2^20 operand is 128 GiB)
+// stream: level l pairs words 4 inner_l apart (inner_l = total / 4^(l+1)), so the
+// levels whose 4-way groups span at most a device block are applied together to
+// contiguous blocks in one pass, and each level with wider groups takes its own pass
+// that gathers the four strided pieces of a chunk of positions (one upload and one
+// download of the vector per pass).
 int interleaved_basis_change(uint64_t* words, uint64_t total_words, int levels, int algo, int factor, int inverse) {
-    DevMem d;
     int rc;
-    if ((rc = d.alloc(total_words * 8, nullptr))) return rc;
-    BMMGPU_CUDA_TRY(memcpy_counted(d.p, words, total_words * 8, cudaMemcpyHostToDevice, nullptr));
-    if ((rc = interleaved_basis_change_dev(d.u(), total_words, levels, algo, factor, inverse, nullptr))) return rc;
-    BMMGPU_CUDA_TRY(memcpy_counted(words, d.p, total_words * 8, cudaMemcpyDeviceToHost, nullptr));
+    if (levels == 0 || total_words == 0) return kOk;
+    uint64_t budget = free_budget();
+    if (const char* b = getenv("BMMGPU_BASIS_BUDGET")) budget = strtoull(b, nullptr, 10);
+    if (total_words * 8 <= budget) {
+        DevMem d;
+        if ((rc = d.alloc(total_words * 8, nullptr))) return rc;
+        BMMGPU_CUDA_TRY(memcpy_counted(d.p, words, total_words * 8, cudaMemcpyHostToDevice, nullptr));
+        if ((rc = interleaved_basis_change_dev(d.u(), total_words, levels, algo, factor, inverse, nullptr))) return rc;
+        BMMGPU_CUDA_TRY(memcpy_counted(words, d.p, total_words * 8, cudaMemcpyDeviceToHost, nullptr));
+        BMMGPU_CUDA_TRY(cudaStreamSynchronize(nullptr));
+        return kOk;
+    }
+    // device block: a power of two of words within the budget
+    uint64_t bw = 1;
+    while (bw * 2 * 8 <= budget && bw * 2 <= total_words) bw *= 2;
+    if (bw < 4) {
+        set_error("basis change: device budget below one 4-way group");
+        return kEinval;
+    }
+    auto inner_of = [&](int l) { return total_words >> (2 * (l + 1)); };
+    int l0 = 0;  // first level whose groups (4 inner_l words) fit a block
+    while (l0 < levels && 4 * inner_of(l0) > bw) ++l0;
+    DevMem d;
+    if ((rc = d.alloc(bw * 8, nullptr))) return rc;
+    // strided levels, one pass each: chunks of c positions, pieces q at q * inner
+    for (int l = 0; l < l0; ++l) {
+        const uint64_t inner = inner_of(l), outer = total_words / (4 * inner), c = bw / 4;
+        for (uint64_t o = 0; o < outer; ++o)
+            for (uint64_t t0 = 0; t0 < inner; t0 += c) {
+                const uint64_t cl = std::min(c, inner - t0);
+                uint64_t* base = words + o * 4 * inner + t0;
+                BMMGPU_CUDA_TRY(memcpy2d_counted(d.p, cl * 8, base, inner * 8, cl * 8, 4, cudaMemcpyHostToDevice,
+                                                 nullptr));
+                if ((rc = interleaved_basis_change_dev(d.u(), 4 * cl, 1, algo, factor, inverse, nullptr))) return rc;
+                BMMGPU_CUDA_TRY(memcpy2d_counted(base, inner * 8, d.p, cl * 8, cl * 8, 4, cudaMemcpyDeviceToHost,
+                                                 nullptr));
+            }
+    }
+    // the remaining levels together, block by block: within a block of bw words the
+    // level-l groups are [bw / (4 inner_l)][4][inner_l], i.e. levels l0.. of a vector
+    // of bw words whose outermost mode starts at l0
+    if (l0 < levels) {
+        for (uint64_t b0 = 0; b0 < total_words; b0 += bw) {
+            BMMGPU_CUDA_TRY(memcpy_counted(d.p, words + b0, bw * 8, cudaMemcpyHostToDevice, nullptr));
+            for (int l = l0; l < levels; ++l) {
+                const uint64_t inner = inner_of(l), outer_b = bw / (4 * inner);
+                if ((rc = interleaved_basis_change_level_dev(d.u(), outer_b, inner, algo, factor, inverse, nullptr)))
+                    return rc;
+            }
+            BMMGPU_CUDA_TRY(memcpy_counted(words + b0, d.p, bw * 8, cudaMemcpyDeviceToHost, nullptr));
+        }
+    }
     BMMGPU_CUDA_TRY(cudaStreamSynchronize(nullptr));
     return kOk;
 }

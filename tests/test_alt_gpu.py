@@ -170,3 +170,28 @@ def test_streamed_host_path_pinned_buffers(engine, oracle, leaf):
                            bmm.BitMatrix(n, n, hb.numpy().view(np.uint64)), algo, bmm.LayerPlan.auto_plan(n, 1),
                            bmm.Semiring.Gf2XorAnd, leaf_log2=leaf, out=out)
         assert np.array_equal(got.words, want), (algo, leaf)
+
+
+@pytest.mark.parametrize("budget", [None, 64 << 10, 16 << 10, 4 << 10])
+def test_interleaved_basis_change_streams_beyond_the_budget(engine, oracle, monkeypatch, budget):
+    """bmmgpu_basis_change on vectors larger than the device budget (the standalone
+    transform at 2^20 is 128 GiB): levels whose groups exceed a device block stream as
+    strided passes, the rest in one blocked pass -- same words as the in-core run, and
+    the inverse restores the input."""
+    lib = engine.lib()
+    levels = 4
+    v = oracle.random(1, (4 ** levels) * 4096, 43)  # [4]^4 [4096]: 128 KiB
+    want = {}
+    for algo, factor in ((2, 0), (2, 2), (3, 0), (3, 1), (3, 2)):
+        w = v.copy()
+        monkeypatch.delenv("BMMGPU_BASIS_BUDGET", raising=False)
+        assert lib.bmmgpu_basis_change(w.ctypes.data, w.size, levels, algo, factor, 0) == 0
+        want[(algo, factor)] = w
+    if budget is not None:
+        monkeypatch.setenv("BMMGPU_BASIS_BUDGET", str(budget))
+    for (algo, factor), ref in want.items():
+        w = v.copy()
+        assert lib.bmmgpu_basis_change(w.ctypes.data, w.size, levels, algo, factor, 0) == 0
+        assert np.array_equal(w, ref), (algo, factor, budget)
+        assert lib.bmmgpu_basis_change(w.ctypes.data, w.size, levels, algo, factor, 1) == 0
+        assert np.array_equal(w, v), (algo, factor, budget)
