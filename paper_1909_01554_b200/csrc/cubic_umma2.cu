@@ -76,7 +76,7 @@ constexpr int P_STAGE = 2 * P_REGION;
 constexpr int P_PRODUCERS = 256;          // expanders: two threads per row of A and of Bt
 constexpr int P_MMA_WARP = P_PRODUCERS / 32;
 #ifndef BMMGPU_EPI_WARPS
-#define BMMGPU_EPI_WARPS 4  // 8 measured no faster: the drain is TMEM-read bound, not issue bound
+#define BMMGPU_EPI_WARPS 4  // 8 (two per TMEM lane quarter) measured no faster, and spills at 96 registers
 #endif
 constexpr int P_EPI_WARPS = BMMGPU_EPI_WARPS;     // 4: one per TMEM lane quarter; 8: two, 128 columns each
 constexpr int P_EPI_COLS = 256 * 4 / P_EPI_WARPS;  // accumulator columns one epilogue warp drains
@@ -158,9 +158,6 @@ __device__ unsigned long long g_probe[2 * P_MAX_PAIRS * 8];
 #define BMMGPU_EPI_SLEEP 512  // ns the epilogue warps sleep between polls of acc_full on long tiles
 #endif
 
-#ifndef BMMGPU_DRAIN_GROUP
-#define BMMGPU_DRAIN_GROUP 1  // x16 TMEM loads per drain phase
-#endif
 
 #ifndef BMMGPU_L2_HINT
 #define BMMGPU_L2_HINT 1  // 0 normal / normal, 1 A evict_last + Bt evict_first (measured best), 2 A normal + Bt evict_first
@@ -482,6 +479,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             uint32_t pk_empty_parity = 0;
             uint64_t qn = 0;
             uint32_t local = 0;
+            bool align = wave_ctr != nullptr;
             for (uint32_t t = pair; t < (PROBE(256) ? 0 : total_tiles); t += n_pairs, ++local) {
                 uint32_t b, tm, tn;
                 map.decode(t, b, tm, tn);
@@ -493,10 +491,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                 // loader has issued its previous one.  The loaders run two superstages ahead
                 // of the MMAs, so the wait hides behind buffered work.  Bounded: after
                 // kWaveSpinLimit polls it proceeds anyway (co-residency is not assumed).
-                if (wave_ctr && local > 0) {
+                if (align && local > 0) {
                     const unsigned long long target = (unsigned long long)n_pairs * local;
-                    for (uint32_t i = 0; i < kWaveSpinLimit && umma::ld_acquire_u64(wave_ctr) < target; ++i)
+                    uint32_t i = 0;
+                    while (i < kWaveSpinLimit && umma::ld_acquire_u64(wave_ctr) < target) {
                         __nanosleep(64);
+                        ++i;
+                    }
+                    // a timeout means the pairs are not all resident (another kernel holds
+                    // SMs): stop aligning for the rest of this launch instead of paying it
+                    // on every tile
+                    if (i == kWaveSpinLimit) align = false;
                 }
                 for (uint64_t k0 = 0; k0 < n_stages; k0 += 4, ++qn) {
                     if (qn >= P_SST_SLOTS) umma::mbar_wait(&pk_empty_bar[slot], pk_empty_parity);
