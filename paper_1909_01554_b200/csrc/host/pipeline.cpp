@@ -65,20 +65,20 @@ struct SubvectorLocks::Cell {
 
 SubvectorLocks::SubvectorLocks(int d_host) {
     if (d_host < 0) throw std::invalid_argument("negative host level count");
-    count_ = std::size_t(1) << (2 * d_host);
-    cells_.reset(new Cell[count_]);
+    n_ = std::size_t(1) << (2 * d_host);
+    slots_.reset(new Cell[n_]);
 }
 
 SubvectorLocks::~SubvectorLocks() = default;
 
 void SubvectorLocks::lock(std::size_t index) {
-    Cell& c = cells_[index];
+    Cell& c = slots_[index];
     c.mu.lock();
-    if (c.held.exchange(true, std::memory_order_relaxed)) violations_.fetch_add(1, std::memory_order_relaxed);
+    if (c.held.exchange(true, std::memory_order_relaxed)) overlaps_.fetch_add(1, std::memory_order_relaxed);
 }
 
 void SubvectorLocks::unlock(std::size_t index) {
-    Cell& c = cells_[index];
+    Cell& c = slots_[index];
     c.held.store(false, std::memory_order_relaxed);
     c.mu.unlock();
 }
