@@ -721,6 +721,7 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
 
     int rc;
     DevMem dA, dB, dBt, dC, T, S, Q;
+    StreamDrain drain{{st3.c, st3.h, st3.d, nullptr}};
     if ((rc = dA.alloc(n * w * 8, s)) || (rc = dB.alloc(n * w * 8, s)) || (rc = dBt.alloc(n * w * 8, s)) ||
         (rc = dC.alloc(n * w * 8, s)) || (rc = T.alloc(half * hw * 8, s)) || (rc = S.alloc(half * hw * 8, s)) ||
         (rc = Q.alloc(half * hw * 8, s)))

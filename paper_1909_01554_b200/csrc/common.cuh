@@ -39,6 +39,17 @@ inline cudaError_t memcpy_counted(void* dst, const void* src, size_t bytes, cuda
 // level's buffer needs no stream synchronisation.
 void enable_pool_caching();
 
+// Declared after a driver's buffers, so it is destroyed first: waits for every stream
+// the driver used before the buffers' stream-ordered frees run (on error returns the
+// copy streams may still be reading or writing them).
+struct StreamDrain {
+    cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};
+    ~StreamDrain() {
+        for (cudaStream_t x : s)
+            if (x) cudaStreamSynchronize(x);
+    }
+};
+
 struct DeviceBuffer {
     void* p = nullptr;
     cudaStream_t s = nullptr;

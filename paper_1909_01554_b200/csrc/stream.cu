@@ -134,6 +134,7 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
         BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&ev.e[i], i >= 12 ? 0 : cudaEventDisableTiming));
     const int n_abuf = m > P.TM ? 2 : 1;
     DeviceBuffer dA[2], dB[2], dBt[2], dC[2];
+    StreamDrain drain{{cs, xs, as, ds}};
     for (int i = 0; i < n_abuf; ++i)
         if ((st = dA[i].alloc(P.TM * kwc * 8, cs))) return st;
     for (int i = 0; i < 2; ++i)
@@ -285,6 +286,7 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
     for (int i = 0; i < 14; ++i)
         BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&ev.e[i], i == 5 || i == 6 ? 0 : cudaEventDisableTiming));
     DeviceBuffer dC, dA[2], dB[2], dBt[2];
+    StreamDrain drain{{cs, xs, ds, nullptr}};
     if ((st = dC.alloc(m_pad * cw * 8, cs))) return st;
     for (int b = 0; b < 2; ++b)
         if ((st = dA[b].alloc(m_pad * KCw * 8, cs)) || (st = dB[b].alloc(KCw * 64 * nb * 8, cs)) ||
