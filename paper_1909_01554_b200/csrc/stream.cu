@@ -218,7 +218,7 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
 // K-outer pipelined form for slabs whose C fits in HBM (the common in-core case
 // of the host API): K is cut into chunks; while the tensor cores fold chunk q
 // into the resident C, the copy stream uploads A[:, q+1] and B[q+1, :].  The
-// chunks grow geometrically (first 1/32 of K, then x3, x4 ...): the exposed
+// chunks grow geometrically (first 1/32 of K, then x5 ...): the exposed
 // upload of the first chunk is small, and each later upload (bytes ~ (m + n) s)
 // still hides behind the previous chunk's product (work ~ m n s).  The last
 // chunk's product runs in row slices whose C rows go home on a download stream
@@ -232,7 +232,10 @@ std::vector<uint64_t> kouter_chunks(uint64_t kw, uint64_t gkw, uint64_t max_w, i
         return c;
     }
     uint64_t s = std::min(max_w, std::max(gkw, round_up(ceil_div(kw, 32), std::max<uint64_t>(gkw, 16))));
-    const uint64_t growth[] = {3, 4, 4};
+    // each upload (bytes ~ (m + n) s) must hide behind the previous chunk's product
+    // (work ~ m n s): at n = 131072, 55 GB/s and ~8 Pbop/s that allows ~7x growth per
+    // chunk; 5x keeps margin for slower links.  Fewer chunks = fewer accumulator drains.
+    const uint64_t growth[] = {5, 5, 5};
     int g = 0;
     for (uint64_t o = 0; o < kw;) {
         uint64_t w = std::min(s, kw - o);
@@ -260,7 +263,7 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
     const uint64_t m_pad = round_up(m, gm), n_pad = round_up(n, gn), cw = n_pad / 64;
     const uint64_t kw = round_up(std::max<uint64_t>(ka, 1), gkw);
     // largest chunk the budget allows (double-buffered A, B and Bt chunks + resident C)
-    uint64_t KCw = round_up(ceil_div(kw, 2), gkw);
+    uint64_t KCw = kw;  // the last, largest chunk may take most of K
     auto need = [&](uint64_t kc) { return (m_pad * cw + 2 * (m_pad * kc + kc * 64 * nb + n_pad * kc)) * 8; };
     while (need(KCw) > budget && KCw > gkw) KCw = round_up(KCw / 2, gkw);
     if (need(KCw) > budget) {
