@@ -3,6 +3,7 @@
 // (reference proj/tests/test_bitmatrix.cpp, test_engine.cpp, test_decomposition.cpp).
 // Usage: test_dropin host   -- container, layout, I/O, plan, counts (no GPU)
 //        test_dropin gpu    -- every product through the GPU engine
+#include <algorithm>
 #include <bit>
 #include <cstdio>
 #include <cstring>
@@ -269,6 +270,34 @@ void pipeline_gpu_cases() {
         CHECK(once && st.lock_violations == 0);
         CHECK(throws<std::invalid_argument>([&] { (void)pipeline::coordinate(a, b, asi, plan_for(1, 0, 2), 0); }));
         CHECK(throws<std::invalid_argument>([&] { (void)pipeline::coordinate(a, b, asi, plan_for(1, 1, 2), 2); }));
+    });
+    run("acceptance C1: every scheme and the host layer equal the cubic product, n = 64 .. 4096, 5 seeds", [] {
+        // reference acceptance_main.cpp:83-132 (fast products and pipeline(N=4) against cubic)
+        bool ok = true;
+        for (std::uint64_t n = 64; n <= 4096; n *= 2)
+            for (std::uint64_t seed = 1; seed <= 5; ++seed) {
+                const BitMatrix a = BitMatrix::random(n, n, 1000 * n + seed), b = BitMatrix::random(n, n, 2000 * n + seed);
+                const BitMatrix want = multiply_cubic(a, b, Semiring::Gf2XorAnd);
+                const LayerPlan p = LayerPlan::auto_plan(n, 1);
+                for (Algo al : {Algo::StrassenWinograd, Algo::AltSelfInverse, Algo::AltChaining})
+                    ok = ok && multiply(a, b, al, p, Semiring::Gf2XorAnd) == want;
+                if (p.depth() >= 1) {
+                    const Decomposition& d = builtin(Builtin::AltSelfInverse);
+                    LayerPlan hp = p;
+                    hp.d_host = std::min(2, p.depth());
+                    hp.d_parallel = std::max(0, p.d_parallel - hp.d_host);
+                    hp.d_serial = p.depth() - hp.d_host - hp.d_parallel;
+                    BitVectorTensor ah = to_interleaved(a, hp, Operand::Left), bh = to_interleaved(b, hp, Operand::Right);
+                    basis_change(ah, d, BasisFactor::Phi, hp.depth());
+                    basis_change(bh, d, BasisFactor::Psi, hp.depth());
+                    pipeline::PipelineStats st;
+                    BitVectorTensor ch = pipeline::coordinate(ah, bh, d, hp, 4, nullptr, &st);
+                    basis_change(ch, d, BasisFactor::Chi, hp.depth());
+                    ok = ok && from_interleaved(ch, hp, Operand::Result) == want && st.lock_violations == 0;
+                }
+                if (n <= 256) ok = ok && multiply_cubic(a, b, Semiring::BooleanOrAnd) == naive(a, b, Semiring::BooleanOrAnd);
+            }
+        CHECK(ok);
     });
     run("pipeline: full multiply with host levels", [] {
         const BitMatrix a = BitMatrix::random(256, 256, 261), b = BitMatrix::random(256, 256, 262);
