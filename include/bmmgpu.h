@@ -3,7 +3,7 @@
  *
  * Plain pointers and sizes only.  Every entry point returns a status code;
  * bmmgpu_last_error() gives the message of the last failure on the calling
- * thread.  The C++ drop-in (include/bmm/*.hpp, libbmm_b200.so) turns the codes
+ * thread.  The C++ drop-in (include/bmm/ headers, libbmm_b200.so) turns the codes
  * back into the reference's exception types:
  *     BMMGPU_EINVAL -> std::invalid_argument   (reference engine.cpp:355-365)
  *     BMMGPU_ESHAPE -> bmm::ShapeError         (reference engine.cpp:134, 359-362)

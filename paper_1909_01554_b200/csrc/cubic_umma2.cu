@@ -109,12 +109,12 @@ static_assert(P_SMEM <= 232448 - 1024, "stage ring exceeds shared memory");
 // 1024/2048 empty seen (CTA 0/1), 1536/2560 full arrive (first warp of the stage's group).
 // Compiled in only with -DBMMGPU_TRACE (the build never sets it by default).
 __device__ unsigned long long g_trace[6144];
+#ifdef BMMGPU_TRACE
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#ifdef BMMGPU_TRACE
 #define TRACE_AT(cond, idx)                                \
     do {                                                   \
         if ((flags & 16) && (cond)) g_trace[idx] = gtime(); \
