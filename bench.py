@@ -69,25 +69,33 @@ def eff_bops(m: int, k: int, n: int) -> float:
 
 # ------------------------------------------------------------------ distributed plumbing
 class Dist:
+    """One process per GPU (torchrun env).  NCCL for the barrier and the max-over-ranks
+    reduction; BMM_DIST_BACKEND=gloo runs the same rank logic over gloo, which also
+    lets several ranks share one GPU (the multi-rank path tested on a 1-GPU box)."""
+
     def __init__(self) -> None:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.device = self.local_rank
         self.pg = None
+        self.backend = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
-            if backend == "nccl":
-                torch.cuda.set_device(self.local_rank)
-            dist.init_process_group(backend=backend)
+            cuda = torch.cuda.is_available()
+            if cuda:
+                self.device = self.local_rank % torch.cuda.device_count()
+            self.backend = os.environ.get("BMM_DIST_BACKEND") or ("nccl" if cuda else "gloo")
+            if self.backend == "nccl":
+                torch.cuda.set_device(self.device)
+            dist.init_process_group(backend=self.backend)
             self.pg = dist
 
     def barrier(self) -> None:
         if self.pg is not None:
-            import torch
-            if torch.cuda.is_available():
-                self.pg.barrier(device_ids=[self.local_rank])
+            if self.backend == "nccl":
+                self.pg.barrier(device_ids=[self.device])
             else:
                 self.pg.barrier()
 
@@ -95,7 +103,7 @@ class Dist:
         if self.pg is None:
             return x
         import torch
-        dev = f"cuda:{self.local_rank}" if torch.cuda.is_available() else "cpu"
+        dev = f"cuda:{self.device}" if self.backend == "nccl" else "cpu"
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
@@ -311,7 +319,7 @@ def run_ooc(args, dist: Dist) -> None:
 
     n, ring, algo, desc = WORKLOADS[args.workload]
     lib = bmm.lib()
-    dev = dist.local_rank
+    dev = dist.device
     torch.cuda.set_device(dev)
     w = n // 64
     r0, r1 = shard_rows(n, dist.rank, dist.world, 256)
@@ -393,12 +401,12 @@ def run_ours(args, dist: Dist) -> None:
     import paper_1909_01554_b200 as bmm
 
     n, ring, algo, desc = WORKLOADS[args.workload]
-    args.cpus = bind_to_gpu_cpus(dist.local_rank)
+    args.cpus = bind_to_gpu_cpus(dist.device)
     if args.workload.startswith("c5-"):
         return run_ooc(args, dist)
     kernel = KERNEL_IDS[args.kernel]
     lib = bmm.lib()
-    dev = dist.local_rank
+    dev = dist.device
     torch.cuda.set_device(dev)
     gm, gn, gk = bmm.granularity(kernel)
     w = n // 64

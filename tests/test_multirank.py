@@ -65,3 +65,25 @@ def test_slab_rule_matches_for_every_part_count():
             assert prev == m
     with pytest.raises(ValueError):
         bmm.slab_rows(10, 2, 2, 64)
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_share_one_gpu():
+    """bench.py under torchrun with two ranks (gloo for the rank plumbing, so both may
+    share the box's one GPU): each rank multiplies its output-row slab, rank 0 prints
+    one line with the aggregate over both slabs and the max-over-ranks time."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, BMM_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", "bench.py", "--gpus", "2", "--workload",
+           "c1-gf2-cubic-8192", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=str(ROOT), env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["rows_per_rank"] == 4096 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 4096 * 128 * 8 + 8192 * 128 * 8
