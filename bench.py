@@ -48,6 +48,8 @@ WORKLOADS = {
     "c2-gf2-altsi-65536": (65536, GF2, 2, "GF(2) product n=65536 alternative-basis Strassen (BASELINE configs[1])"),
     "c4-gf2-cubic-262144": (262144, GF2, 0, "GF(2) product n=262144, output row slabs (BASELINE configs[3])"),
     "c4-gf2-altsi-262144": (262144, GF2, 2, "GF(2) product n=262144 alternative-basis Strassen"),
+    # a small instance of the same multi-GPU tile partition (tests)
+    "c4s-gf2-altsi-16384": (16384, GF2, 2, "GF(2) product n=16384 alternative-basis Strassen (tile-partition test size)"),
     # configs[4] (n = 2^20 on 8 GPUs needs 384 GiB of host memory for A, B, C; one box has
     # 196 GB), scaled to one GPU: n = 2^19 from pinned host memory through the out-of-core
     # driver with a device budget below the operands (A row panels resident, B streamed in
@@ -396,6 +398,114 @@ def run_ooc(args, dist: Dist) -> None:
         print(json.dumps(line), flush=True)
 
 
+def run_alt_tiles(args, dist: Dist) -> None:
+    """Fast GF(2) product on several GPUs (SURVEY section 8e, configs[3]): C is cut
+    into 4 x 4 output tiles of n/4, tile (I, J) = XOR over K of the alt-basis products
+    A[I, K] . B[K, J] (n/4 each, strided views of the resident operands), and the 16
+    tiles are dealt round robin to the ranks -- disjoint outputs, no exchange, no
+    collective.  (64 block products of n/4 instead of the single-GPU recursion's 49:
+    the price of the partition.)"""
+    import torch
+    import paper_1909_01554_b200 as bmm
+
+    n, ring, algo, desc = WORKLOADS[args.workload]
+    lib = bmm.lib()
+    dev = dist.device
+    torch.cuda.set_device(dev)
+    w, T = n // 64, n // 4
+    tw = T // 64
+    mine = [t for t in range(16) if t % dist.world == dist.rank]
+    hA = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
+    hB = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
+    bmm.random_rows_into(hA.numpy().view(np.uint64), n, 1, 0, n)
+    bmm.random_rows_into(hB.numpy().view(np.uint64), n, 2, 0, n)
+    dA = hA.view(n, w).to(f"cuda:{dev}")
+    dB = hB.view(n, w).to(f"cuda:{dev}")
+    dBt = torch.empty((n, w), dtype=torch.int64, device=f"cuda:{dev}")
+    dC = torch.empty((len(mine), T, tw), dtype=torch.int64, device=f"cuda:{dev}")
+    dP = torch.empty((T, tw), dtype=torch.int64, device=f"cuda:{dev}")
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    torch.cuda.synchronize()
+
+    def check(rc: int) -> None:
+        if rc != 0:
+            raise RuntimeError(lib.bmmgpu_last_error().decode())
+
+    def step() -> None:
+        check(lib.bmmgpu_dev_transpose(dB.data_ptr(), w, n, n, dBt.data_ptr(), n, w, sp))
+        for slot, t in enumerate(mine):
+            I, J = divmod(t, 4)
+            for K in range(4):
+                a = dA.data_ptr() + 8 * (I * T * w + K * tw)
+                bt = dBt.data_ptr() + 8 * (J * T * w + K * tw)
+                out = dC[slot] if K == 0 else dP
+                check(lib.bmmgpu_dev_multiply(a, w, bt, w, out.data_ptr(), tw, T, algo, args.leaf_log2, 0, sp))
+                if K:
+                    check(lib.bmmgpu_dev_fold(dC[slot].data_ptr(), tw, dP.data_ptr(), tw, T, tw, ring, sp))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    visible = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip().isdigit()]
+    sampler = ClockSampler(int(visible[dev]) if dev < len(visible) else dev)
+    sampler.start()
+    check(lib.bmmgpu_block_timer(1))
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.bmmgpu_last_launch_count()
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = lib.bmmgpu_last_launch_count() - launches0
+    dist.barrier()
+    clocks = sampler.stop()
+    blk_ms, blk_n = ctypes.c_double(0.0), ctypes.c_uint64(0)
+    check(lib.bmmgpu_block_timer_read(ctypes.byref(blk_ms), ctypes.byref(blk_n)))
+    check(lib.bmmgpu_block_timer(0))
+    ms = dist.max(t0.elapsed_time(t1) / args.steps)
+    checked = None
+    if args.check:
+        # every tile of this rank against the tensor-core cubic product of A[I, :] . B[:, J]
+        ref = torch.empty((T, tw), dtype=torch.int64, device=f"cuda:{dev}")
+        checked = 0
+        for slot, t in enumerate(mine):
+            I, J = divmod(t, 4)
+            check(lib.bmmgpu_dev_cubic(dA.data_ptr() + 8 * I * T * w, w, dBt.data_ptr() + 8 * J * T * w, w,
+                                       ref.data_ptr(), tw, T, T, w, ring, 0, 0, sp))
+            torch.cuda.synchronize()
+            if not torch.equal(ref, dC[slot]):
+                raise RuntimeError(f"tile {t} differs from the cubic product")
+            checked += 1
+    depth = (T // 64).bit_length() - 1
+    e_levels = max(0, min(depth, depth + 6 - (args.leaf_log2 or 12)))
+    leaf = T >> e_levels
+    kms = blk_ms.value / args.steps
+    launch_bops = len(mine) * 4 * 7**e_levels * eff_bops(leaf, leaf, leaf)
+    peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())
+    achieved = launch_bops / (kms * 1e-3)
+    value = eff_bops(n, n, n) / (ms * 1e-3) / 1e15
+    if dist.rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "e2m1", "data": "synthetic (BitMatrix::random seeds 1, 2, mt19937_64)",
+                "config": {"workload": args.workload, "desc": desc, "n": n, "ring": "gf2",
+                           "algo": ["cubic", "sw", "alt-si", "alt-chain"][algo],
+                           "parallelism": f"4x4 output tiles of n/4 round robin over {dist.world} ranks, "
+                                          "each tile the XOR of 4 alt-basis block products, no exchange",
+                           "tiles_per_rank0": len(mine)},
+                "roofline": {"bound": "tensor", "achieved": achieved / 1e12, "peak": peaks["umma_mxf4_bops"] / 1e12,
+                             "unit": "Tbop/s", "frac": achieved / peaks["umma_mxf4_bops"], "traffic": None,
+                             "kernel": f"cubic_umma2_kernel (leaf layer: 7^{e_levels} products of {leaf}^3 per block)",
+                             "kernel_ms": kms, "kernel_share_of_step": kms / ms},
+                "cpu_baseline": None, "e2e": None, "tiles_checked_rank0": checked, "clocks": clocks,
+                "gpu_launches": int(launches)}
+        print(json.dumps(line), flush=True)
+
+
 def run_ours(args, dist: Dist) -> None:
     import torch
     import paper_1909_01554_b200 as bmm
@@ -414,7 +524,7 @@ def run_ours(args, dist: Dist) -> None:
         r0, r1 = shard_rows(n, dist.rank, dist.world, gm)
     else:
         if dist.world > 1:
-            raise SystemExit("the alt-basis workload runs on one GPU (BASELINE configs[1])")
+            return run_alt_tiles(args, dist)
         r0, r1 = 0, n
     m = r1 - r0
     # pinned host inputs (the e2e leg copies from these every step)
@@ -625,7 +735,8 @@ def main() -> None:
     ap.add_argument("--device-budget", dest="device_budget", type=int, default=0,
                     help="HBM bytes the e2e call may use (0 = free memory; the c5 workloads default to 40 GiB)")
     ap.add_argument("--check", action="store_true",
-                    help="c5 workloads: verify full rows and a full column of C on the CPU (numpy)")
+                    help="c5 workloads: verify rows and a column of C on the CPU (numpy); multi-rank alt: "
+                         "verify every tile against the tensor-core cubic product")
     args = ap.parse_args()
     dist = Dist()
     try:

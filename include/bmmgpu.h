@@ -138,6 +138,12 @@ int bmmgpu_dev_cubic_batched(const uint64_t* dA, uint64_t lda, uint64_t sA, cons
                              uint64_t n_pad, uint64_t kw, int32_t semiring, int32_t kernel, int32_t accumulate,
                              void* stream);
 
+/* dst (+)= src over rows x words (XOR for GF(2), OR for Boolean), device memory,
+ * row strides ldd / lds words: the integration of partial products of a K-split or
+ * tile-partitioned product (reference cubic_blocked fold, engine.cpp:81-84). */
+int bmmgpu_dev_fold(uint64_t* dst, uint64_t ldd, const uint64_t* src, uint64_t lds, uint64_t rows, uint64_t words,
+                    int32_t semiring, void* stream);
+
 /* Fast GF(2) product on device, n = 64 * 2^depth: dA (n x n/64 words, stride
  * lda), dBt = Bt of B (n x n/64, stride ldbt; rows padded to 256 in memory),
  * dC (n x n/64, stride ldc).  dA and dBt are only read: the scheme's basis

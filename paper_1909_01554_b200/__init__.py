@@ -95,6 +95,8 @@ def lib() -> ctypes.CDLL:
                                                i32, i32, vp]
         L.bmmgpu_slab_rows.argtypes = [u64, ctypes.c_uint32, ctypes.c_uint32, u64, _u64p, _u64p]
         L.bmmgpu_slab_rows.restype = ctypes.c_int
+        L.bmmgpu_dev_fold.argtypes = [vp, u64, vp, u64, u64, u64, i32, vp]
+        L.bmmgpu_dev_fold.restype = ctypes.c_int
         L.bmmgpu_multiply_alt.argtypes = [vp, vp, vp, i32, i32, ctypes.POINTER(_Opts)]
         L.bmmgpu_multiply_alt.restype = ctypes.c_int
         L.bmmgpu_last_copy_bytes.argtypes = [_u64p, _u64p]

@@ -513,6 +513,44 @@ int bmmgpu_dev_cubic(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint
                         accumulate != 0, static_cast<cudaStream_t>(stream), 1, 0, 0, 0);
 }
 
+}  // extern "C"
+
+namespace bmmgpu {
+namespace {
+// dst (+)= src over a rows x words region: XOR for GF(2), OR for Boolean -- the
+// integration of partial products (reference cubic_blocked fold, engine.cpp:81-84).
+__global__ void fold_kernel(uint64_t* __restrict__ dst, uint64_t ldd, const uint64_t* __restrict__ src, uint64_t lds,
+                            uint64_t rows, uint64_t words, int gf2) {
+    const uint64_t total = rows * words;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / words, w = i - r * words;
+        const uint64_t v = src[r * lds + w];
+        uint64_t& d = dst[r * ldd + w];
+        d = gf2 ? (d ^ v) : (d | v);
+    }
+}
+}  // namespace
+}  // namespace bmmgpu
+
+extern "C" {
+
+int bmmgpu_dev_fold(uint64_t* dst, uint64_t ldd, const uint64_t* src, uint64_t lds, uint64_t rows, uint64_t words,
+                    int32_t semiring, void* stream) {
+    if (semiring != BMMGPU_BOOLEAN_OR_AND && semiring != BMMGPU_GF2_XOR_AND) {
+        set_error("unknown semiring");
+        return kEinval;
+    }
+    if (rows == 0 || words == 0) return kOk;
+    const uint64_t total = rows * words;
+    const unsigned grid = unsigned(std::min<uint64_t>((total + 255) / 256, 148ull * 32));
+    fold_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, ldd, src, lds, rows, words,
+                                                                      semiring == BMMGPU_GF2_XOR_AND);
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaGetLastError());
+    return kOk;
+}
+
 int bmmgpu_dev_cubic_batched(const uint64_t* dA, uint64_t lda, uint64_t sA, const uint64_t* dBt, uint64_t ldbt,
                              uint64_t sB, uint64_t* dC, uint64_t ldc, uint64_t sC, uint64_t batch, uint64_t m_pad,
                              uint64_t n_pad, uint64_t kw, int32_t semiring, int32_t kernel, int32_t accumulate,

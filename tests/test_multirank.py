@@ -87,3 +87,23 @@ def test_bench_two_ranks_share_one_gpu():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["rows_per_rank"] == 4096 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 4096 * 128 * 8 + 8192 * 128 * 8
+
+
+@pytest.mark.gpu
+def test_alt_tile_partition_two_ranks():
+    """The multi-GPU fast product (4 x 4 output tiles, each the XOR of 4 alt-basis block
+    products, round robin over ranks): two ranks sharing one GPU, every tile of rank 0
+    checked against the tensor-core cubic product."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, BMM_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2", "--workload",
+           "c4s-gf2-altsi-16384", "--leaf-log2", "9", "--steps", "3", "--warmup", "3", "--check"]
+    r = subprocess.run(cmd, cwd=str(ROOT), env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d["n_gpus"] == 2 and d["config"]["tiles_per_rank0"] == 8 and d["tiles_checked_rank0"] == 8
+    assert d["value"] > 0 and d["gpu_launches"] > 0
