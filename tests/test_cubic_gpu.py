@@ -275,3 +275,34 @@ def test_pageable_host_buffers_are_staged(engine, oracle):
             sel = B[np.flatnonzero(bits)]
             want = np.bitwise_xor.reduce(sel, axis=0) if ring == GF2 else np.bitwise_or.reduce(sel, axis=0)
             assert np.array_equal(got.words.reshape(m, n // 64)[i], want), (ring, i)
+
+
+def test_concurrent_long_k_products_on_one_device(engine, oracle):
+    """Two host threads run wave-aligned (long-K) products on the same GPU at once: the
+    second launch's CTA pairs are not all resident while the first runs, so its
+    loaders' bounded wave wait must give up instead of deadlocking; both results stay
+    exact."""
+    import threading
+    bmm = engine
+    m, k, n = 2048, 32768, 2048  # 128 K-stages: wave alignment on
+    ins = [(oracle.random(m, k, 401 + i), oracle.random(k, n, 501 + i)) for i in range(2)]
+    outs = [None, None]
+
+    def run(i):
+        a, b = ins[i]
+        outs[i] = bmm.multiply_cubic(bmm.BitMatrix(m, k, a), bmm.BitMatrix(k, n, b), bmm.Semiring.Gf2XorAnd)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in th)
+    for i in range(2):
+        a, b = ins[i]
+        A = a.reshape(m, k // 64)
+        B = b.reshape(k, n // 64)
+        for r in (0, m - 1):
+            bits = np.unpackbits(A[r].view(np.uint8), bitorder="little")[:k]
+            want = np.bitwise_xor.reduce(B[np.flatnonzero(bits)], axis=0)
+            assert np.array_equal(outs[i].words.reshape(m, n // 64)[r], want), (i, r)
