@@ -56,6 +56,8 @@ WORKLOADS = {
     # K-chunks, partial products XOR/OR-folded on device, C tiles back to host).
     "c5-bool-ooc-524288": (524288, BOOL, 0, "Boolean n=2^19 out-of-core from host (configs[4] scaled to 1 GPU)"),
     "c5-gf2-ooc-524288": (524288, GF2, 0, "GF(2) n=2^19 out-of-core from host (configs[4] scaled to 1 GPU)"),
+    # a small instance of the same out-of-core path (tests; run with a small --device-budget)
+    "c5s-gf2-ooc-32768": (32768, GF2, 0, "GF(2) n=2^15 out-of-core from host (test size)"),
 }
 OOC_BUDGET = 40 << 30  # device bytes the out-of-core workloads may use (operands are 3 x 32 GiB)
 DEFAULT_WORKLOAD = "c3-bool-cubic-131072"
@@ -272,14 +274,15 @@ def run_reference(args, dist: Dist) -> None:
 
 # ------------------------------------------------------------------ our arm
 def spot_check(hA: np.ndarray, hB: np.ndarray, hC: np.ndarray, n: int, ring: int, rows: list[int],
-               col: int) -> bool:
+               col: int, m: int | None = None) -> bool:
     """Independent CPU check of full rows and one full column of C (numpy, no GPU,
     no oracle): row i = fold over k with A[i,k] = 1 of B row k; column j = per-row
     parity / OR of A[i,:] & B[:, j]."""
     w = n // 64
-    A = hA.reshape(n, w)
+    m = n if m is None else m  # rows of this rank's slab of A and C
+    A = hA[: m * w].reshape(m, w)
     B = hB.reshape(n, w)
-    C = hC.reshape(n, w)
+    C = hC[: m * w].reshape(m, w)
     for i in rows:
         bits = np.unpackbits(A[i].view(np.uint8), bitorder="little")[:n]
         ks = np.flatnonzero(bits)
@@ -295,7 +298,7 @@ def spot_check(hA: np.ndarray, hB: np.ndarray, hC: np.ndarray, n: int, ring: int
     bcol = ((B[:, col // 64] >> np.uint64(col % 64)) & np.uint64(1)).astype(np.uint8)
     bw = np.packbits(bcol, bitorder="little").view(np.uint64)
     got = ((C[:, col // 64] >> np.uint64(col % 64)) & np.uint64(1)).astype(np.uint8)
-    for r0 in range(0, n, 8192):
+    for r0 in range(0, m, 8192):
         x = A[r0:r0 + 8192] & bw
         if ring == GF2:
             v = np.bitwise_xor.reduce(x, axis=1)
@@ -313,6 +316,34 @@ def spot_check(hA: np.ndarray, hB: np.ndarray, hC: np.ndarray, n: int, ring: int
     return True
 
 
+class SharedHostWords:
+    """A host word array shared by the ranks of one node: a /dev/shm file created by rank
+    0 (its name broadcast to the others), mapped by every rank and page-locked with
+    cudaHostRegister so the copies run at link speed.  Rank 0 unlinks the file as soon as
+    every rank has mapped it."""
+
+    def __init__(self, tag: str, words: int, dist: Dist) -> None:
+        import torch
+        import torch.distributed as tdist
+        name = [f"/dev/shm/{tag}"] if dist.rank == 0 else [None]
+        if dist.rank == 0:
+            with open(name[0], "wb") as f:
+                f.truncate(words * 8)
+        tdist.broadcast_object_list(name, src=0)
+        self.path, self.rank = name[0], dist.rank
+        self.tensor = torch.from_file(self.path, shared=True, size=words, dtype=torch.int64)
+        dist.barrier()
+        if dist.rank == 0:
+            os.unlink(self.path)  # the mappings keep the pages; nothing is left behind on a crash
+        rc = torch.cuda.cudart().cudaHostRegister(self.tensor.data_ptr(), words * 8, 0)
+        self.registered = int(rc) == 0 if not isinstance(rc, tuple) else int(rc[0]) == 0
+
+    def close(self) -> None:
+        import torch
+        if self.registered:
+            torch.cuda.cudart().cudaHostUnregister(self.tensor.data_ptr())
+
+
 def run_ooc(args, dist: Dist) -> None:
     """Out-of-core workloads: the inputs live in (pinned) host memory by definition, so
     the measured number is the end-to-end one through bmmgpu_cubic; value = e2e."""
@@ -328,11 +359,22 @@ def run_ooc(args, dist: Dist) -> None:
     m = r1 - r0
     t_gen = time.perf_counter()
     hA = torch.empty(max(m, 1) * w, dtype=torch.int64, pin_memory=True)
-    hB = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
     hC = torch.empty(max(m, 1) * w, dtype=torch.int64, pin_memory=True)
+    shared_b = None
+    if dist.world > 1:
+        # one copy of B in host memory for all ranks of the node (the paper's shared-memory
+        # host; at n = 2^20 a per-rank copy would be 128 GiB each): rank 0 generates it
+        # into /dev/shm, every rank maps it and page-locks its mapping
+        shared_b = SharedHostWords(f"bmm_B_{n}_{os.getpid() if dist.rank == 0 else 0}", n * w, dist)
+        hB = shared_b.tensor
+        if dist.rank == 0:
+            bmm.random_rows_into(hB.numpy().view(np.uint64), n, 2, 0, n)
+        dist.barrier()
+    else:
+        hB = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
+        bmm.random_rows_into(hB.numpy().view(np.uint64), n, 2, 0, n)
     hA_np, hB_np, hC_np = (t.numpy().view(np.uint64) for t in (hA, hB, hC))
     bmm.random_rows_into(hA_np, n, 1, r0, r1)
-    bmm.random_rows_into(hB_np, n, 2, 0, n)
     t_gen = time.perf_counter() - t_gen
     budget = args.device_budget or OOC_BUDGET
     opts = bmm._opts(0 if args.kernel == "auto" else KERNEL_IDS[args.kernel], device_mask=1 << dev,
@@ -367,7 +409,7 @@ def run_ooc(args, dist: Dist) -> None:
     value = total_bops / t / 1e15
     ok = None
     if args.check and dist.rank == 0:
-        ok = spot_check(hA_np, hB_np, hC_np, n, ring, [0, m // 2 + 1, m - 1], n // 3)
+        ok = spot_check(hA_np, hB_np, hC_np, n, ring, [0, m // 2 + 1, m - 1], n // 3, m)
     peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())
     kms = blk_ms.value / args.steps
     achieved = eff_bops(m, n, n) / (kms * 1e-3)
@@ -396,6 +438,8 @@ def run_ooc(args, dist: Dist) -> None:
                         "path": "bmmgpu_cubic (include/bmmgpu.h) from pinned host buffers, per rank"},
                 "spot_check": ok, "clocks": clocks, "gpu_launches": int(launches * args.steps)}
         print(json.dumps(line), flush=True)
+    if shared_b is not None:
+        shared_b.close()
 
 
 def run_alt_tiles(args, dist: Dist) -> None:
@@ -512,7 +556,7 @@ def run_ours(args, dist: Dist) -> None:
 
     n, ring, algo, desc = WORKLOADS[args.workload]
     args.cpus = bind_to_gpu_cpus(dist.device)
-    if args.workload.startswith("c5-"):
+    if args.workload.startswith(("c5-", "c5s-")):
         return run_ooc(args, dist)
     kernel = KERNEL_IDS[args.kernel]
     lib = bmm.lib()
