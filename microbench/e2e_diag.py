@@ -13,7 +13,7 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1909_01554_b200 as bmm  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
+n = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 131072
 w = n // 64
 lib = bmm.lib()
 h = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
@@ -33,24 +33,33 @@ hC = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
 bmm.random_rows_into(hA.numpy().view(np.uint64), n, 1, 0, n)
 bmm.random_rows_into(h.numpy().view(np.uint64), n, 2, 0, n)
 import os
-for mode, chunks in ((0, None), (1, None), (2, "2"), (2, "3"), (2, "4"), (2, "8")):
+cases = [(0, None, v) for _ in range(3) for v in ("equal", None, "3,64", "2,32")]
+if "--all" in sys.argv:
+    cases += [(1, None, None), (2, "2", None), (2, "3", None), (2, "4", None), (2, "8", None)]
+for mode, chunks, slices in cases:
+    if slices:
+        os.environ["BMMGPU_KOUTER_SLICES"] = slices
+    else:
+        os.environ.pop("BMMGPU_KOUTER_SLICES", None)
     if chunks:
         os.environ["BMMGPU_KOUTER_CHUNKS"] = chunks
     else:
         os.environ.pop("BMMGPU_KOUTER_CHUNKS", None)
     t = ctypes.c_double(0)
     opts = bmm._opts(0, timing=t, device_mask=1, force_streaming=mode)
-    for rep in range(3):
+    walls = []
+    for rep in range(int(os.environ.get('DIAG_REPS', '4'))):
         lib.bmmgpu_block_timer(1)
         s0 = time.perf_counter()
         assert lib.bmmgpu_cubic(hA.data_ptr(), h.data_ptr(), hC.data_ptr(), n, n, n, 0, ctypes.byref(opts)) == 0
         wall = time.perf_counter() - s0
+        walls.append(wall)
         bms, bl = ctypes.c_double(0), ctypes.c_uint64(0)
         lib.bmmgpu_block_timer_read(ctypes.byref(bms), ctypes.byref(bl))
         lib.bmmgpu_block_timer(0)
     h2d, d2h = ctypes.c_uint64(0), ctypes.c_uint64(0)
     lib.bmmgpu_last_copy_bytes(ctypes.byref(h2d), ctypes.byref(d2h))
-    print(json.dumps({"force_streaming": mode, "chunks": chunks, "wall_ms": wall * 1e3, "device_span_ms": t.value,
+    print(json.dumps({"force_streaming": mode, "chunks": chunks, "slices": slices, "wall_ms": wall * 1e3, "walls_ms": [round(x * 1e3, 1) for x in walls], "device_span_ms": t.value,
                       "block_ms": bms.value, "block_launches": bl.value,
                       "h2d_GB": h2d.value / 1e9, "d2h_GB": d2h.value / 1e9,
                       "Pbops": (2.0 * n**3 - n * n) / wall / 1e15}), flush=True)

@@ -20,6 +20,9 @@
 // so PCIe transfers in both directions overlap the tensor-core work.  Tile
 // sizes are chosen from the byte budget so the working set stays inside it.
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -221,8 +224,9 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
 // chunks grow geometrically (first 1/32 of K, then x5 ...): the exposed
 // upload of the first chunk is small, and each later upload (bytes ~ (m + n) s)
 // still hides behind the previous chunk's product (work ~ m n s).  The last
-// chunk's product runs in row slices whose C rows go home on a download stream
-// while the next slice computes, so only one slice of the D2H is exposed.
+// chunk's product runs in row slices (shrinking geometrically) whose C rows go home
+// on a download stream while the next slice computes, so only the last, small
+// slice's D2H is exposed.
 namespace {
 std::vector<uint64_t> kouter_chunks(uint64_t kw, uint64_t gkw, uint64_t max_w, int chunks) {
     std::vector<uint64_t> c;
@@ -246,6 +250,39 @@ std::vector<uint64_t> kouter_chunks(uint64_t kw, uint64_t gkw, uint64_t max_w, i
         s = std::min(max_w, round_up(s * growth[std::min(g++, 2)], gkw));
     }
     return c;
+}
+
+// Row slices of the last chunk, in launch order.  Slice i's rows go home while slice
+// i + 1 computes, so the exposed tail is the last slice's download.  Compute per row
+// over download per row is r = (2 n K_last / R) / (n / 8 / BW) = 16 K_last BW / R
+// (~12 at n = 131072, 55 GB/s, 8 Pbop/s): when it is large the slices shrink
+// geometrically (each <= shrink x the next, shrink = min(4, r / 2)) down to a last
+// slice of ~1/128 of the rows; otherwise six equal slices.
+std::vector<uint64_t> last_chunk_slices(uint64_t m_pad, uint64_t gm, uint64_t k_last) {
+    std::vector<uint64_t> sl;
+    const double r = 16.0 * double(k_last) * 55e9 / 8e15;
+    double max_shrink = 4.0, last_div = 128.0;
+    const char* mode = getenv("BMMGPU_KOUTER_SLICES");  // dev: "equal" = six equal slices, "S,D" = shrink, 1/last
+    if (mode && strcmp(mode, "equal")) sscanf(mode, "%lf,%lf", &max_shrink, &last_div);
+    const double shrink = std::min(max_shrink, r / 2);
+    if (shrink < 1.5 || (mode && !strcmp(mode, "equal"))) {
+        const uint64_t n_slices = std::max<uint64_t>(1, std::min<uint64_t>(6, m_pad / gm));
+        const uint64_t slice = round_up(ceil_div(m_pad, n_slices), gm);
+        for (uint64_t r0 = 0; r0 < m_pad; r0 += slice) sl.push_back(std::min(slice, m_pad - r0));
+        return sl;
+    }
+    uint64_t total = 0, s = round_up(std::max<uint64_t>(gm, uint64_t(double(m_pad) / last_div)), gm);
+    for (;;) {
+        if (m_pad - total <= s) {
+            sl.push_back(m_pad - total);
+            break;
+        }
+        sl.push_back(s);
+        total += s;
+        s = round_up(uint64_t(double(s) * shrink), gm);
+    }
+    std::reverse(sl.begin(), sl.end());
+    return sl;
 }
 }  // namespace
 
@@ -306,8 +343,8 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
         count_launch();
     }
     // row slices of the last chunk (multiples of the kernel's row tile)
-    const uint64_t n_slices = std::min<uint64_t>(6, m_pad / gm);
-    const uint64_t slice = round_up(ceil_div(m_pad, std::max<uint64_t>(n_slices, 1)), gm);
+    const std::vector<uint64_t> slices = last_chunk_slices(m_pad, gm, sched.back() * 64);
+    const uint64_t n_slices = slices.size();
     uint64_t w0 = 0;
     for (uint64_t q = 0; q < n_chunks; ++q) {
         const int buf = int(q & 1);
@@ -333,8 +370,8 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
                 return st;
         } else {
             int e_slot = 0;
-            for (uint64_t r0 = 0; r0 < m_pad; r0 += slice, e_slot ^= 1) {
-                const uint64_t rs = std::min(slice, m_pad - r0);
+            uint64_t r0 = 0;
+            for (const uint64_t rs : slices) {
                 if ((st = launch_cubic(kernel, dA[buf].u() + r0 * cwq, cwq, dBt[buf].u(), cwq, dC.u() + r0 * cw, cw,
                                        rs, n_pad, cwq, gf2, acc, cs, 1, 0, 0, 0)))
                     return st;
@@ -345,6 +382,8 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
                     BMMGPU_CUDA_TRY(memcpy2d_counted(C + (row_begin + r0) * nb, nb * 8, dC.u() + r0 * cw, cw * 8,
                                                       nb * 8, rows, cudaMemcpyDeviceToHost, ds));
                 }
+                r0 += rs;
+                e_slot ^= 1;
             }
         }
         BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[2 + buf], cs));
