@@ -24,6 +24,8 @@
 // All passes are HBM-streaming XOR kernels: bytes moved, not XORs, bound them.
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "../../include/bmmgpu.h"
@@ -493,12 +495,27 @@ __global__ void __launch_bounds__(256) scatter_xor_kernel(const uint64_t* __rest
     }
 }
 
+// Quadrant geometry of a select / scatter: L/2 x L/2 blocks whose four sources (or
+// targets) start sp rows / sp/64 words apart (sp = L/2: the quadrants of an L x L
+// matrix; sp > L/2: the same-position sub-blocks of four larger quadrants).
+PassGeom quad_geom(uint64_t L, uint64_t sp, int V) {
+    PassGeom g = pass_geom(L, 1, V);
+    if (sp) {
+        g.ls = sp;
+        g.ws = sp / 64;
+    }
+    return g;
+}
+
 int launch_select(const uint64_t* in, uint64_t ld_in, uint64_t L, uint64_t* out, uint64_t ld_out, uint32_t mask,
-                  cudaStream_t s) {
+                  cudaStream_t s, uint64_t sp = 0) {
     const uint64_t ws = L / 128;
-    const int V = (ws % 2 == 0 && ld_in % 2 == 0 && ld_out % 2 == 0 && aligned16(in) && aligned16(out)) ? 2 : 1;
-    const PassGeom g = pass_geom(L, 1, V);
-    const uint64_t total = g.ls * (ws / V);
+    const int V = (ws % 2 == 0 && ld_in % 2 == 0 && ld_out % 2 == 0 && (sp / 64) % 2 == 0 && aligned16(in) &&
+                   aligned16(out))
+                      ? 2
+                      : 1;
+    const PassGeom g = quad_geom(L, sp, V);
+    const uint64_t total = (L / 2) * (ws / V);
     if (V == 2)
         select_kernel<2><<<grid_for(total), 256, 0, s>>>(in, ld_in, total, g, out, ld_out, mask);
     else
@@ -509,12 +526,15 @@ int launch_select(const uint64_t* in, uint64_t ld_in, uint64_t L, uint64_t* out,
 }
 
 int launch_scatter(const uint64_t* q_in, uint64_t ld_q, uint64_t L, uint64_t* C, uint64_t ldc, uint32_t mask,
-                   cudaStream_t s) {
+                   cudaStream_t s, uint64_t sp = 0) {
     if (!mask) return kOk;
     const uint64_t ws = L / 128;
-    const int V = (ws % 2 == 0 && ld_q % 2 == 0 && ldc % 2 == 0 && aligned16(q_in) && aligned16(C)) ? 2 : 1;
-    const PassGeom g = pass_geom(L, 1, V);
-    const uint64_t total = g.ls * (ws / V);
+    const int V = (ws % 2 == 0 && ld_q % 2 == 0 && ldc % 2 == 0 && (sp / 64) % 2 == 0 && aligned16(q_in) &&
+                   aligned16(C))
+                      ? 2
+                      : 1;
+    const PassGeom g = quad_geom(L, sp, V);
+    const uint64_t total = (L / 2) * (ws / V);
     if (V == 2)
         scatter_xor_kernel<2><<<grid_for(total), 256, 0, s>>>(q_in, ld_q, total, g, C, ldc, mask);
     else
@@ -645,6 +665,9 @@ struct EventSet {
 // in.  The H2D of most of the operands and the D2H of most of C overlap the leaf
 // products.  With pageable host memory the copies are host-synchronous, so the
 // uploads are interleaved with the children and the downloads run at the end.
+int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, const Scheme* sc,
+                                int e, int kernel, const int* child, double* timing_ms);
+
 int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, const Scheme* sc,
                                int e, int kernel, double* timing_ms) {
     const uint64_t w = n / 64, half = n / 2, hw = w / 2;
@@ -689,6 +712,15 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
             }
         } while (std::next_permutation(perm, perm + 7));
     }
+    // Page-locked operands and result at n >= 2^17: the same top level, streamed in
+    // sub-blocks.  Below that the 49 grandchildren are too small to run at full rate
+    // (n = 65536: +1.6 ms in the block products, +3 ms span against quadrant
+    // streaming; n = 262144: -45 ms span, +3.2 % end to end; microbench/stream2_diag.py).
+    // BMMGPU_ALT_STREAM_LEVELS=1 / 2 forces one / two streamed levels (tests, A/B).
+    const char* lv_env = getenv("BMMGPU_ALT_STREAM_LEVELS");
+    const int stream_levels = lv_env ? atoi(lv_env) : (n >= (1u << 17) ? 2 : 1);
+    if (stream_levels == 2 && e >= 3 && n >= 1024 && host_pinned(A) && host_pinned(B) && host_pinned(C))
+        return alt_multiply_host_streamed2(A, B, C, n, sc, e, kernel, order, timing_ms);
     int last_pos[4] = {-1, -1, -1, -1};  // position in `order` after which quadrant q of C is final
     for (int i = 0; i < 7; ++i)
         for (int q = 0; q < 4; ++q)
@@ -795,6 +827,263 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
     BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, t0, t1);
+    if (timing_ms) *timing_ms = ms;
+    return kOk;
+}
+
+// Two-level streamed host path (e >= 3, page-locked A, B and C).  The top two levels
+// run depth-first as 49 grandchildren (child-major), and the copies move n/4 x n/4
+// sub-blocks instead of quadrants: a child's operand T_h (S_h) is formed sub-block
+// by sub-block as the A (Bt) sub-blocks it sums arrive, a grandchild starts once the
+// sub-blocks of T_h / S_h it selects exist, and each sub-block of C goes home as soon
+// as its last contribution is folded in.  The exposed head shrinks from the first
+// child's quadrants to the first grandchild's sub-blocks (4x smaller), the exposed
+// tail from the last child's C quadrants to the sub-blocks its last grandchild
+// finishes.  Orders: children by the quadrant model above, then each child's
+// grandchildren by an exhaustive 7! search over a sub-block pipeline model (one
+// upload engine, compute in order, one download engine), cached per (scheme, n).
+namespace {
+
+struct Orders2 {
+    int child[7];
+    int gc[7][7];
+};
+
+struct Model2 {
+    Masks7 ma, mb;
+    Masks4 mg;
+    double ts, tg;  // one sub-block copy, one grandchild product
+
+    // state after a prefix of the schedule
+    struct State {
+        uint32_t upA = 0, upB = 0;  // uploaded A sub-blocks (4q + u), B sub-blocks (4p + v), B indexing
+        double t_up = 0, t_comp = 0, t_d = 0;
+        double availA[16] = {}, availB[16] = {};
+    };
+
+    // last child (position) folding into C quadrant q
+    int last_child_pos(const int* child, int q) const {
+        int last = -1;
+        for (int i = 0; i < 7; ++i)
+            if (mg.m[q] & (1u << child[i])) last = i;
+        return last;
+    }
+
+    // run child `pos` (= child[pos]) with grandchild order `gco` from state `st`
+    void run_child(State& st, const int* child, int pos, const int* gco) const {
+        const int h = child[pos];
+        int lastg[4];  // position in gco after which Q_h sub-block j is final
+        for (int j = 0; j < 4; ++j) {
+            lastg[j] = -1;
+            for (int i = 0; i < 7; ++i)
+                if (mg.m[j] & (1u << gco[i])) lastg[j] = i;
+        }
+        for (int i = 0; i < 7; ++i) {
+            const int g = gco[i];
+            double ready = 0;
+            for (int q = 0; q < 4; ++q)
+                for (int u = 0; u < 4; ++u) {
+                    if ((ma.m[h] >> q & 1) && (ma.m[g] >> u & 1)) {
+                        const int b = 4 * q + u;
+                        if (!(st.upA >> b & 1)) {
+                            st.t_up += ts;
+                            st.availA[b] = st.t_up;
+                            st.upA |= 1u << b;
+                        }
+                        ready = std::max(ready, st.availA[b]);
+                    }
+                    if ((mb.m[h] >> q & 1) && (mb.m[g] >> u & 1)) {
+                        const int b = 4 * sigma(q) + sigma(u);
+                        if (!(st.upB >> b & 1)) {
+                            st.t_up += ts;
+                            st.availB[b] = st.t_up;
+                            st.upB |= 1u << b;
+                        }
+                        ready = std::max(ready, st.availB[b]);
+                    }
+                }
+            st.t_comp = std::max(st.t_comp, ready) + tg;
+            for (int j = 0; j < 4; ++j)
+                if (lastg[j] == i)
+                    for (int q = 0; q < 4; ++q)
+                        if ((mg.m[q] >> h & 1) && last_child_pos(child, q) == pos) st.t_d = std::max(st.t_d, st.t_comp) + ts;
+        }
+    }
+};
+
+const Orders2& orders2(const Scheme* sc, const Masks7& ma, const Masks7& mb, const Masks4& mg, const int* child,
+                       uint64_t n) {
+    static std::mutex mu;
+    static std::map<std::pair<const Scheme*, uint64_t>, Orders2> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({sc, n});
+    if (it != cache.end()) return it->second;
+    Model2 m{ma, mb, mg, 0, 0};
+    const double q4 = double(n) / 4;
+    m.ts = q4 * q4 / 8 / 50e9;
+    m.tg = 2.0 * q4 * q4 * q4 / 10e15;
+    Orders2 o{};
+    std::copy(child, child + 7, o.child);
+    Model2::State st;
+    for (int pos = 0; pos < 7; ++pos) {
+        int perm[7] = {0, 1, 2, 3, 4, 5, 6}, best_perm[7];
+        double best = 1e300;
+        do {
+            Model2::State t = st;
+            m.run_child(t, o.child, pos, perm);
+            const double cost = std::max(t.t_comp, t.t_d) + 1e-3 * t.t_comp;  // finish, then compute first
+            if (cost < best - 1e-12) {
+                best = cost;
+                std::copy(perm, perm + 7, best_perm);
+            }
+        } while (std::next_permutation(perm, perm + 7));
+        std::copy(best_perm, best_perm + 7, o.gc[pos]);
+        m.run_child(st, o.child, pos, o.gc[pos]);
+    }
+    return cache.emplace(std::make_pair(sc, n), o).first->second;
+}
+
+}  // namespace
+
+int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, const Scheme* sc,
+                                int e, int kernel, const int* child, double* timing_ms) {
+    const uint64_t w = n / 64, half = n / 2, hw = w / 2, quarter = n / 4, qw = w / 4;
+    const Masks7 ma = fused_expand(sc->alpha, sc->phi, sc->n_phi, false);
+    const Masks7 mb = fused_expand(sc->beta, sc->psi, sc->n_psi, true);
+    const Masks4 mg = fused_compress(sc);
+    const Orders2& ord = orders2(sc, ma, mb, mg, child, n);
+
+    struct Streams {
+        cudaStream_t c = nullptr, h = nullptr, d = nullptr;
+        cudaEvent_t ev[50] = {};  // 0-15 A blocks, 16-31 B blocks, 32-47 C blocks, 48/49 timing
+        ~Streams() {
+            for (auto e : ev)
+                if (e) cudaEventDestroy(e);
+            if (c) cudaStreamDestroy(c);
+            if (h) cudaStreamDestroy(h);
+            if (d) cudaStreamDestroy(d);
+        }
+    } st3;
+    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.c, cudaStreamNonBlocking));
+    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.h, cudaStreamNonBlocking));
+    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.d, cudaStreamNonBlocking));
+    for (int i = 0; i < 50; ++i)
+        BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&st3.ev[i], i >= 48 ? 0 : cudaEventDisableTiming));
+    const cudaStream_t s = st3.c;
+    int rc;
+    DevMem dA, dB, dBt, dC, T1, S1, Q1, T2, S2, Q2;
+    StreamDrain drain{{st3.c, st3.h, st3.d, nullptr}};
+    if ((rc = dA.alloc(n * w * 8, s)) || (rc = dB.alloc(n * w * 8, s)) || (rc = dBt.alloc(n * w * 8, s)) ||
+        (rc = dC.alloc(n * w * 8, s)) || (rc = T1.alloc(half * hw * 8, s)) || (rc = S1.alloc(half * hw * 8, s)) ||
+        (rc = Q1.alloc(half * hw * 8, s)) || (rc = T2.alloc(quarter * qw * 8, s)) ||
+        (rc = S2.alloc(quarter * qw * 8, s)) || (rc = Q2.alloc(quarter * qw * 8, s)))
+        return rc;
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
+    BMMGPU_CUDA_TRY(cudaMemsetAsync(dC.p, 0, n * w * 8, s));
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaEventRecord(st3.ev[48], s));
+    // sub-block (q, u) of an n x n matrix (ld w): quadrant q, its quadrant u
+    auto blk = [&](auto* base, int q, int u) {
+        return base + ((q >> 1) * half + (u >> 1) * quarter) * w + (q & 1) * hw + (u & 1) * qw;
+    };
+    auto sub = [&](uint64_t* base, int u) { return base + (u >> 1) * quarter * hw + (u & 1) * qw; };  // of a half
+    const int e2 = e - 2, es2 = choose_serial_levels(quarter, e2);
+    uint32_t upA = 0, upB = 0, waitA = 0, doneBt = 0;
+    // position of the last child folding into each C quadrant
+    int last_pos[4] = {-1, -1, -1, -1};
+    for (int i = 0; i < 7; ++i)
+        for (int q = 0; q < 4; ++q)
+            if (mg.m[q] & (1u << ord.child[i])) last_pos[q] = i;
+    for (int pos = 0; pos < 7; ++pos) {
+        const int h = ord.child[pos];
+        uint32_t formT = 0, formS = 0;
+        int lastg[4];
+        for (int j = 0; j < 4; ++j) {
+            lastg[j] = -1;
+            for (int i = 0; i < 7; ++i)
+                if (mg.m[j] & (1u << ord.gc[pos][i])) lastg[j] = i;
+        }
+        BMMGPU_CUDA_TRY(cudaMemsetAsync(Q1.p, 0, half * hw * 8, s));
+        count_launch();
+        for (int i = 0; i < 7; ++i) {
+            const int g = ord.gc[pos][i];
+            // T_h sub-block u = XOR of A sub-blocks (q, u), q in ma[h]; needed for u in ma[g]
+            for (int u = 0; u < 4; ++u) {
+                if (!(ma.m[g] >> u & 1) || (formT >> u & 1)) continue;
+                for (int q = 0; q < 4; ++q) {
+                    if (!(ma.m[h] >> q & 1)) continue;
+                    const int b = 4 * q + u;
+                    if (!(upA >> b & 1)) {
+                        BMMGPU_CUDA_TRY(memcpy2d_counted(blk(dA.u(), q, u), w * 8, blk(A, q, u), w * 8, qw * 8,
+                                                          quarter, cudaMemcpyHostToDevice, st3.h));
+                        BMMGPU_CUDA_TRY(cudaEventRecord(st3.ev[b], st3.h));
+                        upA |= 1u << b;
+                    }
+                    if (!(waitA >> b & 1)) {
+                        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(s, st3.ev[b]));
+                        waitA |= 1u << b;
+                    }
+                }
+                if ((rc = launch_select(blk(dA.u(), 0, u), w, half, sub(T1.u(), u), hw, ma.m[h], s, half))) return rc;
+                formT |= 1u << u;
+            }
+            // S_h sub-block v = XOR of Bt sub-blocks (t, v), t in mb[h]; Bt (t, v) is the
+            // transpose of B (sigma t, sigma v)
+            for (int v = 0; v < 4; ++v) {
+                if (!(mb.m[g] >> v & 1) || (formS >> v & 1)) continue;
+                for (int t = 0; t < 4; ++t) {
+                    if (!(mb.m[h] >> t & 1)) continue;
+                    const int bt = 4 * t + v, b = 4 * sigma(t) + sigma(v);
+                    if (!(upB >> b & 1)) {
+                        BMMGPU_CUDA_TRY(memcpy2d_counted(blk(dB.u(), sigma(t), sigma(v)), w * 8,
+                                                          blk(B, sigma(t), sigma(v)), w * 8, qw * 8, quarter,
+                                                          cudaMemcpyHostToDevice, st3.h));
+                        BMMGPU_CUDA_TRY(cudaEventRecord(st3.ev[16 + b], st3.h));
+                        upB |= 1u << b;
+                    }
+                    if (!(doneBt >> bt & 1)) {
+                        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(s, st3.ev[16 + b]));
+                        if ((rc = launch_transpose_ld(blk(dB.u(), sigma(t), sigma(v)), w, quarter, quarter,
+                                                      blk(dBt.u(), t, v), quarter, qw, w, s)))
+                            return rc;
+                        doneBt |= 1u << bt;
+                    }
+                }
+                if ((rc = launch_select(blk(dBt.u(), 0, v), w, half, sub(S1.u(), v), hw, mb.m[h], s, half)))
+                    return rc;
+                formS |= 1u << v;
+            }
+            if ((rc = launch_select(T1.u(), hw, half, T2.u(), qw, ma.m[g], s)) ||
+                (rc = launch_select(S1.u(), hw, half, S2.u(), qw, mb.m[g], s)))
+                return rc;
+            if ((rc = alt_serial(T2.u(), qw, S2.u(), qw, Q2.u(), qw, quarter, sc, es2, e2 - es2, kernel, s)))
+                return rc;
+            uint32_t jmask = 0;  // Q_h sub-blocks this grandchild folds into
+            for (int j = 0; j < 4; ++j)
+                if (mg.m[j] & (1u << g)) jmask |= 1u << j;
+            if ((rc = launch_scatter(Q2.u(), qw, half, Q1.u(), hw, jmask, s))) return rc;
+            // Q_h sub-blocks that are now final go into C's quadrants (chi . gamma column h)
+            uint32_t cmask = 0;
+            for (int q = 0; q < 4; ++q)
+                if (mg.m[q] & (1u << h)) cmask |= 1u << q;
+            for (int j = 0; j < 4; ++j) {
+                if (lastg[j] != i) continue;
+                if ((rc = launch_scatter(sub(Q1.u(), j), hw, half, blk(dC.u(), 0, j), w, cmask, s, half))) return rc;
+                for (int q = 0; q < 4; ++q)
+                    if ((cmask >> q & 1) && last_pos[q] == pos) {
+                        BMMGPU_CUDA_TRY(cudaEventRecord(st3.ev[32 + 4 * q + j], s));
+                        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(st3.d, st3.ev[32 + 4 * q + j]));
+                        BMMGPU_CUDA_TRY(memcpy2d_counted(blk(C, q, j), w * 8, blk(dC.u(), q, j), w * 8, qw * 8,
+                                                          quarter, cudaMemcpyDeviceToHost, st3.d));
+                    }
+            }
+        }
+    }
+    BMMGPU_CUDA_TRY(cudaEventRecord(st3.ev[49], s));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(st3.d));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, st3.ev[48], st3.ev[49]);
     if (timing_ms) *timing_ms = ms;
     return kOk;
 }

@@ -150,14 +150,18 @@ def test_device_fast_product_reads_operands_only(engine, oracle, leaf):
         assert torch.equal(dBt, bt0)
 
 
-@pytest.mark.parametrize("leaf", [6, 8])
-def test_streamed_host_path_pinned_buffers(engine, oracle, leaf):
+@pytest.mark.parametrize("n,leaf,levels", [(1024, 6, None), (1024, 8, None), (1024, 6, "2"), (1024, 8, "2"),
+                                           (2048, 8, "2"), (2048, 7, "2"), (2048, 8, "1")])
+def test_streamed_host_path_pinned_buffers(engine, oracle, monkeypatch, n, leaf, levels):
     """bmmgpu_multiply from page-locked host buffers: the streamed driver uploads A / B
-    quadrant by quadrant behind the first children and downloads each C quadrant as
-    soon as it is final; same bits as the cubic product for every scheme."""
+    quadrant by quadrant (below n = 2^17, or BMMGPU_ALT_STREAM_LEVELS=1) or sub-block by
+    sub-block over 49 grandchildren (e >= 3 and n >= 2^17, or BMMGPU_ALT_STREAM_LEVELS=2)
+    behind the first products and downloads each part of
+    C as soon as it is final; same bits as the cubic product for every scheme."""
     import torch
     bmm = engine
-    n = 1024
+    if levels:
+        monkeypatch.setenv("BMMGPU_ALT_STREAM_LEVELS", levels)
     a = oracle.random(n, n, 81)
     b = oracle.random(n, n, 82)
     want = oracle.multiply_cubic(a, b, n, n, n, GF2)
