@@ -1,7 +1,8 @@
 """Where the end-to-end time of the streamed fast path goes (dev helper): wall time of
 bmmgpu_multiply from pinned buffers against its device span (timing) and the time
 inside the block-product launches, for quadrant streaming (BMMGPU_ALT_STREAM_LEVELS=1)
-and sub-block streaming (default, e >= 3)."""
+and sub-block streaming (2: every child split into grandchildren, 3: first / last).
+argv: n reps modes (comma list)."""
 import ctypes
 import json
 import os
@@ -27,7 +28,8 @@ bmm.random_rows_into(hB.numpy().view(np.uint64), n, 2, 0, n)
 A = bmm.BitMatrix(n, n, hA.numpy().view(np.uint64))
 B = bmm.BitMatrix(n, n, hB.numpy().view(np.uint64))
 plan = bmm.LayerPlan.auto_plan(n, 1)
-for levels in ("1", "2", "1", "2"):
+modes = sys.argv[3].split(",") if len(sys.argv) > 3 else ["1", "2", "3"]
+for levels in modes + modes:
     os.environ["BMMGPU_ALT_STREAM_LEVELS"] = levels
     walls, spans, blocks = [], [], []
     for rep in range(reps + 1):

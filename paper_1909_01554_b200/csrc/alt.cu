@@ -26,6 +26,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "../../include/bmmgpu.h"
@@ -666,7 +667,7 @@ struct EventSet {
 // products.  With pageable host memory the copies are host-synchronous, so the
 // uploads are interleaved with the children and the downloads run at the end.
 int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, const Scheme* sc,
-                                int e, int kernel, const int* child, double* timing_ms);
+                                int e, int kernel, const int* child, uint32_t split, double* timing_ms);
 
 int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, const Scheme* sc,
                                int e, int kernel, double* timing_ms) {
@@ -712,15 +713,17 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
             }
         } while (std::next_permutation(perm, perm + 7));
     }
-    // Page-locked operands and result at n >= 2^17: the same top level, streamed in
-    // sub-blocks.  Below that the 49 grandchildren are too small to run at full rate
-    // (n = 65536: +1.6 ms in the block products, +3 ms span against quadrant
-    // streaming; n = 262144: -45 ms span, +3.2 % end to end; microbench/stream2_diag.py).
-    // BMMGPU_ALT_STREAM_LEVELS=1 / 2 forces one / two streamed levels (tests, A/B).
+    // Page-locked operands and result: the same top level, streamed in sub-blocks.  At
+    // n >= 2^17 every child runs as its 7 grandchildren (n = 262144: -45 ms span, +3.2 %
+    // end to end); below that only the first and the last child do -- the exposed head
+    // and tail -- since 49 grandchildren are too small to run at full rate (n = 65536:
+    // +1.6 ms in the block products; microbench/stream2_diag.py).
+    // BMMGPU_ALT_STREAM_LEVELS forces: 1 quadrants, 2 all children split, 3 first / last.
     const char* lv_env = getenv("BMMGPU_ALT_STREAM_LEVELS");
-    const int stream_levels = lv_env ? atoi(lv_env) : (n >= (1u << 17) ? 2 : 1);
-    if (stream_levels == 2 && e >= 3 && n >= 1024 && host_pinned(A) && host_pinned(B) && host_pinned(C))
-        return alt_multiply_host_streamed2(A, B, C, n, sc, e, kernel, order, timing_ms);
+    const int stream_mode = lv_env ? atoi(lv_env) : (n >= (1u << 17) ? 2 : 3);
+    if (stream_mode >= 2 && e >= 3 && n >= 1024 && host_pinned(A) && host_pinned(B) && host_pinned(C))
+        return alt_multiply_host_streamed2(A, B, C, n, sc, e, kernel, order, stream_mode == 2 ? 0x7Fu : 0x41u,
+                                           timing_ms);
     int last_pos[4] = {-1, -1, -1, -1};  // position in `order` after which quadrant q of C is final
     for (int i = 0; i < 7; ++i)
         for (int q = 0; q < 4; ++q)
@@ -869,21 +872,22 @@ struct Model2 {
         return last;
     }
 
-    // run child `pos` (= child[pos]) with grandchild order `gco` from state `st`
-    void run_child(State& st, const int* child, int pos, const int* gco) const {
+    // run child `pos` (= child[pos]) from state `st`: split, its grandchildren in order
+    // `gco`; whole, one product over all four sub-blocks of its operands
+    void run_child(State& st, const int* child, int pos, const int* gco, bool split) const {
         const int h = child[pos];
-        int lastg[4];  // position in gco after which Q_h sub-block j is final
+        int lastg[4];  // step after which Q_h sub-block j is final
         for (int j = 0; j < 4; ++j) {
-            lastg[j] = -1;
-            for (int i = 0; i < 7; ++i)
+            lastg[j] = split ? -1 : 0;
+            for (int i = 0; split && i < 7; ++i)
                 if (mg.m[j] & (1u << gco[i])) lastg[j] = i;
         }
-        for (int i = 0; i < 7; ++i) {
-            const int g = gco[i];
+        for (int i = 0; i < (split ? 7 : 1); ++i) {
+            const uint32_t am = split ? ma.m[gco[i]] : 0xF, bm = split ? mb.m[gco[i]] : 0xF;
             double ready = 0;
             for (int q = 0; q < 4; ++q)
                 for (int u = 0; u < 4; ++u) {
-                    if ((ma.m[h] >> q & 1) && (ma.m[g] >> u & 1)) {
+                    if ((ma.m[h] >> q & 1) && (am >> u & 1)) {
                         const int b = 4 * q + u;
                         if (!(st.upA >> b & 1)) {
                             st.t_up += ts;
@@ -892,7 +896,7 @@ struct Model2 {
                         }
                         ready = std::max(ready, st.availA[b]);
                     }
-                    if ((mb.m[h] >> q & 1) && (mb.m[g] >> u & 1)) {
+                    if ((mb.m[h] >> q & 1) && (bm >> u & 1)) {
                         const int b = 4 * sigma(q) + sigma(u);
                         if (!(st.upB >> b & 1)) {
                             st.t_up += ts;
@@ -902,7 +906,7 @@ struct Model2 {
                         ready = std::max(ready, st.availB[b]);
                     }
                 }
-            st.t_comp = std::max(st.t_comp, ready) + tg;
+            st.t_comp = std::max(st.t_comp, ready) + (split ? tg : 7 * tg);
             for (int j = 0; j < 4; ++j)
                 if (lastg[j] == i)
                     for (int q = 0; q < 4; ++q)
@@ -912,11 +916,11 @@ struct Model2 {
 };
 
 const Orders2& orders2(const Scheme* sc, const Masks7& ma, const Masks7& mb, const Masks4& mg, const int* child,
-                       uint64_t n) {
+                       uint64_t n, uint32_t split) {
     static std::mutex mu;
-    static std::map<std::pair<const Scheme*, uint64_t>, Orders2> cache;
+    static std::map<std::tuple<const Scheme*, uint64_t, uint32_t>, Orders2> cache;
     std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find({sc, n});
+    auto it = cache.find({sc, n, split});
     if (it != cache.end()) return it->second;
     Model2 m{ma, mb, mg, 0, 0};
     const double q4 = double(n) / 4;
@@ -926,11 +930,12 @@ const Orders2& orders2(const Scheme* sc, const Masks7& ma, const Masks7& mb, con
     std::copy(child, child + 7, o.child);
     Model2::State st;
     for (int pos = 0; pos < 7; ++pos) {
-        int perm[7] = {0, 1, 2, 3, 4, 5, 6}, best_perm[7];
+        int perm[7] = {0, 1, 2, 3, 4, 5, 6}, best_perm[7] = {0, 1, 2, 3, 4, 5, 6};
         double best = 1e300;
-        do {
+        const bool sp = split >> pos & 1;
+        if (sp) do {
             Model2::State t = st;
-            m.run_child(t, o.child, pos, perm);
+            m.run_child(t, o.child, pos, perm, true);
             const double cost = std::max(t.t_comp, t.t_d) + 1e-3 * t.t_comp;  // finish, then compute first
             if (cost < best - 1e-12) {
                 best = cost;
@@ -938,20 +943,20 @@ const Orders2& orders2(const Scheme* sc, const Masks7& ma, const Masks7& mb, con
             }
         } while (std::next_permutation(perm, perm + 7));
         std::copy(best_perm, best_perm + 7, o.gc[pos]);
-        m.run_child(st, o.child, pos, o.gc[pos]);
+        m.run_child(st, o.child, pos, o.gc[pos], sp);
     }
-    return cache.emplace(std::make_pair(sc, n), o).first->second;
+    return cache.emplace(std::make_tuple(sc, n, split), o).first->second;
 }
 
 }  // namespace
 
 int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, const Scheme* sc,
-                                int e, int kernel, const int* child, double* timing_ms) {
+                                int e, int kernel, const int* child, uint32_t split, double* timing_ms) {
     const uint64_t w = n / 64, half = n / 2, hw = w / 2, quarter = n / 4, qw = w / 4;
     const Masks7 ma = fused_expand(sc->alpha, sc->phi, sc->n_phi, false);
     const Masks7 mb = fused_expand(sc->beta, sc->psi, sc->n_psi, true);
     const Masks4 mg = fused_compress(sc);
-    const Orders2& ord = orders2(sc, ma, mb, mg, child, n);
+    const Orders2& ord = orders2(sc, ma, mb, mg, child, n, split);
 
     struct Streams {
         cudaStream_t c = nullptr, h = nullptr, d = nullptr;
@@ -988,6 +993,7 @@ int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* 
     };
     auto sub = [&](uint64_t* base, int u) { return base + (u >> 1) * quarter * hw + (u & 1) * qw; };  // of a half
     const int e2 = e - 2, es2 = choose_serial_levels(quarter, e2);
+    const int e1 = e - 1, es1 = choose_serial_levels(half, e1);
     uint32_t upA = 0, upB = 0, waitA = 0, doneBt = 0;
     // position of the last child folding into each C quadrant
     int last_pos[4] = {-1, -1, -1, -1};
@@ -996,20 +1002,26 @@ int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* 
             if (mg.m[q] & (1u << ord.child[i])) last_pos[q] = i;
     for (int pos = 0; pos < 7; ++pos) {
         const int h = ord.child[pos];
+        // split: the child's 7 grandchildren one by one; whole: one product of the
+        // child's full operands (its sub-blocks still formed as they arrive)
+        const bool split_h = split >> pos & 1;
         uint32_t formT = 0, formS = 0;
         int lastg[4];
         for (int j = 0; j < 4; ++j) {
-            lastg[j] = -1;
-            for (int i = 0; i < 7; ++i)
+            lastg[j] = split_h ? -1 : 0;
+            for (int i = 0; split_h && i < 7; ++i)
                 if (mg.m[j] & (1u << ord.gc[pos][i])) lastg[j] = i;
         }
-        BMMGPU_CUDA_TRY(cudaMemsetAsync(Q1.p, 0, half * hw * 8, s));
-        count_launch();
-        for (int i = 0; i < 7; ++i) {
+        if (split_h) {
+            BMMGPU_CUDA_TRY(cudaMemsetAsync(Q1.p, 0, half * hw * 8, s));
+            count_launch();
+        }
+        for (int i = 0; i < (split_h ? 7 : 1); ++i) {
             const int g = ord.gc[pos][i];
-            // T_h sub-block u = XOR of A sub-blocks (q, u), q in ma[h]; needed for u in ma[g]
+            const uint32_t am = split_h ? ma.m[g] : 0xF, bm = split_h ? mb.m[g] : 0xF;
+            // T_h sub-block u = XOR of A sub-blocks (q, u), q in ma[h]; needed for u in am
             for (int u = 0; u < 4; ++u) {
-                if (!(ma.m[g] >> u & 1) || (formT >> u & 1)) continue;
+                if (!(am >> u & 1) || (formT >> u & 1)) continue;
                 for (int q = 0; q < 4; ++q) {
                     if (!(ma.m[h] >> q & 1)) continue;
                     const int b = 4 * q + u;
@@ -1030,7 +1042,7 @@ int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* 
             // S_h sub-block v = XOR of Bt sub-blocks (t, v), t in mb[h]; Bt (t, v) is the
             // transpose of B (sigma t, sigma v)
             for (int v = 0; v < 4; ++v) {
-                if (!(mb.m[g] >> v & 1) || (formS >> v & 1)) continue;
+                if (!(bm >> v & 1) || (formS >> v & 1)) continue;
                 for (int t = 0; t < 4; ++t) {
                     if (!(mb.m[h] >> t & 1)) continue;
                     const int bt = 4 * t + v, b = 4 * sigma(t) + sigma(v);
@@ -1053,15 +1065,19 @@ int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* 
                     return rc;
                 formS |= 1u << v;
             }
-            if ((rc = launch_select(T1.u(), hw, half, T2.u(), qw, ma.m[g], s)) ||
-                (rc = launch_select(S1.u(), hw, half, S2.u(), qw, mb.m[g], s)))
+            if (split_h) {
+                if ((rc = launch_select(T1.u(), hw, half, T2.u(), qw, ma.m[g], s)) ||
+                    (rc = launch_select(S1.u(), hw, half, S2.u(), qw, mb.m[g], s)))
+                    return rc;
+                if ((rc = alt_serial(T2.u(), qw, S2.u(), qw, Q2.u(), qw, quarter, sc, es2, e2 - es2, kernel, s)))
+                    return rc;
+                uint32_t jmask = 0;  // Q_h sub-blocks this grandchild folds into
+                for (int j = 0; j < 4; ++j)
+                    if (mg.m[j] & (1u << g)) jmask |= 1u << j;
+                if ((rc = launch_scatter(Q2.u(), qw, half, Q1.u(), hw, jmask, s))) return rc;
+            } else if ((rc = alt_serial(T1.u(), hw, S1.u(), hw, Q1.u(), hw, half, sc, es1, e1 - es1, kernel, s))) {
                 return rc;
-            if ((rc = alt_serial(T2.u(), qw, S2.u(), qw, Q2.u(), qw, quarter, sc, es2, e2 - es2, kernel, s)))
-                return rc;
-            uint32_t jmask = 0;  // Q_h sub-blocks this grandchild folds into
-            for (int j = 0; j < 4; ++j)
-                if (mg.m[j] & (1u << g)) jmask |= 1u << j;
-            if ((rc = launch_scatter(Q2.u(), qw, half, Q1.u(), hw, jmask, s))) return rc;
+            }
             // Q_h sub-blocks that are now final go into C's quadrants (chi . gamma column h)
             uint32_t cmask = 0;
             for (int q = 0; q < 4; ++q)

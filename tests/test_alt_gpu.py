@@ -151,12 +151,13 @@ def test_device_fast_product_reads_operands_only(engine, oracle, leaf):
 
 
 @pytest.mark.parametrize("n,leaf,levels", [(1024, 6, None), (1024, 8, None), (1024, 6, "2"), (1024, 8, "2"),
-                                           (2048, 8, "2"), (2048, 7, "2"), (2048, 8, "1")])
+                                           (2048, 8, "2"), (2048, 7, "2"), (2048, 8, "1"), (2048, 7, "1"),
+                                           (2048, 7, "3"), (1024, 6, "3")])
 def test_streamed_host_path_pinned_buffers(engine, oracle, monkeypatch, n, leaf, levels):
     """bmmgpu_multiply from page-locked host buffers: the streamed driver uploads A / B
-    quadrant by quadrant (below n = 2^17, or BMMGPU_ALT_STREAM_LEVELS=1) or sub-block by
-    sub-block over 49 grandchildren (e >= 3 and n >= 2^17, or BMMGPU_ALT_STREAM_LEVELS=2)
-    behind the first products and downloads each part of
+    quadrant by quadrant (e = 2, or BMMGPU_ALT_STREAM_LEVELS=1) or sub-block by sub-block
+    (e >= 3: every child as its 7 grandchildren at n >= 2^17 or with =2, the first and
+    last child only below that or with =3) behind the first products and downloads each part of
     C as soon as it is final; same bits as the cubic product for every scheme."""
     import torch
     bmm = engine
