@@ -23,6 +23,8 @@
 // bit-identical to the cubic product and to the reference's 64-level-deep run.
 // All passes are HBM-streaming XOR kernels: bytes moved, not XORs, bound them.
 #include <algorithm>
+#include <array>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -682,7 +684,12 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
     // exposed head (first child's quadrants) plus the exposed tail (quadrants that only
     // complete with the last children).
     int order[7];
-    {
+    static std::mutex order_mu;
+    static std::map<std::pair<const Scheme*, uint64_t>, std::array<int, 7>> order_cache;
+    std::unique_lock<std::mutex> order_lock(order_mu);
+    if (auto it = order_cache.find({sc, n}); it != order_cache.end()) {
+        std::copy(it->second.begin(), it->second.end(), order);
+    } else {
         const double quad_bytes = double(n) * double(n) / 32.0;  // one quadrant of one operand
         const double tq = quad_bytes / 50e9;                     // PCIe 5 x16, measured ~55 GB/s
         const double tc = (2.0 * double(n) * n * n / 7.0) / 10e15; // a child at ~10 effective Pbop/s
@@ -712,7 +719,11 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
                 std::copy(perm, perm + 7, order);
             }
         } while (std::next_permutation(perm, perm + 7));
+        std::array<int, 7> o;
+        std::copy(order, order + 7, o.begin());
+        order_cache.emplace(std::make_pair(sc, n), o);
     }
+    order_lock.unlock();
     // Page-locked operands and result: the same top level, streamed in sub-blocks.  At
     // n >= 2^17 every child runs as its 7 grandchildren (n = 262144: -45 ms span, +3.2 %
     // end to end); below that only the first and the last child do -- the exposed head
@@ -960,7 +971,8 @@ int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* 
 
     struct Streams {
         cudaStream_t c = nullptr, h = nullptr, d = nullptr;
-        cudaEvent_t ev[50] = {};  // 0-15 A blocks, 16-31 B blocks, 32-47 C blocks, 48/49 timing
+        cudaEvent_t ev[73] = {};  // 0-15 A blocks, 16-31 B blocks, 32-47 C blocks, 48/49 timing,
+                                  // trace: 50-56 child ends, 57-72 C downloads done
         ~Streams() {
             for (auto e : ev)
                 if (e) cudaEventDestroy(e);
@@ -972,8 +984,9 @@ int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* 
     BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.c, cudaStreamNonBlocking));
     BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.h, cudaStreamNonBlocking));
     BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.d, cudaStreamNonBlocking));
-    for (int i = 0; i < 50; ++i)
-        BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&st3.ev[i], i >= 48 ? 0 : cudaEventDisableTiming));
+    const bool trace = getenv("BMMGPU_ALT_TRACE") != nullptr;  // dev: per-block timeline on stderr
+    for (int i = 0; i < (trace ? 73 : 50); ++i)
+        BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&st3.ev[i], trace || i >= 48 ? 0 : cudaEventDisableTiming));
     const cudaStream_t s = st3.c;
     int rc;
     DevMem dA, dB, dBt, dC, T1, S1, Q1, T2, S2, Q2;
@@ -1091,9 +1104,11 @@ int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* 
                         BMMGPU_CUDA_TRY(cudaStreamWaitEvent(st3.d, st3.ev[32 + 4 * q + j]));
                         BMMGPU_CUDA_TRY(memcpy2d_counted(blk(C, q, j), w * 8, blk(dC.u(), q, j), w * 8, qw * 8,
                                                           quarter, cudaMemcpyDeviceToHost, st3.d));
+                        if (trace) BMMGPU_CUDA_TRY(cudaEventRecord(st3.ev[57 + 4 * q + j], st3.d));
                     }
             }
         }
+        if (trace) BMMGPU_CUDA_TRY(cudaEventRecord(st3.ev[50 + pos], s));
     }
     BMMGPU_CUDA_TRY(cudaEventRecord(st3.ev[49], s));
     BMMGPU_CUDA_TRY(cudaStreamSynchronize(st3.d));
@@ -1101,6 +1116,21 @@ int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* 
     float ms = 0.f;
     cudaEventElapsedTime(&ms, st3.ev[48], st3.ev[49]);
     if (timing_ms) *timing_ms = ms;
+    if (trace) {
+        auto at = [&](int i) {
+            float t = -1.f;
+            if (cudaEventElapsedTime(&t, st3.ev[48], st3.ev[i]) != cudaSuccess) {
+                cudaGetLastError();
+                return -1.f;
+            }
+            return t;
+        };
+        fprintf(stderr, "alt streamed2 n=%llu split=0x%x span %.2f ms\n", (unsigned long long)n, split, ms);
+        for (int pos = 0; pos < 7; ++pos)
+            fprintf(stderr, "  child %d (h=%d): ends %.2f\n", pos, ord.child[pos], at(50 + pos));
+        for (int b = 0; b < 16; ++b) fprintf(stderr, "  A(%d,%d) up %.2f   B(%d,%d) up %.2f   C(%d,%d) down %.2f\n",
+                                             b / 4, b % 4, at(b), b / 4, b % 4, at(16 + b), b / 4, b % 4, at(57 + b));
+    }
     return kOk;
 }
 
