@@ -740,17 +740,11 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
         for (int q = 0; q < 4; ++q)
             if (mg.m[q] & (1u << order[i])) last_pos[q] = i;
 
-    struct Streams {
-        cudaStream_t c = nullptr, h = nullptr, d = nullptr;
-        ~Streams() {
-            if (c) cudaStreamDestroy(c);
-            if (h) cudaStreamDestroy(h);
-            if (d) cudaStreamDestroy(d);
-        }
-    } st3;
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.c, cudaStreamNonBlocking));
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.h, cudaStreamNonBlocking));
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.d, cudaStreamNonBlocking));
+    StreamSet ss;  // compute, uploads, downloads
+    if (int r = ss.acquire(3)) return r;
+    struct {
+        cudaStream_t c, h, d;
+    } st3{ss[0], ss[1], ss[2]};
     const cudaStream_t s = st3.c;
     EventSet evs;  // 0-3 A quadrants, 4-7 B quadrants, 8-11 C quadrants
     for (auto& ev : evs.ev) BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -969,6 +963,8 @@ int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* 
     const Masks4 mg = fused_compress(sc);
     const Orders2& ord = orders2(sc, ma, mb, mg, child, n, split);
 
+    StreamSet ss;  // compute, uploads, downloads
+    if (int r = ss.acquire(3)) return r;
     struct Streams {
         cudaStream_t c = nullptr, h = nullptr, d = nullptr;
         cudaEvent_t ev[73] = {};  // 0-15 A blocks, 16-31 B blocks, 32-47 C blocks, 48/49 timing,
@@ -976,14 +972,11 @@ int alt_multiply_host_streamed2(const uint64_t* A, const uint64_t* B, uint64_t* 
         ~Streams() {
             for (auto e : ev)
                 if (e) cudaEventDestroy(e);
-            if (c) cudaStreamDestroy(c);
-            if (h) cudaStreamDestroy(h);
-            if (d) cudaStreamDestroy(d);
         }
     } st3;
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.c, cudaStreamNonBlocking));
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.h, cudaStreamNonBlocking));
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&st3.d, cudaStreamNonBlocking));
+    st3.c = ss[0];
+    st3.h = ss[1];
+    st3.d = ss[2];
     const bool trace = getenv("BMMGPU_ALT_TRACE") != nullptr;  // dev: per-block timeline on stderr
     for (int i = 0; i < (trace ? 73 : 50); ++i)
         BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&st3.ev[i], trace || i >= 48 ? 0 : cudaEventDisableTiming));
@@ -1149,12 +1142,9 @@ int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_
         return alt_multiply_host_streamed(A, B, C, n, sc, e, kernel, timing_ms);
     }
     const uint64_t w = n / 64;
-    cudaStream_t s;
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    struct G {
-        cudaStream_t s;
-        ~G() { cudaStreamDestroy(s); }
-    } guard{s};
+    StreamSet ss;
+    if (int r = ss.acquire(1)) return r;
+    const cudaStream_t s = ss[0];
     int st;
     DevMem dA, dB, dBt, dC;
     uint64_t gm, gn, gk;
@@ -1422,12 +1412,9 @@ int multiply_alt_interleaved(const uint64_t* a_hat, const uint64_t* b_hat, uint6
     if ((st = granularity(kernel, &gm, &gn, &gk))) return st;
     const int e = alt_levels(n, leaf_log2);
     const uint64_t rows_pad = round_up(n, std::max(gm, gn)), kw = round_up(w, gk / 64), cw = rows_pad / 64;
-    cudaStream_t s;
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    struct G {
-        cudaStream_t s;
-        ~G() { cudaStreamDestroy(s); }
-    } guard{s};
+    StreamSet ss;
+    if (int r = ss.acquire(1)) return r;
+    const cudaStream_t s = ss[0];
     DevMem dV, dA, dBt, dC;
     if ((st = dV.alloc(total * 8, s)) || (st = dA.alloc(rows_pad * kw * 8, s)) ||
         (st = dBt.alloc(round_up(rows_pad, 256) * kw * 8, s)) || (st = dC.alloc(rows_pad * cw * 8, s)))

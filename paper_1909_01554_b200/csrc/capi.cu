@@ -69,6 +69,40 @@ void enable_pool_caching() {
     }
     done_mask |= 1u << dev;
 }
+namespace {
+std::mutex g_stream_mu;
+std::vector<cudaStream_t> g_stream_pool[32];  // idle leased-out-and-returned streams per device
+}  // namespace
+
+int StreamSet::acquire(int count) {
+    if (cudaGetDevice(&device) != cudaSuccess || device < 0 || device >= 32) return kEcuda;
+    n = 0;
+    {
+        std::lock_guard<std::mutex> lock(g_stream_mu);
+        auto& pool = g_stream_pool[device];
+        while (n < count && !pool.empty()) {
+            s[n++] = pool.back();
+            pool.pop_back();
+        }
+    }
+    for (; n < count; ++n) {
+        const cudaError_t e = cudaStreamCreateWithFlags(&s[n], cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            s[n] = nullptr;
+            set_error(std::string("cudaStreamCreateWithFlags: ") + cudaGetErrorString(e));
+            return kEcuda;
+        }
+    }
+    return kOk;
+}
+
+StreamSet::~StreamSet() {
+    if (n == 0) return;
+    std::lock_guard<std::mutex> lock(g_stream_mu);
+    for (int i = 0; i < n; ++i)
+        if (s[i]) g_stream_pool[device].push_back(s[i]);
+}
+
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
 void count_copy(cudaMemcpyKind kind, uint64_t bytes) {
@@ -313,14 +347,29 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
     const uint64_t kw = round_up(std::max<uint64_t>(ka, 1), gk / 64);
     const uint64_t cw = n_pad / 64;
     {
-        uint64_t limit = budget;
-        if (limit == 0) {
-            size_t free_b = 0, total_b = 0;
-            BMMGPU_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-            limit = uint64_t(double(free_b) * 0.9);
-        }
         const uint64_t in_core = (m_pad * kw + k * nb + n_pad * kw + m_pad * cw) * 8;
         const uint64_t c_slab = m_pad * cw * 8;
+        uint64_t limit = budget;
+        if (limit == 0) {
+            // cudaMemGetInfo costs ~65 us of host time: small products (under 1/32 of the
+            // device) skip it and take the in-core path
+            static std::mutex mu;
+            static uint64_t total_mem[32] = {};
+            uint64_t total = 0;
+            {
+                std::lock_guard<std::mutex> lock(mu);
+                total = job.device < 32 ? total_mem[job.device] : 0;
+            }
+            if (total && in_core * 32 <= total && k < 32768) {
+                limit = in_core;
+            } else {
+                size_t free_b = 0, total_b = 0;
+                BMMGPU_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+                limit = uint64_t(double(free_b) * 0.9);
+                std::lock_guard<std::mutex> lock(mu);
+                if (job.device < 32) total_mem[job.device] = total_b;
+            }
+        }
         // force_streaming 1: the out-of-core tile driver; 2: the K-outer pipeline.
         // Otherwise: long K with C resident -> K-outer pipeline (H2D hidden behind
         // the product); everything fits -> in core; else the tile driver.
@@ -334,56 +383,87 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
                                                                        ? atoi(getenv("BMMGPU_KOUTER_CHUNKS"))
                                                                        : 0);
     }
-    cudaStream_t s;
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    struct StreamGuard {
-        cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } sg{s};
+    // In core, pipelined over row slices of A / C: B goes up first (every slice needs
+    // all of it) and is transposed while the A slices follow on the copy stream; slice
+    // i's product starts when its rows of A have landed and its rows of C go home on a
+    // download stream while slice i + 1 computes.  Exposed: B's upload, one A slice,
+    // the last slice's product and download (n = 8192: the in-order H2D / product /
+    // D2H sequence was ~0.62 ms of copies and kernels).  Slices keep >= 8 row tiles.
+    const char* sl_env = getenv("BMMGPU_INCORE_SLICES");  // dev: 1 = one slice (in order)
+    const uint64_t row_tiles = m_pad / gm;
+    const uint64_t n_slices =
+        std::max<uint64_t>(1, std::min<uint64_t>(sl_env ? std::max(1, atoi(sl_env)) : 4, row_tiles / 8));
+    const uint64_t slice = round_up(ceil_div(m_pad, n_slices), gm);
+    StreamSet ss;
+    if ((st = ss.acquire(3))) return st;
+    struct Events {
+        std::vector<cudaEvent_t> ev;
+        ~Events() {
+            for (auto e : ev)
+                if (e) cudaEventDestroy(e);
+        }
+    } pp;
+    // events: 0 allocated, 1 B ready, 2 / 3 timing, then per slice: A ready, C ready
+    pp.ev.assign(4 + 2 * size_t(ceil_div(m_pad, slice)), nullptr);
+    for (size_t i = 0; i < pp.ev.size(); ++i)
+        BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&pp.ev[i], i == 2 || i == 3 ? 0 : cudaEventDisableTiming));
+    const cudaStream_t cs = ss[0], xs = ss[1], ds = ss[2];
     DeviceBuffer dA, dB, dBt, dC;
-    if ((st = dA.alloc(m_pad * kw * 8, s)) || (st = dBt.alloc(n_pad * kw * 8, s)) ||
-        (st = dC.alloc(m_pad * cw * 8, s)))
+    StreamDrain drain{{cs, xs, ds, nullptr}};
+    if ((st = dA.alloc(m_pad * kw * 8, cs)) || (st = dBt.alloc(n_pad * kw * 8, cs)) ||
+        (st = dC.alloc(m_pad * cw * 8, cs)) || (k > 0 && (st = dB.alloc(k * nb * 8, cs))))
         return st;
-    // A slab into the zero-padded panel (pad columns / rows stay zero).
-    BMMGPU_CUDA_TRY(cudaMemsetAsync(dA.p, 0, m_pad * kw * 8, s));
-    count_launch();
-    if (ka > 0)
-        BMMGPU_CUDA_TRY(memcpy2d_counted(dA.p, kw * 8, A + job.row_begin * ka, ka * 8, ka * 8, m,
-                                          cudaMemcpyHostToDevice, s));
-    // B, then Bt on device.
-    if (k > 0 && nb > 0) {
-        if ((st = dB.alloc(k * nb * 8, s))) return st;
-        BMMGPU_CUDA_TRY(memcpy_counted(dB.p, B, k * nb * 8, cudaMemcpyHostToDevice, s));
-        if ((st = launch_transpose(dB.u(), nb, k, n, dBt.u(), n_pad, kw, s))) return st;
+    BMMGPU_CUDA_TRY(cudaEventRecord(pp.ev[0], cs));
+    BMMGPU_CUDA_TRY(cudaStreamWaitEvent(xs, pp.ev[0], 0));
+    BMMGPU_CUDA_TRY(cudaStreamWaitEvent(ds, pp.ev[0], 0));
+    // B, then Bt on device
+    if (k > 0) BMMGPU_CUDA_TRY(memcpy_counted(dB.p, B, k * nb * 8, cudaMemcpyHostToDevice, xs));
+    BMMGPU_CUDA_TRY(cudaEventRecord(pp.ev[1], xs));
+    // A slab into the zero-padded panel (pad columns / rows stay zero)
+    if (m_pad != m || kw != ka) {
+        BMMGPU_CUDA_TRY(cudaMemsetAsync(dA.p, 0, m_pad * kw * 8, xs));
+        count_launch();
+    }
+    if (accumulate) {
+        BMMGPU_CUDA_TRY(cudaMemsetAsync(dC.p, 0, m_pad * cw * 8, xs));
+        count_launch();
+    }
+    BMMGPU_CUDA_TRY(cudaStreamWaitEvent(cs, pp.ev[1], 0));
+    if (k > 0) {
+        if ((st = launch_transpose(dB.u(), nb, k, n, dBt.u(), n_pad, kw, cs))) return st;
     } else {
-        BMMGPU_CUDA_TRY(cudaMemsetAsync(dBt.p, 0, n_pad * kw * 8, s));
+        BMMGPU_CUDA_TRY(cudaMemsetAsync(dBt.p, 0, n_pad * kw * 8, cs));
         count_launch();
     }
-    if (accumulate && nb > 0) {
-        BMMGPU_CUDA_TRY(cudaMemsetAsync(dC.p, 0, m_pad * cw * 8, s));
-        count_launch();
-        BMMGPU_CUDA_TRY(memcpy2d_counted(dC.p, cw * 8, C + job.row_begin * nb, nb * 8, nb * 8, m,
-                                          cudaMemcpyHostToDevice, s));
+    BMMGPU_CUDA_TRY(cudaEventRecord(pp.ev[2], cs));
+    size_t si = 0;
+    for (uint64_t r0 = 0; r0 < m_pad; r0 += slice, ++si) {
+        const uint64_t rs = std::min(slice, m_pad - r0);
+        const uint64_t rows = r0 < m ? std::min(rs, m - r0) : 0;  // real rows of this slice
+        cudaEvent_t a_ready = pp.ev[4 + 2 * si], c_ready = pp.ev[5 + 2 * si];
+        if (rows > 0 && ka > 0)
+            BMMGPU_CUDA_TRY(memcpy2d_counted(dA.u() + r0 * kw, kw * 8, A + (job.row_begin + r0) * ka, ka * 8,
+                                              ka * 8, rows, cudaMemcpyHostToDevice, xs));
+        if (rows > 0 && accumulate)
+            BMMGPU_CUDA_TRY(memcpy2d_counted(dC.u() + r0 * cw, cw * 8, C + (job.row_begin + r0) * nb, nb * 8,
+                                              nb * 8, rows, cudaMemcpyHostToDevice, xs));
+        BMMGPU_CUDA_TRY(cudaEventRecord(a_ready, xs));
+        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(cs, a_ready, 0));
+        if ((st = launch_cubic(kernel, dA.u() + r0 * kw, kw, dBt.u(), kw, dC.u() + r0 * cw, cw, rs, n_pad, kw, gf2,
+                               accumulate, cs, 1, 0, 0, 0)))
+            return st;
+        BMMGPU_CUDA_TRY(cudaEventRecord(c_ready, cs));
+        if (rows > 0) {
+            BMMGPU_CUDA_TRY(cudaStreamWaitEvent(ds, c_ready, 0));
+            BMMGPU_CUDA_TRY(memcpy2d_counted(C + (job.row_begin + r0) * nb, nb * 8, dC.u() + r0 * cw, cw * 8, nb * 8,
+                                              rows, cudaMemcpyDeviceToHost, ds));
+        }
     }
-    cudaEvent_t e0, e1;
-    BMMGPU_CUDA_TRY(cudaEventCreate(&e0));
-    BMMGPU_CUDA_TRY(cudaEventCreate(&e1));
-    BMMGPU_CUDA_TRY(cudaEventRecord(e0, s));
-    st = launch_cubic(kernel, dA.u(), kw, dBt.u(), kw, dC.u(), cw, m_pad, n_pad, kw, gf2, accumulate, s, 1, 0, 0,
-                      0);
-    if (st) {
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        return st;
-    }
-    BMMGPU_CUDA_TRY(cudaEventRecord(e1, s));
-    if (nb > 0)
-        BMMGPU_CUDA_TRY(memcpy2d_counted(C + job.row_begin * nb, nb * 8, dC.p, cw * 8, nb * 8, m,
-                                          cudaMemcpyDeviceToHost, s));
-    BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
-    cudaEventElapsedTime(&job.ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    BMMGPU_CUDA_TRY(cudaEventRecord(pp.ev[3], cs));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(ds));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(cs));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(xs));
+    cudaEventElapsedTime(&job.ms, pp.ev[2], pp.ev[3]);
     return kOk;
 }
 

@@ -39,6 +39,22 @@ inline cudaError_t memcpy_counted(void* dst, const void* src, size_t bytes, cuda
 // level's buffer needs no stream synchronisation.
 void enable_pool_caching();
 
+// Non-blocking streams leased from a per-device pool: creating and destroying a
+// stream costs ~100 us of host time (measured, microbench/api_cost.py), three per call
+// were most of a small product's end-to-end time.  Concurrent calls lease distinct
+// streams; a lease goes back to the pool when the set is destroyed -- declare it
+// before the driver's buffers and StreamDrain, so the streams are idle by then.
+struct StreamSet {
+    int device = -1, n = 0;
+    cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};
+    StreamSet() = default;
+    StreamSet(const StreamSet&) = delete;
+    StreamSet& operator=(const StreamSet&) = delete;
+    int acquire(int count);  // on the current device; 0 or a CUDA status
+    ~StreamSet();
+    cudaStream_t operator[](int i) const { return s[i]; }
+};
+
 // Declared after a driver's buffers, so it is destroyed first: waits for every stream
 // the driver used before the buffers' stream-ordered frees run (on error returns the
 // copy streams may still be reading or writing them).

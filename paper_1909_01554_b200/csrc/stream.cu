@@ -116,20 +116,9 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
     const uint64_t TNw = P.TN / 64;
     const uint64_t KC = P.KCw * 64;
 
-    cudaStream_t cs, xs, as, ds;  // compute, B copies, A prefetch, C downloads
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&as, cudaStreamNonBlocking));
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
-    struct Guard {
-        cudaStream_t a, b, c, d;
-        ~Guard() {
-            cudaStreamDestroy(a);
-            cudaStreamDestroy(b);
-            cudaStreamDestroy(c);
-            cudaStreamDestroy(d);
-        }
-    } guard{cs, xs, as, ds};
+    StreamSet ss;  // compute, B copies, A prefetch, C downloads
+    if ((st = ss.acquire(4))) return st;
+    const cudaStream_t cs = ss[0], xs = ss[1], as = ss[2], ds = ss[3];
     // 0,1 b_ready[buf]  2,3 b_free[buf]  4,5 a_ready[abuf]  6,7 a_free[abuf]
     // 8,9 c_done[cbuf]  10,11 c_free[cbuf]  12 start  13 stop
     Events ev;
@@ -310,18 +299,9 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
     const std::vector<uint64_t> sched = kouter_chunks(kw, gkw, KCw, chunks);
     const uint64_t n_chunks = sched.size();
 
-    cudaStream_t cs, xs, ds;  // compute, uploads, downloads
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
-    BMMGPU_CUDA_TRY(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
-    struct Guard {
-        cudaStream_t a, b, c;
-        ~Guard() {
-            cudaStreamDestroy(a);
-            cudaStreamDestroy(b);
-            cudaStreamDestroy(c);
-        }
-    } guard{cs, xs, ds};
+    StreamSet ss;  // compute, uploads, downloads
+    if ((st = ss.acquire(3))) return st;
+    const cudaStream_t cs = ss[0], xs = ss[1], ds = ss[2];
     Events ev;  // 0,1 ready[buf]; 2,3 free[buf]; 5 start; 6 stop; 8.. slice done
     for (int i = 0; i < 14; ++i)
         BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&ev.e[i], i == 5 || i == 6 ? 0 : cudaEventDisableTiming));
