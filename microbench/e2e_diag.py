@@ -33,18 +33,24 @@ hC = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
 bmm.random_rows_into(hA.numpy().view(np.uint64), n, 1, 0, n)
 bmm.random_rows_into(h.numpy().view(np.uint64), n, 2, 0, n)
 import os
-cases = [(0, None, v) for _ in range(3) for v in ("equal", None, "3,64", "2,32")]
+# each case: "-" (defaults) or "VAR=val,VAR=val" library knobs; argv[2:] or the slice A/B
+case_args = [a for a in sys.argv[1:] if not a.isdigit() and a != "--all"]
+if not case_args:
+    case_args = ["BMMGPU_KOUTER_SLICES=equal", "-", "BMMGPU_KOUTER_SLICES=3,64", "BMMGPU_KOUTER_SLICES=2,32"]
+knobs = sorted({kv.split("=")[0] for c in case_args if c != "-" for kv in c.split(",")})
+cases = [(0, None, c) for _ in range(3) for c in case_args]
 if "--all" in sys.argv:
-    cases += [(1, None, None), (2, "2", None), (2, "3", None), (2, "4", None), (2, "8", None)]
-for mode, chunks, slices in cases:
-    if slices:
-        os.environ["BMMGPU_KOUTER_SLICES"] = slices
-    else:
-        os.environ.pop("BMMGPU_KOUTER_SLICES", None)
+    cases += [(1, None, "-"), (2, "2", "-"), (2, "3", "-"), (2, "4", "-"), (2, "8", "-")]
+for mode, chunks, case in cases:
+    for kname in knobs + ["BMMGPU_KOUTER_CHUNKS"]:
+        os.environ.pop(kname, None)
+    if case != "-":
+        for kv in case.split(","):
+            kk, vv = kv.split("=", 1)
+            os.environ[kk] = vv
     if chunks:
         os.environ["BMMGPU_KOUTER_CHUNKS"] = chunks
-    else:
-        os.environ.pop("BMMGPU_KOUTER_CHUNKS", None)
+    slices = case
     t = ctypes.c_double(0)
     opts = bmm._opts(0, timing=t, device_mask=1, force_streaming=mode)
     walls = []

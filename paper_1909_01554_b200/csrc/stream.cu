@@ -325,6 +325,8 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
     // row slices of the last chunk (multiples of the kernel's row tile)
     const std::vector<uint64_t> slices = last_chunk_slices(m_pad, gm, sched.back() * 64);
     const uint64_t n_slices = slices.size();
+    const char* xp_env = getenv("BMMGPU_KOUTER_XPOSE");
+    const bool xpose_on_cs = xp_env && !strcmp(xp_env, "cs");
     uint64_t w0 = 0;
     for (uint64_t q = 0; q < n_chunks; ++q) {
         const int buf = int(q & 1);
@@ -333,16 +335,27 @@ int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const u
         const uint64_t k0 = w0 * 64;
         const uint64_t krows = k0 < k ? std::min<uint64_t>(cwq * 64, k - k0) : 0;
         BMMGPU_CUDA_TRY(cudaStreamWaitEvent(xs, ev.e[2 + buf], 0));
-        BMMGPU_CUDA_TRY(cudaMemsetAsync(dA[buf].p, 0, m_pad * cwq * 8, xs));
-        count_launch();
+        if (aw < cwq || m_pad > m) {  // zero pad rows / words (none when the chunk is dense)
+            BMMGPU_CUDA_TRY(cudaMemsetAsync(dA[buf].p, 0, m_pad * cwq * 8, xs));
+            count_launch();
+        }
         if (aw > 0)
             BMMGPU_CUDA_TRY(memcpy2d_counted(dA[buf].p, cwq * 8, A + row_begin * ka + w0, ka * 8, aw * 8, m,
                                               cudaMemcpyHostToDevice, xs));
         if (krows > 0)
             BMMGPU_CUDA_TRY(memcpy_counted(dB[buf].p, B + k0 * nb, krows * nb * 8, cudaMemcpyHostToDevice, xs));
-        BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[buf], xs));
-        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(cs, ev.e[buf], 0));
-        if ((st = launch_transpose(dB[buf].u(), nb, krows, n, dBt[buf].u(), n_pad, cwq, cs))) return st;
+        // Later chunks' B transposes run on the copy stream, queued behind the running
+        // product instead of between two products on the compute stream
+        // (BMMGPU_KOUTER_XPOSE=cs: on the compute stream, dev A/B).
+        if (q > 0 && !xpose_on_cs) {
+            if ((st = launch_transpose(dB[buf].u(), nb, krows, n, dBt[buf].u(), n_pad, cwq, xs))) return st;
+            BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[buf], xs));
+            BMMGPU_CUDA_TRY(cudaStreamWaitEvent(cs, ev.e[buf], 0));
+        } else {
+            BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[buf], xs));
+            BMMGPU_CUDA_TRY(cudaStreamWaitEvent(cs, ev.e[buf], 0));
+            if ((st = launch_transpose(dB[buf].u(), nb, krows, n, dBt[buf].u(), n_pad, cwq, cs))) return st;
+        }
         const bool acc = accumulate || q > 0;
         if (q + 1 < n_chunks || n_slices < 2) {
             if ((st = launch_cubic(kernel, dA[buf].u(), cwq, dBt[buf].u(), cwq, dC.u(), cw, m_pad, n_pad, cwq, gf2,

@@ -306,3 +306,49 @@ def test_concurrent_long_k_products_on_one_device(engine, oracle):
             bits = np.unpackbits(A[r].view(np.uint8), bitorder="little")[:k]
             want = np.bitwise_xor.reduce(B[np.flatnonzero(bits)], axis=0)
             assert np.array_equal(outs[i].words.reshape(m, n // 64)[r], want), (i, r)
+
+
+@pytest.mark.parametrize("slices", [None, "1", "3"])
+def test_in_core_row_slices(engine, oracle, monkeypatch, slices):
+    """csrc/capi.cu in-core path: A / C row slices pipelined behind B's upload, the last
+    slice ragged (m = 4100: 17 row tiles) and padded columns / K; accumulate folds into
+    the uploaded C slice by slice.  Same bits for any slice count."""
+    bmm = engine
+    if slices:
+        monkeypatch.setenv("BMMGPU_INCORE_SLICES", slices)
+    m, k, n = 4100, 777, 1000
+    a = _bm(bmm, oracle, m, k, 91)
+    b = _bm(bmm, oracle, k, n, 92)
+    for ring in (GF2, BOOL):
+        want = oracle.multiply_cubic(a.words, b.words, m, k, n, ring)
+        c = bmm.multiply_cubic(a, b, bmm.Semiring(ring))
+        assert np.array_equal(c.words, want), ring
+        bmm.multiply_cubic(a, b, bmm.Semiring(ring), out=c, accumulate=True)
+        twice = np.zeros_like(want) if ring == GF2 else want
+        assert np.array_equal(c.words, twice), ring
+
+
+def test_concurrent_calls_lease_distinct_streams(engine, oracle):
+    """Four host threads call the host API at once: each call leases its own streams
+    from the per-device pool (csrc/capi.cu StreamSet), results stay exact, and repeated
+    calls reuse the pooled streams."""
+    import threading
+    bmm = engine
+    m = k = n = 4096
+    ins = [(oracle.random(m, k, 601 + i), oracle.random(k, n, 701 + i)) for i in range(4)]
+    wants = [oracle.multiply_cubic(a, b, m, k, n, GF2) for a, b in ins]
+    outs = [None] * 4
+
+    def run(i):
+        a, b = ins[i]
+        for _ in range(3):
+            outs[i] = bmm.multiply_cubic(bmm.BitMatrix(m, k, a), bmm.BitMatrix(k, n, b), bmm.Semiring.Gf2XorAnd)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in th)
+    for i in range(4):
+        assert np.array_equal(outs[i].words, wants[i]), i
