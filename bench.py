@@ -208,6 +208,24 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference CPU arm
+def cpu_sample_shape(n: int) -> tuple[int, int]:
+    """C[0:rows, 0:cols] (full K = n) timed for the CPU reference: the whole product up
+    to n = 8192, else a slab sized for ~5 s per repetition on 16 host threads (the
+    reference cubic runs at ~2 Tbop/s there), ~10-30 s over the repetitions."""
+    if n <= 8192:
+        return n, n
+    return min(n, 1024), min(n, 32768)
+
+
+ALT_SAMPLE_N = 8192  # reference alt-si sub-instance (full product, 1 worker: ~2-3 s)
+
+
+def alt_auto_plan(n: int) -> tuple[int, int]:
+    """(d_serial, d_parallel) of the reference's auto_plan (engine.cpp:13-22)."""
+    k = n.bit_length() - 1 - 6
+    return k - min(3, k), min(3, k)
+
+
 def reference_sample(n: int, ring: int, rows: int, cols: int, hB: np.ndarray | None):
     """A bounded sample of the workload for the reference CPU implementation:
     C[0:rows, 0:cols] = A[0:rows, :] . B[:, 0:cols] with the full K = n, through
@@ -235,14 +253,14 @@ def run_reference(args, dist: Dist) -> None:
     n, ring, algo, desc = WORKLOADS[args.workload]
     if dist.rank != 0:
         return
-    rows, cols = (512, 8192) if n >= 16384 else (min(n, 1024), n)
+    rows, cols = cpu_sample_shape(n)
     if algo != 0:
-        # the reference alt-si path on a bounded sub-instance: n_s = 4096 full product, workers=1
+        # the reference alt-si path on a bounded sub-instance: an n_s = ALT_SAMPLE_N full product, workers=1
         # (more workers make the reference alt path slower)
         import paper_1909_01554_b200 as bmm
         from oracle import Reference
         ref = Reference()
-        ns = 4096
+        ns = ALT_SAMPLE_N
         a = np.zeros(ns * ns // 64, dtype=np.uint64)
         b = np.zeros_like(a)
         bmm.random_rows_into(a, ns, 1, 0, ns)
@@ -250,7 +268,7 @@ def run_reference(args, dist: Dist) -> None:
 
         def step() -> float:
             t0 = time.perf_counter()
-            ref.multiply(a, b, ns, 2, 0, 3, 3, 1, GF2)
+            ref.multiply(a, b, ns, 2, 0, *alt_auto_plan(ns), 1, GF2)
             return time.perf_counter() - t0
         bops, workers, sample = eff_bops(ns, ns, ns), 1, f"alt-si full product n={ns}, auto plan, 1 worker"
     else:
@@ -728,13 +746,13 @@ def run_ours(args, dist: Dist) -> None:
     if dist.world == 1 and not args.no_cpu_baseline:
         os.sched_setaffinity(0, range(os.cpu_count() or 1))  # every host core, not just the GPU's node
         if algo == 0:
-            rows, cols = (512, 8192) if n >= 16384 else (min(n, 1024), n)
+            rows, cols = cpu_sample_shape(n)
             stepf, sb, workers = reference_sample(n, ring, rows, cols, hB_np)
             sample = f"C[0:{rows}, 0:{cols}] of the n={n} product (full K={n}), reference multiply_cubic"
         else:
             from oracle import Reference
             ref = Reference()
-            ns = 4096
+            ns = ALT_SAMPLE_N
             a4 = np.zeros(ns * ns // 64, dtype=np.uint64)
             b4 = np.zeros_like(a4)
             bmm.random_rows_into(a4, ns, 1, 0, ns)
@@ -742,7 +760,7 @@ def run_ours(args, dist: Dist) -> None:
 
             def stepf() -> float:
                 s0 = time.perf_counter()
-                ref.multiply(a4, b4, ns, 2, 0, 3, 3, 1, GF2)
+                ref.multiply(a4, b4, ns, 2, 0, *alt_auto_plan(ns), 1, GF2)
                 return time.perf_counter() - s0
             sb, workers, sample = eff_bops(ns, ns, ns), 1, f"reference alt-si n={ns}, auto plan, 1 worker"
         ts = [stepf() for _ in range(args.cpu_reps)]
