@@ -266,6 +266,46 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tbase, uint32_t (&wor
     }
 }
 
+// Same drain with 32-column groups (two 16-column loads per buffer): the drain of a
+// short-K tile is bound by the TMEM load round trips (one in flight while the other
+// buffer is packed), so halving their number shortens it; 64 buffer registers.
+#ifndef BMMGPU_DRAIN_BATCH
+#define BMMGPU_DRAIN_BATCH 2  // 1: 16-column groups
+#endif
+__device__ __forceinline__ uint32_t (&half16(uint32_t (&v)[32], int h))[16] {
+    return *reinterpret_cast<uint32_t(*)[16]>(&v[16 * h]);
+}
+template <bool kGf2>
+__device__ __forceinline__ uint32_t pack_counts32(uint32_t (&v)[32]) {
+    return __byte_perm(pack_counts16<kGf2>(half16(v, 0)), pack_counts16<kGf2>(half16(v, 1)), 0x5410);
+}
+template <bool kGf2>
+__device__ __forceinline__ void drain_accumulator2(uint32_t tbase, uint32_t (&words)[P_EPI_COLS / 32],
+                                                   uint32_t acc_empty_leader, uint32_t lane) {
+    constexpr int kGroups = P_EPI_COLS / 32;
+    uint32_t va[32], vb[32];
+    umma::tmem_ld16(tbase, half16(va, 0));
+    umma::tmem_ld16(tbase + 16, half16(va, 1));
+    umma::tmem_ld_wait_regs(va);
+#pragma unroll
+    for (int g = 0; g < kGroups; g += 2) {
+        umma::tmem_ld16(tbase + 32 * (g + 1), half16(vb, 0));
+        umma::tmem_ld16(tbase + 32 * (g + 1) + 16, half16(vb, 1));
+        words[g] = pack_counts32<kGf2>(va);
+        umma::tmem_ld_wait_regs(vb);
+        if (g + 2 < kGroups) {
+            umma::tmem_ld16(tbase + 32 * (g + 2), half16(va, 0));
+            umma::tmem_ld16(tbase + 32 * (g + 2) + 16, half16(va, 1));
+        } else {
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
+        }
+        words[g + 1] = pack_counts32<kGf2>(vb);
+        if (g + 2 < kGroups) umma::tmem_ld_wait_regs(va);
+    }
+}
+
 // kTma: the packed superstages arrive by TMA (one 3-D tiled box per operand, 128-byte
 // swizzle, K tail zero-filled by the bounds check) instead of the cp.async loader warps.
 template <bool kTma>
@@ -598,9 +638,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                          3072 + 4 * local + 1);
                 const uint32_t tbase = tmem + ((quarter * 32) << 16) + half * P_EPI_COLS;
                 if (kGf2)
-                    drain_accumulator<true>(tbase, words, acc_empty_leader, lane);
+                    if (BMMGPU_DRAIN_BATCH == 2)
+                        drain_accumulator2<true>(tbase, words, acc_empty_leader, lane);
+                    else
+                        drain_accumulator<true>(tbase, words, acc_empty_leader, lane);
                 else
-                    drain_accumulator<false>(tbase, words, acc_empty_leader, lane);
+                    if (BMMGPU_DRAIN_BATCH == 2)
+                        drain_accumulator2<false>(tbase, words, acc_empty_leader, lane);
+                    else
+                        drain_accumulator<false>(tbase, words, acc_empty_leader, lane);
                 TRACE_AT(pair == 0 && rank == 0 && quarter == 0 && half == 0 && lane == 0 && local < 512,
                          3072 + 4 * local + 2);
             } else {
