@@ -306,6 +306,50 @@ __device__ __forceinline__ void drain_accumulator2(uint32_t tbase, uint32_t (&wo
     }
 }
 
+// GF(2) needs bit 0 of each count only, so the drain reads the accumulator with
+// .pack::16b (the low halves of two columns per register: half the TMEM bytes and
+// half the loads).  The expanders place Bt row 32 G + 16 h + i of a tile at
+// accumulator column 32 G + 2 i + h, so register i of a 32-column load holds output
+// columns i (bit 0) and 16 + i (bit 16) and one AND + shift-add per register builds the
+// word in output order.
+#ifndef BMMGPU_GF2_PACK16
+#define BMMGPU_GF2_PACK16 1
+#endif
+__device__ __forceinline__ uint32_t gf2_column_slot(uint32_t r) {
+    return BMMGPU_GF2_PACK16 ? (r & ~31u) | ((r & 15u) << 1) | ((r >> 4) & 1u) : r;
+}
+__device__ __forceinline__ uint32_t pack_pairs16(const uint32_t (&v)[16]) {
+    uint32_t a = 0, b = 0;  // two chains
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+        a += (v[i] & 0x00010001u) << i;
+        b += (v[i + 1] & 0x00010001u) << (i + 1);
+    }
+    return a | b;
+}
+__device__ __forceinline__ void drain_accumulator_gf2_pack16(uint32_t tbase, uint32_t (&words)[P_EPI_COLS / 32],
+                                                             uint32_t acc_empty_leader, uint32_t lane) {
+    constexpr int kGroups = P_EPI_COLS / 32;
+    uint32_t va[16], vb[16];
+    umma::tmem_ld16_pack16(tbase, va);
+    umma::tmem_ld_wait_regs16(va);
+#pragma unroll
+    for (int g = 0; g < kGroups; g += 2) {
+        umma::tmem_ld16_pack16(tbase + 32 * (g + 1), vb);
+        words[g] = pack_pairs16(va);
+        umma::tmem_ld_wait_regs16(vb);
+        if (g + 2 < kGroups) {
+            umma::tmem_ld16_pack16(tbase + 32 * (g + 2), va);
+        } else {
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
+        }
+        words[g + 1] = pack_pairs16(vb);
+        if (g + 2 < kGroups) umma::tmem_ld_wait_regs16(va);
+    }
+}
+
 // kTma: the packed superstages arrive by TMA (one 3-D tiled box per operand, 128-byte
 // swizzle, K tail zero-filled by the bounds check) instead of the cp.async loader warps.
 template <bool kTma>
@@ -384,6 +428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         // bits) a warp reads its rows' bits for its two stages, frees the packed slot, then
         // expands and stores each stage into the tensor-core ring.
         const uint32_t grp = warp >> 2, r = tid & (P_ROWS - 1), rsw = r & 7;
+        const uint32_t rb = kGf2 ? gf2_column_slot(r) : r;  // accumulator column of Bt row r
         const uint32_t full_leader0 = umma::mapa_shared(smem_u32(&full_bar[0]), 0);
         const uint8_t* pkrow = smem + size_t(P_STAGES) * P_STAGE + r * 128;
         uint64_t base = 0;  // global stage index of stage 0 of the current tile
@@ -423,8 +468,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                     if (!PROBE(64 | 128)) {
                         expand_store_sw128(sa, r, 0, v[i][0]);
                         expand_store_sw128(sa, r, 1, v[i][1]);
-                        expand_store_sw128(sa + P_REGION, r, 0, v[i][2]);
-                        expand_store_sw128(sa + P_REGION, r, 1, v[i][3]);
+                        expand_store_sw128(sa + P_REGION, rb, 0, v[i][2]);
+                        expand_store_sw128(sa + P_REGION, rb, 1, v[i][3]);
                     }
                     umma::fence_proxy_async_smem();
                     __syncwarp();
@@ -638,7 +683,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                          3072 + 4 * local + 1);
                 const uint32_t tbase = tmem + ((quarter * 32) << 16) + half * P_EPI_COLS;
                 if (kGf2)
-                    if (BMMGPU_DRAIN_BATCH == 2)
+                    if (BMMGPU_GF2_PACK16)
+                        drain_accumulator_gf2_pack16(tbase, words, acc_empty_leader, lane);
+                    else if (BMMGPU_DRAIN_BATCH == 2)
                         drain_accumulator2<true>(tbase, words, acc_empty_leader, lane);
                     else
                         drain_accumulator<true>(tbase, words, acc_empty_leader, lane);

@@ -1,6 +1,6 @@
 #!/bin/bash
-# A/B of the K2 epilogue drain: 32-column groups (new, BMMGPU_DRAIN_BATCH=2) against
-# 16-column groups (build/v/old.so) -- leaf-layer timing, configs[1] and configs[2].
+# A/B of a K2 epilogue drain variant (new build) against build/v/old.so --
+
 mkdir -p gpurun_out
 O=gpurun_out/drain_ab.txt
 : > $O
