@@ -50,11 +50,13 @@
 //     bias MMA and then 4 MMAs per stage, commits each stage to both CTAs' empty
 //     barriers and each tile to both CTAs' acc_full barriers.
 //   epilogue (warps 9-12): drain the CTA's 128 accumulator rows with double-buffered
-//     16-column TMEM loads, release the accumulator (acc_empty) as soon as the last
-//     load lands, pack the bits with funnel-shift chains, store.
-// Measured (ncu, microbench/trace_tiles.py): the tensor pipe is 98-99% active on long
-// K, held at ~1.8 GHz by the board power cap; on 4096-bit leaves each tile boundary
-// costs ~0.9 us (drain ~450 ns plus commit / restart latency) against a ~4.3 us tile.
+//     32-column TMEM loads (GF(2): .pack::16b, Bt rows permuted so a register carries
+//     two output columns), release the accumulator (acc_empty) as soon as the last
+//     load lands, pack the bits (funnel-shift chains / AND + shift-add), store.
+// Measured (ncu, microbench/trace_tiles.py, time_leaf.py): the tensor pipe is 98-99%
+// active on long K, held at ~1.8 GHz by the board power cap; on 4096-bit leaves each
+// tile boundary costs ~0.5 us (drain, bias MMA, commit / restart latency) against a
+// ~4.56 us tile.
 #include <cuda.h>
 
 #include "umma.cuh"
