@@ -317,8 +317,20 @@ __device__ __forceinline__ void drain_accumulator2(uint32_t tbase, uint32_t (&wo
 #ifndef BMMGPU_GF2_PACK16
 #define BMMGPU_GF2_PACK16 1
 #endif
-__device__ __forceinline__ uint32_t gf2_column_slot(uint32_t r) {
-    return BMMGPU_GF2_PACK16 ? (r & ~31u) | ((r & 15u) << 1) | ((r >> 4) & 1u) : r;
+// Output column o of a 32-column group sits at accumulator column 2o (o < 16) or
+// 2(o - 16) + 1.  Expander thread t of the group takes Bt row rho(t) so that both its
+// packed-ring reads (row rho & 7) and its operand stores (slot & 7) stay distinct across
+// each 8 lanes -- no shared-memory bank conflicts: lanes 8q .. 8q+3 take rows 4q .. 4q+3,
+// lanes 8q+4 .. 8q+7 rows 16 + 4(q ^ 1) .. +3.
+__device__ __forceinline__ uint32_t gf2_bt_row(uint32_t r) {
+    if (!BMMGPU_GF2_PACK16) return r;
+    const uint32_t t = r & 31u, q = t >> 3, j = t & 7u;
+    return (r & ~31u) | (j < 4 ? 4 * q + j : 16 + 4 * (q ^ 1u) + (j - 4));
+}
+__device__ __forceinline__ uint32_t gf2_column_slot(uint32_t o) {
+    if (!BMMGPU_GF2_PACK16) return o;
+    const uint32_t t = o & 31u;
+    return (o & ~31u) | (t < 16 ? 2 * t : 2 * (t - 16) + 1);
 }
 __device__ __forceinline__ uint32_t pack_pairs16(const uint32_t (&v)[16]) {
     uint32_t a = 0, b = 0;  // two chains
@@ -430,9 +442,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         // bits) a warp reads its rows' bits for its two stages, frees the packed slot, then
         // expands and stores each stage into the tensor-core ring.
         const uint32_t grp = warp >> 2, r = tid & (P_ROWS - 1), rsw = r & 7;
-        const uint32_t rb = kGf2 ? gf2_column_slot(r) : r;  // accumulator column of Bt row r
+        // Bt row this thread expands and the operand row (accumulator column) it goes to
+        const uint32_t rbt = kGf2 ? gf2_bt_row(r) : r, rb = kGf2 ? gf2_column_slot(rbt) : r;
+        const uint32_t rbsw = rbt & 7;
         const uint32_t full_leader0 = umma::mapa_shared(smem_u32(&full_bar[0]), 0);
         const uint8_t* pkrow = smem + size_t(P_STAGES) * P_STAGE + r * 128;
+        const uint8_t* pkrow_b = smem + size_t(P_STAGES) * P_STAGE + rbt * 128 + P_SST_OP;
         uint64_t base = 0;  // global stage index of stage 0 of the current tile
         int slot = 0;
         uint32_t pk_parity = 0;
@@ -445,14 +460,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             for (uint64_t k0 = 0; k0 < n_stages; k0 += 4) {
                 if (!PROBE(256)) PWAIT(1, umma::mbar_wait(&pk_full_bar[slot], pk_parity));
                 const uint8_t* q = pkrow + slot * P_SST;
+                const uint8_t* qb = pkrow_b + slot * P_SST;
                 uint4 v[2][4];  // [stage][A lo, A hi, Bt lo, Bt hi]
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
                     const uint32_t c = 2 * (sub0 + 2 * i);  // 16-byte chunk of the stage's low half
                     v[i][0] = *reinterpret_cast<const uint4*>(q + ((c ^ rsw) << 4));
                     v[i][1] = *reinterpret_cast<const uint4*>(q + (((c + 1) ^ rsw) << 4));
-                    v[i][2] = *reinterpret_cast<const uint4*>(q + P_SST_OP + ((c ^ rsw) << 4));
-                    v[i][3] = *reinterpret_cast<const uint4*>(q + P_SST_OP + (((c + 1) ^ rsw) << 4));
+                    v[i][2] = *reinterpret_cast<const uint4*>(qb + ((c ^ rbsw) << 4));
+                    v[i][3] = *reinterpret_cast<const uint4*>(qb + (((c + 1) ^ rbsw) << 4));
                 }
                 __syncwarp();
                 if (lane == 0 && !PROBE(256)) umma::mbar_arrive(&pk_empty_bar[slot]);

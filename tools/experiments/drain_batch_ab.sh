@@ -11,7 +11,7 @@ for rep in 1 2; do
     if [ $v = old ]; then cp build/v/old.so paper_1909_01554_b200/libbmmgpu.so; else cp /tmp/new.so paper_1909_01554_b200/libbmmgpu.so; fi
     echo "== $v leaf" >> $O; timeout 300 python microbench/time_leaf.py 4096,2048 >> $O 2>&1
     echo "== $v c2" >> $O; timeout 300 python bench.py --workload c2-gf2-altsi-65536 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 >> $O
-    echo "== $v c3" >> $O; timeout 300 python bench.py --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 >> $O
+    echo "== $v c3gf2" >> $O; timeout 300 python bench.py --workload c3-gf2-cubic-131072 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 >> $O
   done
 done
 cp /tmp/new.so paper_1909_01554_b200/libbmmgpu.so
