@@ -2,6 +2,8 @@
 # Refresh the GF(2) evidence after a K2 drain change: bench lines (configs[1], [3], scaled
 # [4] with the independent spot check), the c2 launch list and one --set full leaf capture.
 mkdir -p gpurun_out/ref2
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ref2/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/ref2/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ref2/smoke.log 2>&1
 O=gpurun_out/ref2
 timeout 600 python bench.py --workload c2-gf2-altsi-65536 > $O/bench_c2_altsi.log 2>&1
 timeout 600 python bench.py --workload c3-gf2-cubic-131072 --no-cpu-baseline > $O/bench_c3_gf2.log 2>&1
