@@ -50,8 +50,8 @@
 //     bias MMA and then 4 MMAs per stage, commits each stage to both CTAs' empty
 //     barriers and each tile to both CTAs' acc_full barriers.
 //   epilogue (warps 9-12): drain the CTA's 128 accumulator rows with double-buffered
-//     32-column TMEM loads (GF(2): .pack::16b, Bt rows permuted so a register carries
-//     two output columns), release the accumulator (acc_empty) as soon as the last
+//     32-column TMEM loads (optional GF(2) variant: .pack::16b, Bt rows permuted so a
+//     register carries two output columns), release the accumulator (acc_empty) as soon as the last
 //     load lands, pack the bits (funnel-shift chains / AND + shift-add), store.
 // Measured (ncu, microbench/trace_tiles.py, time_leaf.py): the tensor pipe is 98-99%
 // active on long K, held at ~1.8 GHz by the board power cap; on 4096-bit leaves each
@@ -315,7 +315,7 @@ __device__ __forceinline__ void drain_accumulator2(uint32_t tbase, uint32_t (&wo
 // columns i (bit 0) and 16 + i (bit 16) and one AND + shift-add per register builds the
 // word in output order.
 #ifndef BMMGPU_GF2_PACK16
-#define BMMGPU_GF2_PACK16 1
+#define BMMGPU_GF2_PACK16 0  // 1: fails the two-process tile test intermittently (under investigation)
 #endif
 // Output column o of a 32-column group sits at accumulator column 2o (o < 16) or
 // 2(o - 16) + 1.  Expander thread t of the group takes Bt row rho(t) so that both its
