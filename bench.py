@@ -698,7 +698,8 @@ def run_ours(args, dist: Dist) -> None:
         e2e_t = statistics.median(te)
         e2e = {"value": total_bops / e2e_t / 1e15, "unit": UNIT, "ms_per_step": e2e_t * 1e3,
                "h2d_bytes_per_step": int(2 * n * w * 8), "d2h_bytes_per_step": int(n * w * 8),
-               "path": "bmmgpu_multiply (include/bmmgpu.h) from pinned host buffers"}
+               "path": "bmmgpu_multiply (include/bmmgpu.h) from pinned host buffers",
+               "samples_ms": [round(x * 1e3, 2) for x in te]}
 
     # ---- roofline of the dominant kernel
     peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())
