@@ -315,7 +315,7 @@ __device__ __forceinline__ void drain_accumulator2(uint32_t tbase, uint32_t (&wo
 // columns i (bit 0) and 16 + i (bit 16) and one AND + shift-add per register builds the
 // word in output order.
 #ifndef BMMGPU_GF2_PACK16
-#define BMMGPU_GF2_PACK16 0  // 1: fails the two-process tile test intermittently (under investigation)
+#define BMMGPU_GF2_PACK16 2  // 0 off; 1 Bt-permuted (fails the two-process tile test intermittently); 2 drain-only
 #endif
 // Output column o of a 32-column group sits at accumulator column 2o (o < 16) or
 // 2(o - 16) + 1.  Expander thread t of the group takes Bt row rho(t) so that both its
@@ -323,12 +323,12 @@ __device__ __forceinline__ void drain_accumulator2(uint32_t tbase, uint32_t (&wo
 // each 8 lanes -- no shared-memory bank conflicts: lanes 8q .. 8q+3 take rows 4q .. 4q+3,
 // lanes 8q+4 .. 8q+7 rows 16 + 4(q ^ 1) .. +3.
 __device__ __forceinline__ uint32_t gf2_bt_row(uint32_t r) {
-    if (!BMMGPU_GF2_PACK16) return r;
+    if (BMMGPU_GF2_PACK16 != 1) return r;
     const uint32_t t = r & 31u, q = t >> 3, j = t & 7u;
     return (r & ~31u) | (j < 4 ? 4 * q + j : 16 + 4 * (q ^ 1u) + (j - 4));
 }
 __device__ __forceinline__ uint32_t gf2_column_slot(uint32_t o) {
-    if (!BMMGPU_GF2_PACK16) return o;
+    if (BMMGPU_GF2_PACK16 != 1) return o;
     const uint32_t t = o & 31u;
     return (o & ~31u) | (t < 16 ? 2 * t : 2 * (t - 16) + 1);
 }
@@ -339,7 +339,17 @@ __device__ __forceinline__ uint32_t pack_pairs16(const uint32_t (&v)[16]) {
         a += (v[i] & 0x00010001u) << i;
         b += (v[i + 1] & 0x00010001u) << (i + 1);
     }
-    return a | b;
+    uint32_t x = a | b;
+    if (BMMGPU_GF2_PACK16 == 2) {
+        // natural column order (no Bt permutation): bit i = column 2i, bit 16 + i =
+        // column 2i + 1 -> interleave the halves (outer perfect shuffle)
+        uint32_t t;
+        t = (x ^ (x >> 8)) & 0x0000FF00u; x ^= t ^ (t << 8);
+        t = (x ^ (x >> 4)) & 0x00F000F0u; x ^= t ^ (t << 4);
+        t = (x ^ (x >> 2)) & 0x0C0C0C0Cu; x ^= t ^ (t << 2);
+        t = (x ^ (x >> 1)) & 0x22222222u; x ^= t ^ (t << 1);
+    }
+    return x;
 }
 __device__ __forceinline__ void drain_accumulator_gf2_pack16(uint32_t tbase, uint32_t (&words)[P_EPI_COLS / 32],
                                                              uint32_t acc_empty_leader, uint32_t lane) {
