@@ -64,11 +64,19 @@ DEFAULT_WORKLOAD = "c3-bool-cubic-131072"
 # Paper V100 numbers for the same metric/config at 1 GPU, Pbop/s.
 PUBLISHED_1GPU = {"c3-bool-cubic-131072": 0.15127, "c3-gf2-cubic-131072": 0.17014, "c1-gf2-cubic-8192": 0.13283,
                   "c1-bool-cubic-8192": 0.14000, "c2-gf2-altsi-65536": 0.30177}
-KERNEL_IDS = {"auto": 0, "lop3": 1, "umma": 2, "umma1": 3, "umma2np": 4}
+KERNEL_IDS = {"auto": 0, "lop3": 1, "umma": 2}
 
 
 def eff_bops(m: int, k: int, n: int) -> float:
     return 2.0 * m * k * n - float(m) * n
+
+
+def n3_rate(value: float, n: int) -> dict:
+    """BASELINE.json names the metric "n^3 bops/s"; the headline `value` follows the reference's
+    numerator 2n^3 - n^2 (bmm_cli.cpp:134-141).  Both are reported: this is
+    the same measurement with n^3 as the numerator."""
+    return {"value": value * float(n) ** 3 / eff_bops(n, n, n), "unit": UNIT,
+            "note": "n^3 / T (about half the headline (2n^3 - n^2) / T)"}
 
 
 # ------------------------------------------------------------------ distributed plumbing
@@ -208,6 +216,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference CPU arm
+def cpu_model() -> str | None:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_sample_shape(n: int) -> tuple[int, int]:
     """C[0:rows, 0:cols] (full K = n) timed for the CPU reference: the whole product up
     to n = 8192, else a slab sized for ~5 s per repetition on 16 host threads (the
@@ -230,14 +248,13 @@ def reference_sample(n: int, ring: int, rows: int, cols: int, hB: np.ndarray | N
     """A bounded sample of the workload for the reference CPU implementation:
     C[0:rows, 0:cols] = A[0:rows, :] . B[:, 0:cols] with the full K = n, through
     the unmodified reference multiply_cubic (oracle/_ref) on all host cores."""
-    import paper_1909_01554_b200 as bmm
     from oracle import Reference
     ref = Reference()
-    a = np.zeros(rows * (n // 64), dtype=np.uint64)
-    bmm.random_rows_into(a, n, 1, 0, rows)
+    # rows [0, rows) of BitMatrix::random(n, n, 1) are random(rows, n, 1): one mt19937_64 draw
+    # per word in row-major order (reference bitmatrix.cpp:64-77)
+    a = ref.random(rows, n, 1)
     if hB is None:
-        hB = np.zeros(n * (n // 64), dtype=np.uint64)
-        bmm.random_rows_into(hB, n, 2, 0, n)
+        hB = ref.random(n, n, 2)
     b = np.ascontiguousarray(hB.reshape(n, n // 64)[:, : cols // 64]).ravel()
     workers = os.cpu_count() or 1
 
@@ -257,14 +274,11 @@ def run_reference(args, dist: Dist) -> None:
     if algo != 0:
         # the reference alt-si path on a bounded sub-instance: an n_s = ALT_SAMPLE_N full product, workers=1
         # (more workers make the reference alt path slower)
-        import paper_1909_01554_b200 as bmm
         from oracle import Reference
         ref = Reference()
         ns = ALT_SAMPLE_N
-        a = np.zeros(ns * ns // 64, dtype=np.uint64)
-        b = np.zeros_like(a)
-        bmm.random_rows_into(a, ns, 1, 0, ns)
-        bmm.random_rows_into(b, ns, 2, 0, ns)
+        a = ref.random(ns, ns, 1)
+        b = ref.random(ns, ns, 2)
 
         def step() -> float:
             t0 = time.perf_counter()
@@ -281,11 +295,14 @@ def run_reference(args, dist: Dist) -> None:
     value = bops / t / 1e15
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic (BitMatrix::random seeds 1, 2)",
+            "vs_baseline": None, "dtype": "u64", "n3_rate": n3_rate(value, n), "data": "synthetic (BitMatrix::random seeds 1, 2)",
             "config": {"workload": args.workload, "desc": desc, "n": n, "ring": "gf2" if ring else "boolean",
                        "sample": sample},
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference", "sample": sample,
+                             "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
+                             "code": "unmodified reference bmm_core (oracle/_ref/libbmmref.so, built from "
+                                     "/root/reference/proj/src); inputs from its own BitMatrix::random"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -332,6 +349,134 @@ def spot_check(hA: np.ndarray, hB: np.ndarray, hC: np.ndarray, n: int, ring: int
         if not np.array_equal(want, got[r0:r0 + 8192]):
             return False
     return True
+
+
+# ------------------------------------------------------------------ parity at the benchmarked size
+# Independent checks of the timed product's output, run after the timed region.  They use
+# stock PyTorch ops (gather / XOR) and numpy only -- never the library's kernels.
+FREIVALDS_SEED = 12345
+
+
+def gf2_matvec64(M, cols: int, X, row_block: int = 1024):
+    """Y = M . X over GF(2) for a packed bit matrix M (rows x ceil(cols/64) words, torch
+    int64, host or device; only the first `cols` bits of a row are used) and X = 64 packed
+    bit-columns (`cols` words on the device).  Four Russians with byte tables: table c holds
+    the XOR of the X rows selected by each 8-bit value of byte c, so row i of Y is the XOR
+    over c of table_c[byte c of row i].  Stock torch ops (gather, bitwise XOR); host row
+    blocks are streamed to the device."""
+    import torch
+    dev = X.device
+    nbytes = -(-cols // 8)
+    xpad = torch.zeros(nbytes * 8, dtype=torch.int64, device=dev)
+    xpad[:cols] = X[:cols]
+    xb = xpad.view(nbytes, 8)
+    v = torch.arange(256, device=dev)
+    T = torch.zeros((nbytes, 256), dtype=torch.int64, device=dev)
+    for b in range(8):
+        sel = ((v >> b) & 1).bool()
+        T ^= torch.where(sel[None, :], xb[:, b:b + 1], torch.zeros((), dtype=torch.int64, device=dev))
+    Tf = T.view(-1)
+    p2 = 1 << (nbytes - 1).bit_length()
+    offs = (torch.arange(nbytes, device=dev) * 256)[None, :]
+    rows = M.shape[0]
+    out = torch.empty(rows, dtype=torch.int64, device=dev)
+    for r0 in range(0, rows, row_block):
+        blk = M[r0:r0 + row_block].to(dev, non_blocking=False).contiguous()
+        by = blk.view(torch.uint8)[:, :nbytes].long()
+        if cols % 8:
+            by[:, -1] &= (1 << (cols % 8)) - 1
+        g = Tf[by + offs]
+        if p2 != nbytes:
+            g = torch.nn.functional.pad(g, (0, p2 - nbytes))
+        h = p2
+        while h > 1:
+            h //= 2
+            g = g[:, :h] ^ g[:, h:2 * h]
+        out[r0:r0 + blk.shape[0]] = g[:, 0]
+    return out
+
+
+def freivalds_gf2(A, B, C, m: int, k: int, n: int, reps: int = 1) -> bool:
+    """C == A . B over GF(2) with probability of a false pass <= 2^-64 per rep:
+    C X == A (B X) for 64 random bit-columns X.  A: m x >=k bits,
+    B: k x >= n bits, C: m x >= n bits (torch int64 word matrices, host or device)."""
+    import torch
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    g = torch.Generator(device=dev).manual_seed(FREIVALDS_SEED)
+    for _ in range(reps):
+        X = torch.randint(-2**63, 2**63 - 1, (n,), dtype=torch.int64, device=dev, generator=g)
+        lhs = gf2_matvec64(C[:m], n, X)
+        rhs = gf2_matvec64(A[:m], k, gf2_matvec64(B[:k], n, X))
+        if not torch.equal(lhs, rhs):
+            return False
+    return True
+
+
+def sparse_boolean_inputs(m: int, n: int, r0: int, k_and: int = 9):
+    """Seeded sparse operands for a non-vacuous Boolean check at size: each bit is the AND of
+    k_and uniform bits (density 2^-k_and; at n = 131072 and k_and = 9 about 39 % of C is
+    one).  Returns device tensors A (rows r0 .. r0+m of an n x n matrix) and B (n x n)."""
+    import torch
+    w = n // 64
+    gen = torch.Generator(device="cuda").manual_seed(2024)
+
+    def rnd():
+        out = torch.full((n, w), -1, dtype=torch.int64, device="cuda")
+        for _ in range(k_and):
+            out &= torch.randint(-2**63, 2**63 - 1, (n, w), dtype=torch.int64, device="cuda", generator=gen)
+        return out
+    B = rnd()
+    A = rnd()[r0:r0 + m].contiguous()
+    return A, B
+
+
+def parity_in_core(args, dist, n: int, m: int, r0: int, ring: int, algo: int, kernel: int, dA, dB, dBt, dC,
+                   hA_np: np.ndarray, hB_np: np.ndarray, hC_e2e, run_step) -> dict:
+    """Parity of the benchmarked product at its full size (after the timed region).
+    GF(2): Freivalds with 64 random bit-columns on the timed output + full rows and a full
+    column recomputed in numpy.  Boolean: the dense product must be all ones (every bit),
+    then a sparse seeded product (AND-of-9 inputs, ~39 % ones in C at n = 131072) goes
+    through the same device path (transpose + the same kernel, same shape, so the same
+    long-K wave-aligned mode) and full rows / columns are recomputed in numpy.  The e2e
+    leg's host output must equal the device-resident result bit for bit."""
+    import torch
+    t0 = time.perf_counter()
+    w = n // 64
+    res: dict = {}
+    C = dC[:m, :w]
+    if hC_e2e is not None:
+        res["e2e_output_equals_device_output"] = bool(np.array_equal(
+            hC_e2e[: m * w], C.contiguous().cpu().numpy().view(np.uint64).ravel()))
+    rows = sorted({0, m // 3, m // 2 + 1, m - 1})
+    if ring == GF2:
+        res["freivalds_64_columns"] = freivalds_gf2(dA[:m, :w], dB.view(n, w), C, m, n, n)
+        hC = C.contiguous().cpu().numpy().view(np.uint64).ravel()
+        res["numpy_rows_and_column"] = spot_check(hA_np, hB_np, hC, n, GF2, rows[:2], (7 * n) // 11, m)
+        res["method"] = "GF(2): Freivalds C.X == A.(B.X), 64 random bit-columns (torch gather/XOR, error <= 2^-64); " \
+                        f"rows {rows[:2]} and column {(7 * n) // 11} recomputed in numpy"
+    else:
+        res["dense_all_ones"] = bool(int((C != -1).sum().item()) == 0)
+        sA, sB = sparse_boolean_inputs(m, n, r0)
+        dA[:m, :w].copy_(sA)
+        dB.view(n, w).copy_(sB)
+        del sA, sB
+        run_step()
+        torch.cuda.synchronize()
+        hAs = dA[:m, :w].contiguous().cpu().numpy().view(np.uint64).ravel()
+        hBs = dB.view(n, w).cpu().numpy().view(np.uint64).ravel()
+        Cs = dC[:m, :w].contiguous().cpu().numpy().view(np.uint64).ravel()
+        dens = float(np.unpackbits(Cs[: min(Cs.size, 1 << 22)].view(np.uint8)).mean())
+        srows = sorted({int(x) for x in np.linspace(0, m - 1, 24)})
+        res["sparse_rows_and_columns"] = bool(all(spot_check(hAs, hBs, Cs, n, BOOL, srows if i == 0 else [], j, m)
+                                                  for i, j in enumerate([n // 5, (7 * n) // 11])))
+        res["sparse_density_of_C"] = round(dens, 4)
+        res["method"] = ("Boolean: dense product all ones (every word checked on device); sparse AND-of-9 seeded "
+                         f"inputs through the same transpose + kernel at the same shape, {len(srows)} full rows and "
+                         "2 full columns recomputed in numpy")
+    ok = all(v for v in res.values() if isinstance(v, bool))
+    res["ok"] = bool(dist.max(0.0 if ok else 1.0) == 0.0)
+    res["seconds"] = round(time.perf_counter() - t0, 2)
+    return res
 
 
 class SharedHostWords:
@@ -426,15 +571,29 @@ def run_ooc(args, dist: Dist) -> None:
     total_bops = eff_bops(n, n, n)
     value = total_bops / t / 1e15
     ok = None
-    if args.check and dist.rank == 0:
+    parity = None
+    if args.check:
+        # every rank checks its own slab: rows and a column in numpy; GF(2) also Freivalds with
+        # 64 random bit-columns, the operands streamed from host memory in row blocks
+        pt0 = time.perf_counter()
         ok = spot_check(hA_np, hB_np, hC_np, n, ring, [0, m // 2 + 1, m - 1], n // 3, m)
+        parity = {"numpy_rows_and_column": bool(ok)}
+        if ring == GF2:
+            parity["freivalds_64_columns"] = freivalds_gf2(hA.view(-1, w), hB.view(n, w), hC.view(-1, w), m, n, n)
+        good = all(v for v in parity.values() if isinstance(v, bool))
+        parity["method"] = ("rows 0, m/2+1, m-1 and column n/3 of this rank's slab recomputed in numpy" +
+                            ("; Freivalds C.X == A.(B.X) with 64 random bit-columns (torch gather/XOR)"
+                             if ring == GF2 else ""))
+        parity["ok"] = bool(dist.max(0.0 if good else 1.0) == 0.0)
+        parity["seconds"] = round(time.perf_counter() - pt0, 2)
+        ok = parity["ok"]
     peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())
     kms = blk_ms.value / args.steps
     achieved = eff_bops(m, n, n) / (kms * 1e-3)
     if dist.rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "e2m1",
+                "vs_baseline": None, "n3_rate": n3_rate(value, n), "dtype": "e2m1",
                 "data": "synthetic (BitMatrix::random seeds 1, 2, mt19937_64), pinned host memory",
                 "config": {"workload": args.workload, "desc": desc, "n": n, "ring": "gf2" if ring else "boolean",
                            "algo": "cubic", "rows_per_rank": m, "device_budget_bytes": budget,
@@ -454,7 +613,7 @@ def run_ooc(args, dist: Dist) -> None:
                         "h2d_note": "counted by the library (bmmgpu_last_copy_bytes): A once, B once per "
                                     "resident row panel of the plan",
                         "path": "bmmgpu_cubic (include/bmmgpu.h) from pinned host buffers, per rank"},
-                "spot_check": ok, "clocks": clocks, "gpu_launches": int(launches * args.steps)}
+                "spot_check": ok, "parity": parity, "clocks": clocks, "gpu_launches": int(launches * args.steps)}
         print(json.dumps(line), flush=True)
     if shared_b is not None:
         shared_b.close()
@@ -541,6 +700,9 @@ def run_alt_tiles(args, dist: Dist) -> None:
             torch.cuda.synchronize()
             if not torch.equal(ref, dC[slot]):
                 raise RuntimeError(f"tile {t} differs from the cubic product")
+            # and independently of the library: Freivalds on the tile, C_IJ = A[I, :] . B[:, J]
+            if not freivalds_gf2(dA[I * T:(I + 1) * T], dB[:, J * tw:(J + 1) * tw], dC[slot], T, n, T):
+                raise RuntimeError(f"tile {t} fails the Freivalds check")
             checked += 1
     depth = (T // 64).bit_length() - 1
     e_levels = max(0, min(depth, depth + 6 - (args.leaf_log2 or 12)))
@@ -553,7 +715,7 @@ def run_alt_tiles(args, dist: Dist) -> None:
     if dist.rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "e2m1", "data": "synthetic (BitMatrix::random seeds 1, 2, mt19937_64)",
+                "vs_baseline": None, "n3_rate": n3_rate(value, n), "dtype": "e2m1", "data": "synthetic (BitMatrix::random seeds 1, 2, mt19937_64)",
                 "config": {"workload": args.workload, "desc": desc, "n": n, "ring": "gf2",
                            "algo": ["cubic", "sw", "alt-si", "alt-chain"][algo],
                            "parallelism": f"4x4 output tiles of n/4 round robin over {dist.world} ranks, "
@@ -563,7 +725,12 @@ def run_alt_tiles(args, dist: Dist) -> None:
                              "unit": "Tbop/s", "frac": achieved / peaks["umma_mxf4_bops"], "traffic": None,
                              "kernel": f"cubic_umma2_kernel (leaf layer: 7^{e_levels} products of {leaf}^3 per block)",
                              "kernel_ms": kms, "kernel_share_of_step": kms / ms},
-                "cpu_baseline": None, "e2e": None, "tiles_checked_rank0": checked, "clocks": clocks,
+                "cpu_baseline": None, "e2e": None, "tiles_checked_rank0": checked,
+                "parity": None if checked is None else {
+                    "ok": True, "tiles_checked_rank0": checked,
+                    "method": "every tile of rank 0 equal to the tensor-core cubic product of A[I,:].B[:,J] and "
+                              "passing Freivalds (64 random bit-columns, torch gather/XOR)"},
+                "clocks": clocks,
                 "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
 
@@ -701,12 +868,18 @@ def run_ours(args, dist: Dist) -> None:
                "path": "bmmgpu_multiply (include/bmmgpu.h) from pinned host buffers",
                "samples_ms": [round(x * 1e3, 2) for x in te]}
 
+    # ---- parity of the benchmarked output at full size (after the timed regions)
+    parity = None
+    if args.check:
+        hC_e2e = hC.numpy().view(np.uint64) if e2e is not None else None
+        parity = parity_in_core(args, dist, n, m, r0, ring, algo, kernel, dA, dB, dBt, dC, hA_np, hB_np, hC_e2e,
+                                lambda: step(0))
+
     # ---- roofline of the dominant kernel
     peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())
     resolved = kernel if kernel else 2  # AUTO = the tcgen05 CTA-pair kernel (csrc/capi.cu resolve_kernel)
     peak = peaks["lop3_bops"] if resolved == 1 else peaks["umma_mxf4_bops"]
-    kname = {1: "cubic_lop3_kernel", 2: "cubic_umma2_kernel", 3: "cubic_umma_kernel",
-             4: "cubic_umma2np_kernel"}[resolved]
+    kname = {1: "cubic_lop3_kernel", 2: "cubic_umma2_kernel"}[resolved]
     if algo == 0:
         # algorithmic work of the one product launch: the slab's 2 m n k - m n
         launch_bops = eff_bops(m, n, n)
@@ -766,13 +939,13 @@ def run_ours(args, dist: Dist) -> None:
             sb, workers, sample = eff_bops(ns, ns, ns), 1, f"reference alt-si n={ns}, auto plan, 1 worker"
         ts = [stepf() for _ in range(args.cpu_reps)]
         cpu = {"value": sb / statistics.median(ts) / 1e15, "unit": UNIT, "cores": workers, "kind": "reference",
-               "sample": sample, "seconds": sum(ts)}
+               "sample": sample, "seconds": sum(ts), "cpu_model": cpu_model()}
 
     if dist.rank == 0:
         published = PUBLISHED_1GPU.get(args.workload) if dist.world == 1 else None
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": (value / published) if published else None,
+                "vs_baseline": (value / published) if published else None, "n3_rate": n3_rate(value, n),
                 "dtype": "u32" if resolved == 1 else "e2m1",
                 "data": "synthetic (BitMatrix::random seeds 1, 2, mt19937_64)",
                 "config": {"workload": args.workload, "desc": desc, "n": n, "ring": "gf2" if ring else "boolean",
@@ -780,7 +953,7 @@ def run_ours(args, dist: Dist) -> None:
                            "rows_per_rank": m, "l2": "inputs (n^2/8 B per operand) far exceed the 126 MB L2",
                            "host_cpus_bound": len(args.cpus) if args.cpus else None,
                            "parallelism": f"output row slabs x{dist.world}, no exchange"},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity, "clocks": clocks,
                 "gpu_launches": int(launches_per_step * args.steps)}
         print(json.dumps(line), flush=True)
 
@@ -803,9 +976,10 @@ def main() -> None:
                          "2 K-outer pipeline (C resident, A/B K-chunks uploaded behind the product)")
     ap.add_argument("--device-budget", dest="device_budget", type=int, default=0,
                     help="HBM bytes the e2e call may use (0 = free memory; the c5 workloads default to 40 GiB)")
-    ap.add_argument("--check", action="store_true",
-                    help="c5 workloads: verify rows and a column of C on the CPU (numpy); multi-rank alt: "
-                         "verify every tile against the tensor-core cubic product")
+    ap.add_argument("--check", action=argparse.BooleanOptionalAction, default=True,
+                    help="verify the benchmarked output at full size after the timed region (default on): GF(2) "
+                         "Freivalds + numpy rows/columns, Boolean all-ones + a sparse product's rows/columns in "
+                         "numpy, out-of-core rows/columns in numpy, multi-rank alt tiles against the cubic product")
     args = ap.parse_args()
     dist = Dist()
     try:

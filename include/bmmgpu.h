@@ -43,9 +43,10 @@ extern "C" {
 /* block-product kernel selection */
 #define BMMGPU_KERNEL_AUTO 0
 #define BMMGPU_KERNEL_LOP3 1      /* LOP3 AND/XOR|OR word kernel (integer ALU)      */
-#define BMMGPU_KERNEL_UMMA_F4 2   /* tcgen05 kind::mxf4 0/1 e2m1, f32 accumulate, CTA pair */
-#define BMMGPU_KERNEL_UMMA_F4_1SM 3 /* the same on single CTAs (cta_group::1)          */
-#define BMMGPU_KERNEL_UMMA_F4_PAIR_NP 4 /* CTA pair, one launch CTA per tile (no persistent loop) */
+#define BMMGPU_KERNEL_UMMA_F4 2   /* tcgen05 kind::mxf4 0/1 e2m1, f32 accumulate, persistent CTA pairs */
+/* (ids 3 and 4 were the superseded single-CTA and non-persistent CTA-pair forms of the
+   tensor-core kernel; their sources are kept under microbench/history/ and the ids are
+   rejected with BMMGPU_EINVAL) */
 
 typedef struct bmmgpu_opts {
     uint32_t device_mask; /* bit g = use CUDA device g; 0 = device 0            */
@@ -169,7 +170,9 @@ int bmmgpu_slab_rows(uint64_t m, uint32_t parts, uint32_t index, uint64_t gran, 
 int bmmgpu_block_timer(int32_t enable);
 int bmmgpu_block_timer_read(double* ms, uint64_t* launches);
 
-/* Number of kernel launches the last host-API call made on its devices. */
+/* Number of kernel launches the calling thread's last host-API call made on its
+ * devices (plus device-API launches made on this thread since).  Per thread: concurrent
+ * calls on other threads do not disturb it. */
 uint64_t bmmgpu_last_launch_count(void);
 
 /* Page-locked host memory (cudaHostAlloc, portable across devices) for buffers
@@ -178,8 +181,8 @@ uint64_t bmmgpu_last_launch_count(void);
 int bmmgpu_host_alloc(uint64_t bytes, void** ptr);
 int bmmgpu_host_free(void* ptr);
 
-/* Host->device and device->host bytes the last host-API call copied (operands,
- * re-streamed panels, results). */
+/* Host->device and device->host bytes the calling thread's last host-API call copied
+ * (operands, re-streamed panels, results).  Per thread, like the launch count. */
 int bmmgpu_last_copy_bytes(uint64_t* h2d, uint64_t* d2h);
 
 int bmmgpu_device_count(void);

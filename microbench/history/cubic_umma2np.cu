@@ -1,3 +1,5 @@
+// HISTORY ONLY -- superseded by csrc/cubic_umma2.cu (persistent CTA pairs); not built or linked.
+// Kept for the round-1 A/B measurements in profiles/r01/history/.
 // cubic_umma2np.cu -- K2, CTA-pair form without the persistent tile loop
 // (kernel id BMMGPU_KERNEL_UMMA_F4_PAIR_NP), kept for A/B measurement against
 // the persistent default in cubic_umma2.cu.  The cubic bit-matrix product

@@ -1,3 +1,5 @@
+// HISTORY ONLY -- superseded by csrc/cubic_umma2.cu (persistent CTA pairs); not built or linked.
+// Kept for the round-1 A/B measurements in profiles/r01/history/.
 // cubic_umma.cu -- K2 (single-CTA form, kernel id BMMGPU_KERNEL_UMMA_F4_1SM): the
 // cubic bit-matrix product on the 5th-generation tensor cores (tcgen05.mma
 // kind::mxf4, f32 accumulators in TMEM).  The CTA-pair form in

@@ -55,8 +55,6 @@ class Kernel(enum.IntEnum):
     AUTO = 0
     LOP3 = 1
     UMMA_F4 = 2
-    UMMA_F4_1SM = 3
-    UMMA_F4_PAIR_NP = 4
 
 
 class _Opts(ctypes.Structure):

@@ -1304,6 +1304,10 @@ int interleaved_basis_change(uint64_t* words, uint64_t total_words, int levels, 
         BMMGPU_CUDA_TRY(cudaStreamSynchronize(nullptr));
         return kOk;
     }
+    if (total_words % (uint64_t(1) << (2 * levels))) {
+        set_error("basis change: the vector has fewer than 4^levels words");
+        return kEinval;
+    }
     // device block: a power of two of words within the budget
     uint64_t bw = 1;
     while (bw * 2 * 8 <= budget && bw * 2 <= total_words) bw *= 2;
@@ -1333,15 +1337,20 @@ int interleaved_basis_change(uint64_t* words, uint64_t total_words, int levels, 
     // the remaining levels together, block by block: within a block of bw words the
     // level-l groups are [bw / (4 inner_l)][4][inner_l], i.e. levels l0.. of a vector
     // of bw words whose outermost mode starts at l0
+    // Blocks are whole level-l0 groups (4 inner_l0 words; every deeper level's group divides
+    // it), so vectors whose inner mode is not a power of two ([4]*levels [7 * 64], say) split
+    // cleanly and the last block may be shorter.
     if (l0 < levels) {
-        for (uint64_t b0 = 0; b0 < total_words; b0 += bw) {
-            BMMGPU_CUDA_TRY(memcpy_counted(d.p, words + b0, bw * 8, cudaMemcpyHostToDevice, nullptr));
+        const uint64_t g0 = 4 * inner_of(l0), blk = (bw / g0) * g0;
+        for (uint64_t b0 = 0; b0 < total_words; b0 += blk) {
+            const uint64_t len = std::min(blk, total_words - b0);
+            BMMGPU_CUDA_TRY(memcpy_counted(d.p, words + b0, len * 8, cudaMemcpyHostToDevice, nullptr));
             for (int l = l0; l < levels; ++l) {
-                const uint64_t inner = inner_of(l), outer_b = bw / (4 * inner);
+                const uint64_t inner = inner_of(l), outer_b = len / (4 * inner);
                 if ((rc = interleaved_basis_change_level_dev(d.u(), outer_b, inner, algo, factor, inverse, nullptr)))
                     return rc;
             }
-            BMMGPU_CUDA_TRY(memcpy_counted(words + b0, d.p, bw * 8, cudaMemcpyDeviceToHost, nullptr));
+            BMMGPU_CUDA_TRY(memcpy_counted(words + b0, d.p, len * 8, cudaMemcpyDeviceToHost, nullptr));
         }
     }
     BMMGPU_CUDA_TRY(cudaStreamSynchronize(nullptr));

@@ -31,14 +31,6 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
                       uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate, cudaStream_t stream,
                       uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
 void umma_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
-int launch_cubic_umma1(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
-                       uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate, cudaStream_t stream,
-                       uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
-void umma1_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
-int launch_cubic_umma2np(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
-                         uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate,
-                         cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
-void umma2np_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits);
 int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, const bmmgpu_plan* plan,
                       int kernel, int leaf_log2, double* timing_ms);
 int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const uint64_t* A, const uint64_t* B,
@@ -50,8 +42,22 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
 
 namespace {
 thread_local std::string g_error;
-std::atomic<uint64_t> g_launches{0};
+struct CallStats {
+    std::atomic<uint64_t> launches{0}, h2d{0}, d2h{0};
+};
+thread_local CallStats t_stats;               // this thread's last host-API call
+thread_local CallStats* t_parent = nullptr;   // worker thread of a call on another thread
+CallStats& cur_stats() { return t_parent ? *t_parent : t_stats; }
 }  // namespace
+
+void* call_stats() { return &cur_stats(); }
+void adopt_call_stats(void* stats) { t_parent = static_cast<CallStats*>(stats); }
+void reset_call_stats() {
+    CallStats& c = cur_stats();
+    c.launches.store(0);
+    c.h2d.store(0);
+    c.d2h.store(0);
+}
 
 void set_error(const std::string& msg) { g_error = msg; }
 
@@ -103,11 +109,10 @@ StreamSet::~StreamSet() {
         if (s[i]) g_stream_pool[device].push_back(s[i]);
 }
 
-void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
-std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
+void count_launch(uint64_t n) { cur_stats().launches.fetch_add(n, std::memory_order_relaxed); }
 void count_copy(cudaMemcpyKind kind, uint64_t bytes) {
-    if (kind == cudaMemcpyHostToDevice) g_h2d.fetch_add(bytes, std::memory_order_relaxed);
-    if (kind == cudaMemcpyDeviceToHost) g_d2h.fetch_add(bytes, std::memory_order_relaxed);
+    if (kind == cudaMemcpyHostToDevice) cur_stats().h2d.fetch_add(bytes, std::memory_order_relaxed);
+    if (kind == cudaMemcpyDeviceToHost) cur_stats().d2h.fetch_add(bytes, std::memory_order_relaxed);
 }
 
 namespace {
@@ -227,8 +232,6 @@ int granularity(int kernel, uint64_t* gm, uint64_t* gn, uint64_t* gk) {
     switch (resolve_kernel(kernel)) {
         case BMMGPU_KERNEL_LOP3: lop3_granularity(gm, gn, gk); return kOk;
         case BMMGPU_KERNEL_UMMA_F4: umma_granularity(gm, gn, gk); return kOk;
-        case BMMGPU_KERNEL_UMMA_F4_1SM: umma1_granularity(gm, gn, gk); return kOk;
-        case BMMGPU_KERNEL_UMMA_F4_PAIR_NP: umma2np_granularity(gm, gn, gk); return kOk;
         default: set_error("unknown kernel id " + std::to_string(kernel)); return kEinval;
     }
 }
@@ -312,12 +315,6 @@ int launch_cubic_kernel(int kernel, const uint64_t* dA, uint64_t lda, const uint
         case BMMGPU_KERNEL_UMMA_F4:
             return launch_cubic_umma(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream, batch,
                                      sA_batch, sB_batch, sC_batch);
-        case BMMGPU_KERNEL_UMMA_F4_1SM:
-            return launch_cubic_umma1(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream, batch,
-                                      sA_batch, sB_batch, sC_batch);
-        case BMMGPU_KERNEL_UMMA_F4_PAIR_NP:
-            return launch_cubic_umma2np(dA, lda, dBt, ldbt, dC, ldc, m_pad, n_pad, kw, gf2, accumulate, stream,
-                                        batch, sA_batch, sB_batch, sC_batch);
         default: set_error("unknown kernel id " + std::to_string(kernel)); return kEinval;
     }
 }
@@ -511,7 +508,7 @@ int bmmgpu_slab_rows(uint64_t m, uint32_t parts, uint32_t index, uint64_t gran, 
     return kOk;
 }
 const char* bmmgpu_version(void) { return "bmm-b200 0.1 (sm_100a)"; }
-uint64_t bmmgpu_last_launch_count(void) { return g_launches.load(); }
+uint64_t bmmgpu_last_launch_count(void) { return t_stats.launches.load(); }
 
 int bmmgpu_host_alloc(uint64_t bytes, void** ptr) {
     if (!ptr) {
@@ -537,8 +534,8 @@ int bmmgpu_host_free(void* ptr) {
 }
 
 int bmmgpu_last_copy_bytes(uint64_t* h2d, uint64_t* d2h) {
-    if (h2d) *h2d = g_h2d.load();
-    if (d2h) *d2h = g_d2h.load();
+    if (h2d) *h2d = t_stats.h2d.load();
+    if (d2h) *d2h = t_stats.d2h.load();
     return kOk;
 }
 
@@ -657,9 +654,7 @@ int bmmgpu_dev_cubic_batched(const uint64_t* dA, uint64_t lda, uint64_t sA, cons
 
 int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, uint64_t k, uint64_t n,
                  int32_t semiring, const bmmgpu_opts* opts) {
-    g_launches.store(0);
-    g_h2d.store(0);
-    g_d2h.store(0);
+    reset_call_stats();
     if (semiring != BMMGPU_BOOLEAN_OR_AND && semiring != BMMGPU_GF2_XOR_AND) {
         set_error("unknown semiring");
         return kEinval;
@@ -692,7 +687,12 @@ int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, 
         work(jobs[0]);
     } else {
         std::vector<std::thread> threads;
-        for (auto& j : jobs) threads.emplace_back(work, std::ref(j));
+        void* stats = call_stats();
+        for (auto& j : jobs)
+            threads.emplace_back([&work, stats](SlabJob& jj) {
+                adopt_call_stats(stats);
+                work(jj);
+            }, std::ref(j));
         for (auto& t : threads) t.join();
     }
     float worst = 0.f;
@@ -709,9 +709,7 @@ int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, 
 
 int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int32_t algo,
                     const bmmgpu_plan* plan, int32_t semiring, const bmmgpu_opts* opts) {
-    g_launches.store(0);
-    g_h2d.store(0);
-    g_d2h.store(0);
+    reset_call_stats();
     const bmmgpu_opts defaults{};
     const bmmgpu_opts& o = opts ? *opts : defaults;
     if (algo == BMMGPU_ALGO_CUBIC) return bmmgpu_cubic(A, B, C, n, n, n, semiring, opts);

@@ -13,6 +13,13 @@ void set_error(const std::string& msg);
 void count_launch(uint64_t n = 1);
 // Host<->device bytes moved by the host-API drivers (bmmgpu_last_copy_bytes).
 void count_copy(cudaMemcpyKind kind, uint64_t bytes);
+// Per-call diagnostics (launch count, copied bytes) belong to the calling thread: a
+// host-API call resets its thread's tallies, and the worker threads it spawns (one per
+// device) add into the caller's with call_stats() / adopt_call_stats(), so concurrent
+// calls on different threads never see each other's counts.
+void* call_stats();
+void adopt_call_stats(void* stats);  // nullptr: back to this thread's own tallies
+void reset_call_stats();
 // Host<->device copies of the host-API drivers.  Page-locked host buffers go straight
 // to the DMA engines (asynchronous on `s`); large pageable ones (the reference API's
 // std::vector storage) are staged through pinned double buffers, with host threads

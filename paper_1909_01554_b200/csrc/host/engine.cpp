@@ -9,6 +9,7 @@
 #include <string>
 
 #include "bmmgpu.h"
+#include "../schemes.h"
 
 namespace bmm {
 
@@ -225,9 +226,29 @@ BitMatrix multiply(const BitMatrix& a, const BitMatrix& b, Algo algo, const Laye
         const std::uint64_t kernels = ipow(7, depth);
         counter->add_kernels(kernels);
         counter->add_ands(kernels * kBlockBits);
-        counter->add_xors((predicted_additions(d, depth, CostPart::LinearCombinations) +
-                           predicted_additions(d, depth, CostPart::BasisChanges)) *
-                          kBlockWords);
+        std::uint64_t xors = predicted_additions(d, depth, CostPart::BasisChanges) * kBlockWords;
+        if (plan.d_host == 0) {
+            xors += predicted_additions(d, depth, CostPart::LinearCombinations) * kBlockWords;
+        } else {
+            // The reference runs the top d_host levels through pipeline::coordinate
+            // (engine.cpp:375-378), which tallies folds, not SLP additions: per sub-instance
+            // h, (nnz(alpha^(x)d_host row h) - 1) + (nnz(beta row h) - 1) generation folds and
+            // nnz(gamma column h) aggregation folds of inner_words each (pipeline.cpp:108-179),
+            // plus each sub-instance's multiply_alt at depth - d_host.  Summed over h the
+            // Kronecker row weights factor: sum_h prod_l nnz(h_l) = (sum_h nnz(h))^d_host.
+            const bmmgpu::Scheme* sc = bmmgpu::scheme_for(algo_id(d.which));
+            std::uint64_t wa = 0, wb = 0, wg = 0;
+            for (int h = 0; h < 7; ++h) {
+                wa += std::popcount(bmmgpu::row_mask(sc->alpha[h]));
+                wb += std::popcount(bmmgpu::row_mask(sc->beta[h]));
+            }
+            for (int q = 0; q < 4; ++q) wg += std::popcount(bmmgpu::row_mask(sc->gamma[q]));
+            const std::uint64_t subs = ipow(7, plan.d_host);
+            const std::uint64_t inner_words = (a.rows * a.rows / kWordBits) >> (2 * plan.d_host);
+            xors += (ipow(wa, plan.d_host) - subs + ipow(wb, plan.d_host) - subs + ipow(wg, plan.d_host)) * inner_words;
+            xors += subs * predicted_additions(d, depth - plan.d_host, CostPart::LinearCombinations) * kBlockWords;
+        }
+        counter->add_xors(xors);
     }
     return c;
 }

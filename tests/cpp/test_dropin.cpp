@@ -310,6 +310,29 @@ void pipeline_gpu_cases() {
         CHECK(multiply(a, b, Algo::AltChaining, p2, Semiring::Gf2XorAnd) == want);
         CHECK(multiply(a, b, Algo::StrassenWinograd, p3, Semiring::Gf2XorAnd) == want);
     });
+    run("multiply: OpCounter tallies with host levels equal the reference's", [] {
+        // expected [word_xors] of the UNMODIFIED reference multiply at n = 512 (depth 3), read
+        // from oracle/_ref (bmmref_multiply with counts); d_host > 0 goes through its
+        // pipeline::coordinate, which counts folds rather than SLP additions
+        const BitMatrix a = BitMatrix::random(512, 512, 1), b = BitMatrix::random(512, 512, 2);
+        struct Case {
+            Algo algo;
+            int dh, ds, dp;
+            std::uint64_t xors;
+        };
+        const Case cases[] = {{Algo::StrassenWinograd, 0, 1, 2, 89280},  {Algo::StrassenWinograd, 1, 1, 1, 102592},
+                              {Algo::StrassenWinograd, 2, 0, 1, 172480}, {Algo::StrassenWinograd, 3, 0, 0, 482944},
+                              {Algo::AltSelfInverse, 0, 1, 2, 89856},    {Algo::AltSelfInverse, 1, 1, 1, 93952},
+                              {Algo::AltSelfInverse, 2, 0, 1, 107776},   {Algo::AltSelfInverse, 3, 0, 0, 166528},
+                              {Algo::AltChaining, 1, 0, 2, 96000},       {Algo::AltChaining, 2, 0, 1, 119040},
+                              {Algo::AltChaining, 3, 0, 0, 213120}};
+        for (const Case& k : cases) {
+            LayerPlan p = plan_for(k.ds, k.dp, k.dh);
+            OpCounter c;
+            (void)multiply(a, b, k.algo, p, Semiring::Gf2XorAnd, &c);
+            CHECK(c.word_xors == k.xors && c.kernel_invocations == 343 && c.word_ands == 343 * kBlockBits);
+        }
+    });
 }
 
 void host_cases() {

@@ -200,3 +200,30 @@ def test_interleaved_basis_change_streams_beyond_the_budget(engine, oracle, monk
         assert np.array_equal(w, ref), (algo, factor, budget)
         assert lib.bmmgpu_basis_change(w.ctypes.data, w.size, levels, algo, factor, 1) == 0
         assert np.array_equal(w, v), (algo, factor, budget)
+
+
+@pytest.mark.parametrize("budget", [None, 24 << 10, 6 << 10])
+def test_basis_change_inner_mode_not_power_of_two(engine, oracle, monkeypatch, budget):
+    """[4]*3 [7 * 4096 bits] vectors (the inner mode is not a power of two; reference
+    basis_change accepts them, engine.cpp:146-172): streamed blocks are whole level
+    groups, so the result equals the in-core run and the inverse restores the input."""
+    lib = engine.lib()
+    levels, inner = 3, 7 * 64
+    v = oracle.random(1, (4 ** levels) * inner * 64, 47)
+    monkeypatch.delenv("BMMGPU_BASIS_BUDGET", raising=False)
+    want = v.copy()
+    assert lib.bmmgpu_basis_change(want.ctypes.data, want.size, levels, 2, 0, 0) == 0
+    # phi of alt-si applied level by level in numpy: x11 ^= x01 ^ x10 over [outer][4][inner_l]
+    ref = v.copy()
+    for l in range(levels):
+        il = v.size >> (2 * (l + 1))
+        r = ref.reshape(-1, 4, il)
+        r[:, 3] ^= r[:, 1] ^ r[:, 2]
+    assert np.array_equal(want, ref)
+    if budget is not None:
+        monkeypatch.setenv("BMMGPU_BASIS_BUDGET", str(budget))
+    w = v.copy()
+    assert lib.bmmgpu_basis_change(w.ctypes.data, w.size, levels, 2, 0, 0) == 0
+    assert np.array_equal(w, want), budget
+    assert lib.bmmgpu_basis_change(w.ctypes.data, w.size, levels, 2, 0, 1) == 0
+    assert np.array_equal(w, v), budget
