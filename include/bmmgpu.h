@@ -186,6 +186,11 @@ int bmmgpu_host_free(void* ptr);
 int bmmgpu_last_copy_bytes(uint64_t* h2d, uint64_t* d2h);
 
 int bmmgpu_device_count(void);
+
+/* Debug: tensor-core launches that ran with wave-aligned loaders (long-K products with
+ * more output tiles than CTA pairs) and loaders that stopped aligning at the spin limit,
+ * since the library was loaded (the tests assert the mode runs and never times out). */
+int bmmgpu_debug_wave_stats(uint64_t* aligned_launches, uint64_t* loader_timeouts);
 const char* bmmgpu_last_error(void);
 const char* bmmgpu_version(void);
 

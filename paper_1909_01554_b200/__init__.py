@@ -104,6 +104,8 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_block_timer_read.argtypes = [ctypes.POINTER(ctypes.c_double), _u64p]
         L.bmmgpu_block_timer_read.restype = ctypes.c_int
         L.bmmgpu_last_launch_count.restype = u64
+        L.bmmgpu_debug_wave_stats.argtypes = [_u64p, _u64p]
+        L.bmmgpu_debug_wave_stats.restype = ctypes.c_int
         L.bmmgpu_device_count.restype = ctypes.c_int
         L.bmmgpu_last_error.restype = ctypes.c_char_p
         L.bmmgpu_version.restype = ctypes.c_char_p

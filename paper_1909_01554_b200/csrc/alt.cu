@@ -1480,6 +1480,7 @@ extern "C" int bmmgpu_dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, ui
 
 extern "C" int bmmgpu_multiply_alt(const uint64_t* a_hat, const uint64_t* b_hat, uint64_t* c_hat, int32_t depth,
                                    int32_t algo, const bmmgpu_opts* opts) {
+    bmmgpu::reset_call_stats();
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
         bmmgpu::set_error("no CUDA device available; the bit-matrix engine has no CPU fallback");
@@ -1506,6 +1507,7 @@ extern "C" int bmmgpu_multiply_alt(const uint64_t* a_hat, const uint64_t* b_hat,
 
 extern "C" int bmmgpu_basis_change(uint64_t* words, uint64_t total_words, int32_t levels, int32_t algo,
                                    int32_t factor, int32_t inverse) {
+    bmmgpu::reset_call_stats();
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
         bmmgpu::set_error("no CUDA device available; the bit-matrix engine has no CPU fallback");

@@ -59,6 +59,8 @@
 // ~4.56 us tile.
 #include <cuda.h>
 
+#include <atomic>
+
 #include "umma.cuh"
 
 namespace bmmgpu {
@@ -111,6 +113,9 @@ static_assert(P_SMEM <= 232448 - 1024, "stage ring exceeds shared memory");
 // 1024/2048 empty seen (CTA 0/1), 1536/2560 full arrive (first warp of the stage's group).
 // Compiled in only with -DBMMGPU_TRACE (the build never sets it by default).
 __device__ unsigned long long g_trace[6144];
+// Loaders of wave-aligned launches that hit the spin limit and stopped aligning (debug
+// counter behind bmmgpu_debug_wave_stats; the tests assert it stays 0).
+__device__ unsigned long long g_wave_timeouts;
 #ifdef BMMGPU_TRACE
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -632,6 +637,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                 }
                 if (wave_ctr && rank == 0) umma::red_release_add_u64(wave_ctr, 1);
             }
+            if (wave_ctr && !align) atomicAdd(&g_wave_timeouts, 1ull);
         }
     } else if (warp >= P_LOADER_WARP0) {
         // ------------------------------------------------ loaders: packed bits global -> shared (cp.async)
@@ -759,6 +765,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #define BMMGPU_L2_PROMOTION 3  // CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
 
+std::atomic<uint64_t> g_wave_aligned_launches{0};
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -863,6 +871,7 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
         BMMGPU_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, 8, stream));
         count_launch();
         wave_ctr = static_cast<unsigned long long*>(ctr.p);
+        g_wave_aligned_launches.fetch_add(1, std::memory_order_relaxed);
     }
     kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw, flags, map,
                                                              uint32_t(total), epi_sleep, wave_ctr, tmA, tmB);
@@ -881,6 +890,18 @@ extern "C" int bmmgpu_debug_umma2_probe(unsigned long long* out) {
     (void)out;
     return 1;
 #endif
+}
+
+// Debug: K2 launches that ran with wave-aligned loaders (host count) and loaders that gave
+// up aligning after the spin limit (device count), since the library was loaded.
+extern "C" int bmmgpu_debug_wave_stats(uint64_t* aligned_launches, uint64_t* loader_timeouts) {
+    if (aligned_launches) *aligned_launches = bmmgpu::g_wave_aligned_launches.load();
+    if (loader_timeouts) {
+        unsigned long long t = 0;
+        if (cudaMemcpyFromSymbol(&t, bmmgpu::g_wave_timeouts, sizeof(t)) != cudaSuccess) return 5;
+        *loader_timeouts = t;
+    }
+    return 0;
 }
 
 // Debug: copy the pipeline timestamps of the last traced launch.

@@ -126,6 +126,15 @@ def main() -> None:
         c = ref.multiply_alt(ah, bh, ds, dp, 1, 1)
         C["multiply_alt"].append({"d_serial": ds, "d_parallel": dp, "a_seed": sa, "b_seed": sb, "scheme": 1,
                                   **digest(c)})
+    # the other two schemes, and a deeper alt-si vector (n = 2048) for the GPU tests
+    for scheme, ds, dp, sa, sb in [(0, 1, 2, 81, 82), (2, 1, 2, 83, 84), (1, 2, 3, 85, 86)]:
+        depth = ds + dp
+        n = 64 << depth
+        ah = ref.random(1, n * n, sa)
+        bh = ref.random(1, n * n, sb)
+        c = ref.multiply_alt(ah, bh, ds, dp, 1, scheme)
+        C["multiply_alt"].append({"d_serial": ds, "d_parallel": dp, "a_seed": sa, "b_seed": sb, "scheme": scheme,
+                                  **digest(c)})
 
     C["predicted_additions"] = []
     for scheme in (0, 1, 2):

@@ -3,6 +3,8 @@ alt-chain) on B200 equal the reference's outputs bit for bit, for every leaf
 size the recursion can stop at."""
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -227,3 +229,23 @@ def test_basis_change_inner_mode_not_power_of_two(engine, oracle, monkeypatch, b
     assert np.array_equal(w, want), budget
     assert lib.bmmgpu_basis_change(w.ctypes.data, w.size, levels, 2, 0, 1) == 0
     assert np.array_equal(w, v), budget
+
+
+def test_multiply_alt_hat_vectors_match_reference_digests(engine, oracle, golden):
+    """bmmgpu_multiply_alt (the reference's multiply_alt on interleaved vectors already in
+    the scheme's basis, engine.cpp:293-349, and the solve stage of the host pipeline)
+    reproduces the reference's own outputs: FNV digests, popcounts and first words from
+    oracle/_ref for all three schemes, depths 2 to 5."""
+    lib = engine.lib()
+    for c in golden["multiply_alt"]:
+        depth = c["d_serial"] + c["d_parallel"]
+        n = 64 << depth
+        ah = oracle.random(1, n * n, c["a_seed"])
+        bh = oracle.random(1, n * n, c["b_seed"])
+        ch = np.zeros_like(ah)
+        for leaf in (0, 7):  # default leaves, and 128-bit leaves (more recursion levels on the GPU)
+            opts = engine._opts(0, leaf_log2=leaf)
+            assert lib.bmmgpu_multiply_alt(ah.ctypes.data, bh.ctypes.data, ch.ctypes.data, depth, c["scheme"] + 1,
+                                           ctypes.byref(opts)) == 0, lib.bmmgpu_last_error()
+            assert f"{oracle.fnv1a64(ch):016x}" == c["fnv"], (c, leaf)
+            assert oracle.popcount(ch) == c["pop"] and f"{int(ch[0]):016x}" == c["w0"]

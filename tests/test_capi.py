@@ -56,6 +56,15 @@ def test_kernels_are_sm100a_native():
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", str(bmm.LIB_PATH)], capture_output=True, text=True).stdout
     assert "LOP3.LUT" in sass
+    # the default block product is a tcgen05 CTA-pair kernel fed by TMA: pair MMAs
+    # (UTCOMMA.2CTA = tcgen05.mma.cta_group::2 kind::mxf4), TMEM loads / stores (LDTM /
+    # STTM), the pair's TMEM allocator and commit barriers, 3-D tensor-map loads
+    fns = sass.split("Function : ")
+    k2 = [f for f in fns if "cubic_umma2_kernel" in f.splitlines()[0]]
+    assert len(k2) == 2, "the TMA and the cp.async-loader instantiations"
+    for op in ("UTCOMMA.2CTA", "LDTM", "STTM", "UTCATOMSWS.2CTA", "UTCBAR.2CTA"):
+        assert all(op in f for f in k2), op
+    assert any("UTMALDG.3D" in f for f in k2)
 
 
 @pytest.mark.skipif(HAS_GPU, reason="checks the no-device path")

@@ -94,6 +94,8 @@ def test_basis_change_alt_si(oracle, golden):
 
 def test_multiply_alt_on_hat_vectors(oracle, golden):
     for c in golden["multiply_alt"]:
+        if c["scheme"] != 1:  # the oracle restates the alt-si scheme; the GPU test covers all three
+            continue
         depth = c["d_serial"] + c["d_parallel"]
         n = 64 << depth
         ah = oracle.random(1, n * n, c["a_seed"])
