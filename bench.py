@@ -49,7 +49,7 @@ WORKLOADS = {
     "c4-gf2-cubic-262144": (262144, GF2, 0, "GF(2) product n=262144, output row slabs (BASELINE configs[3])"),
     "c4-gf2-altsi-262144": (262144, GF2, 2, "GF(2) product n=262144 alternative-basis Strassen"),
     # a small instance of the same multi-GPU tile partition (tests)
-    "c4s-gf2-altsi-16384": (16384, GF2, 2, "GF(2) product n=16384 alternative-basis Strassen (tile-partition test size)"),
+    "c4s-gf2-altsi-16384": (16384, GF2, 2, "GF(2) product n=16384 alternative-basis Strassen (multi-rank test size)"),
     # configs[4] (n = 2^20 on 8 GPUs needs 384 GiB of host memory for A, B, C; one box has
     # 196 GB), scaled to one GPU: n = 2^19 from pinned host memory through the out-of-core
     # driver with a device budget below the operands (A row panels resident, B streamed in
@@ -619,23 +619,53 @@ def run_ooc(args, dist: Dist) -> None:
         shared_b.close()
 
 
-def run_alt_tiles(args, dist: Dist) -> None:
-    """Fast GF(2) product on several GPUs (SURVEY section 8e, configs[3]): C is cut
-    into 4 x 4 output tiles of n/4, tile (I, J) = XOR over K of the alt-basis products
-    A[I, K] . B[K, J] (n/4 each, strided views of the resident operands), and the 16
-    tiles are dealt round robin to the ranks -- disjoint outputs, no exchange, no
-    collective.  (64 block products of n/4 instead of the single-GPU recursion's 49:
-    the price of the partition.)"""
+def slab_exchange_xor(P, R, slabs: list[tuple[int, int]], me: int, G: int, stage_on_host: bool, fold) -> None:
+    """The multi-rank fast product's one exchange step: rank d receives row slab d of every
+    rank's partial product P (n x w words) into R (G pieces of its slab, rank order) by one
+    all-to-all, then XOR-folds pieces 1 .. G-1 into piece 0 (`fold(d)`, the library's fold
+    kernel on the GPU).  With gloo the tensors are staged through host memory."""
     import torch
+    import torch.distributed as tdist
+    r0, r1 = slabs[me]
+    w = P.shape[1]
+    if G > 1:
+        splits_in = [(r1 - r0) * w] * G
+        splits_out = [(b - a) * w for a, b in slabs]
+        if stage_on_host:
+            recv = torch.empty(R.numel(), dtype=torch.int64)
+            tdist.all_to_all_single(recv, P.reshape(-1).cpu(), splits_in, splits_out)
+            R.view(-1).copy_(recv)
+        else:
+            tdist.all_to_all_single(R.view(-1), P.reshape(-1), splits_in, splits_out)
+    else:
+        R.copy_(P[r0:r1])
+    for d in range(1, G):
+        fold(d)
+
+
+def run_alt_deal(args, dist: Dist) -> None:
+    """Fast GF(2) product on several GPUs (SURVEY section 8e, configs[3]): the top dh
+    levels of the recursion are 7^dh independent sub-instances (the reference host layer,
+    pipeline.cpp:198-369), dealt round robin to the ranks; each rank computes the partial
+    product of its share on its GPU from resident A and Bt (bmmgpu_dev_multiply_partial),
+    then the one exchange step: an all-to-all of output-row slabs (NCCL over NVLink), each
+    rank XOR-folding the partials of the slab it owns.  dh is the library's most even deal
+    (bmmgpu_host_levels: 343 sub-instances of n/8 over 8 ranks)."""
+    import torch
+    import torch.distributed as tdist
     import paper_1909_01554_b200 as bmm
 
     n, ring, algo, desc = WORKLOADS[args.workload]
     lib = bmm.lib()
     dev = dist.device
     torch.cuda.set_device(dev)
-    w, T = n // 64, n // 4
-    tw = T // 64
-    mine = [t for t in range(16) if t % dist.world == dist.rank]
+    G, me = dist.world, dist.rank
+    w = n // 64
+    dh = lib.bmmgpu_host_levels(n, G, args.leaf_log2)
+    subs = 7 ** dh
+    mine = len(range(me, subs, G))
+    slabs = [bmm.slab_rows(n, G, d, 256) for d in range(G)]
+    r0, r1 = slabs[me]
     hA = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
     hB = torch.empty(n * w, dtype=torch.int64, pin_memory=True)
     bmm.random_rows_into(hA.numpy().view(np.uint64), n, 1, 0, n)
@@ -643,10 +673,11 @@ def run_alt_tiles(args, dist: Dist) -> None:
     dA = hA.view(n, w).to(f"cuda:{dev}")
     dB = hB.view(n, w).to(f"cuda:{dev}")
     dBt = torch.empty((n, w), dtype=torch.int64, device=f"cuda:{dev}")
-    dC = torch.empty((len(mine), T, tw), dtype=torch.int64, device=f"cuda:{dev}")
-    dP = torch.empty((T, tw), dtype=torch.int64, device=f"cuda:{dev}")
+    dP = torch.empty((n, w), dtype=torch.int64, device=f"cuda:{dev}")       # this rank's partial product
+    dR = torch.empty((G * (r1 - r0), w), dtype=torch.int64, device=f"cuda:{dev}")  # received pieces of my slab
     stream = torch.cuda.current_stream()
     sp = ctypes.c_void_p(stream.cuda_stream)
+    on_cpu = dist.backend == "gloo"
     torch.cuda.synchronize()
 
     def check(rc: int) -> None:
@@ -655,15 +686,11 @@ def run_alt_tiles(args, dist: Dist) -> None:
 
     def step() -> None:
         check(lib.bmmgpu_dev_transpose(dB.data_ptr(), w, n, n, dBt.data_ptr(), n, w, sp))
-        for slot, t in enumerate(mine):
-            I, J = divmod(t, 4)
-            for K in range(4):
-                a = dA.data_ptr() + 8 * (I * T * w + K * tw)
-                bt = dBt.data_ptr() + 8 * (J * T * w + K * tw)
-                out = dC[slot] if K == 0 else dP
-                check(lib.bmmgpu_dev_multiply(a, w, bt, w, out.data_ptr(), tw, T, algo, args.leaf_log2, 0, sp))
-                if K:
-                    check(lib.bmmgpu_dev_fold(dC[slot].data_ptr(), tw, dP.data_ptr(), tw, T, tw, ring, sp))
+        check(lib.bmmgpu_dev_multiply_partial(dA.data_ptr(), w, dBt.data_ptr(), w, dP.data_ptr(), w, n, algo, dh,
+                                              me, G, args.leaf_log2, 0, sp))
+        slab_exchange_xor(dP, dR, slabs, me, G, on_cpu,
+                          lambda d: check(lib.bmmgpu_dev_fold(dR.data_ptr(), w, dR.data_ptr() + 8 * d * (r1 - r0) * w,
+                                                              w, r1 - r0, w, ring, sp)))
 
     for _ in range(args.warmup):
         step()
@@ -688,49 +715,48 @@ def run_alt_tiles(args, dist: Dist) -> None:
     check(lib.bmmgpu_block_timer_read(ctypes.byref(blk_ms), ctypes.byref(blk_n)))
     check(lib.bmmgpu_block_timer(0))
     ms = dist.max(t0.elapsed_time(t1) / args.steps)
-    checked = None
+    parity = None
     if args.check:
-        # every tile of this rank against the tensor-core cubic product of A[I, :] . B[:, J]
-        ref = torch.empty((T, tw), dtype=torch.int64, device=f"cuda:{dev}")
-        checked = 0
-        for slot, t in enumerate(mine):
-            I, J = divmod(t, 4)
-            check(lib.bmmgpu_dev_cubic(dA.data_ptr() + 8 * I * T * w, w, dBt.data_ptr() + 8 * J * T * w, w,
-                                       ref.data_ptr(), tw, T, T, w, ring, 0, 0, sp))
-            torch.cuda.synchronize()
-            if not torch.equal(ref, dC[slot]):
-                raise RuntimeError(f"tile {t} differs from the cubic product")
-            # and independently of the library: Freivalds on the tile, C_IJ = A[I, :] . B[:, J]
-            if not freivalds_gf2(dA[I * T:(I + 1) * T], dB[:, J * tw:(J + 1) * tw], dC[slot], T, n, T):
-                raise RuntimeError(f"tile {t} fails the Freivalds check")
-            checked += 1
-    depth = (T // 64).bit_length() - 1
-    e_levels = max(0, min(depth, depth + 6 - (args.leaf_log2 or 12)))
-    leaf = T >> e_levels
+        # this rank's slab against the tensor-core cubic product of A[slab, :] . B (a different
+        # algorithm) and, independently of the library, Freivalds with 64 random bit-columns
+        pt0 = time.perf_counter()
+        ref = torch.empty((r1 - r0, w), dtype=torch.int64, device=f"cuda:{dev}")
+        check(lib.bmmgpu_dev_cubic(dA.data_ptr() + 8 * r0 * w, w, dBt.data_ptr(), w, ref.data_ptr(), w, r1 - r0, n, w,
+                                   ring, 0, 0, sp))
+        torch.cuda.synchronize()
+        mine_slab = dR[: r1 - r0]
+        ok_cubic = bool(torch.equal(ref, mine_slab))
+        ok_frei = freivalds_gf2(dA[r0:r1], dB, mine_slab, r1 - r0, n, n)
+        good = ok_cubic and ok_frei
+        parity = {"slab_equals_cubic_product": ok_cubic, "freivalds_64_columns": ok_frei,
+                  "ok": bool(dist.max(0.0 if good else 1.0) == 0.0), "seconds": round(time.perf_counter() - pt0, 2),
+                  "method": "every rank's output slab equal to the tensor-core cubic product A[slab,:].B and passing "
+                            "Freivalds (64 random bit-columns, torch gather/XOR)"}
+    e = max(0, min((n // 64).bit_length() - 1, (n // 64).bit_length() - 1 + 6 - (args.leaf_log2 or 12)))
+    e_sub = e - dh
+    leaf = n >> e
     kms = blk_ms.value / args.steps
-    launch_bops = len(mine) * 4 * 7**e_levels * eff_bops(leaf, leaf, leaf)
+    launch_bops = mine * 7 ** e_sub * eff_bops(leaf, leaf, leaf)
     peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())
     achieved = launch_bops / (kms * 1e-3)
     value = eff_bops(n, n, n) / (ms * 1e-3) / 1e15
     if dist.rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "n3_rate": n3_rate(value, n), "dtype": "e2m1", "data": "synthetic (BitMatrix::random seeds 1, 2, mt19937_64)",
+                "vs_baseline": None, "n3_rate": n3_rate(value, n), "dtype": "e2m1",
+                "data": "synthetic (BitMatrix::random seeds 1, 2, mt19937_64)",
                 "config": {"workload": args.workload, "desc": desc, "n": n, "ring": "gf2",
                            "algo": ["cubic", "sw", "alt-si", "alt-chain"][algo],
-                           "parallelism": f"4x4 output tiles of n/4 round robin over {dist.world} ranks, "
-                                          "each tile the XOR of 4 alt-basis block products, no exchange",
-                           "tiles_per_rank0": len(mine)},
+                           "parallelism": f"7^{dh} host-layer sub-instances of n/{2 ** dh} round robin over "
+                                          f"{dist.world} ranks, partial products XOR-folded after one all-to-all "
+                                          "of output-row slabs",
+                           "host_levels": dh, "subinstances_rank0": mine},
                 "roofline": {"bound": "tensor", "achieved": achieved / 1e12, "peak": peaks["umma_mxf4_bops"] / 1e12,
                              "unit": "Tbop/s", "frac": achieved / peaks["umma_mxf4_bops"], "traffic": None,
-                             "kernel": f"cubic_umma2_kernel (leaf layer: 7^{e_levels} products of {leaf}^3 per block)",
+                             "kernel": f"cubic_umma2_kernel (leaf layer: 7^{e_sub} products of {leaf}^3 per "
+                                       "sub-instance)",
                              "kernel_ms": kms, "kernel_share_of_step": kms / ms},
-                "cpu_baseline": None, "e2e": None, "tiles_checked_rank0": checked,
-                "parity": None if checked is None else {
-                    "ok": True, "tiles_checked_rank0": checked,
-                    "method": "every tile of rank 0 equal to the tensor-core cubic product of A[I,:].B[:,J] and "
-                              "passing Freivalds (64 random bit-columns, torch gather/XOR)"},
-                "clocks": clocks,
+                "cpu_baseline": None, "e2e": None, "parity": parity, "clocks": clocks,
                 "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
 
@@ -753,7 +779,7 @@ def run_ours(args, dist: Dist) -> None:
         r0, r1 = shard_rows(n, dist.rank, dist.world, gm)
     else:
         if dist.world > 1:
-            return run_alt_tiles(args, dist)
+            return run_alt_deal(args, dist)
         r0, r1 = 0, n
     m = r1 - r0
     # pinned host inputs (the e2e leg copies from these every step)

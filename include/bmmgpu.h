@@ -86,7 +86,11 @@ int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, 
 
 /* Fast product through a bilinear scheme: square n = 64 * 2^depth, plan.depth()
  * must equal depth.  Cubic algo dispatches to bmmgpu_cubic; Boolean with a fast
- * algo is BMMGPU_EINVAL.  Replaces bmm::multiply (reference engine.cpp:351-382). */
+ * algo is BMMGPU_EINVAL.  Replaces bmm::multiply (reference engine.cpp:351-382).
+ * With several devices in opts->device_mask the top host levels of the recursion
+ * (plan.d_host, or an automatic choice when it is 0) are dealt across the devices,
+ * one host thread each, and the partial products are XOR-folded slab by slab over
+ * peer copies (bmmgpu_dev_multiply_partial). */
 int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int32_t algo,
                     const bmmgpu_plan* plan, int32_t semiring, const bmmgpu_opts* opts);
 
@@ -153,6 +157,23 @@ int bmmgpu_dev_fold(uint64_t* dst, uint64_t ldd, const uint64_t* src, uint64_t l
  * device's memory pool as the recursion proceeds. */
 int bmmgpu_dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
                         uint64_t n, int32_t algo, int32_t leaf_log2, int32_t kernel, void* stream);
+
+/* The host layer on one device (reference pipeline::coordinate, pipeline.cpp:198-369,
+ * with generate_into / aggregate 108-179): the top `host_levels` recursion levels of the
+ * fast product are 7^host_levels independent sub-instances; dC (n x n/64, stride ldc,
+ * overwritten) = the XOR of the contributions of sub-instances first, first + stride,
+ * ... (each generated on the device from dA / dBt, solved by the fast product, folded
+ * into its C sub-blocks).  The XOR over first = 0 .. stride-1 is A.B: the multi-device
+ * and multi-rank drivers deal sub-instances this way and fold the partials once.
+ * 0 <= host_levels <= 4 and at least one recursion level must remain below them
+ * (leaf_log2 as in bmmgpu_opts).  dA / dBt are only read. */
+int bmmgpu_dev_multiply_partial(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
+                                uint64_t ldc, uint64_t n, int32_t algo, int32_t host_levels, uint32_t first,
+                                uint32_t stride, int32_t leaf_log2, int32_t kernel, void* stream);
+
+/* Host levels the multi-device fast product uses for n on `parts` devices when the
+ * plan does not fix them (the most even deal of sub-instances, see capi.cu). */
+int bmmgpu_host_levels(uint64_t n, uint32_t parts, int32_t leaf_log2);
 
 /* The output-row slab [begin, end) of part `index` of `parts` (gran-aligned,
  * contiguous, covering [0, m) exactly once).  The single partition rule of the

@@ -104,6 +104,11 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_block_timer_read.argtypes = [ctypes.POINTER(ctypes.c_double), _u64p]
         L.bmmgpu_block_timer_read.restype = ctypes.c_int
         L.bmmgpu_last_launch_count.restype = u64
+        L.bmmgpu_dev_multiply_partial.argtypes = [vp, u64, vp, u64, vp, u64, u64, i32, i32, ctypes.c_uint32,
+                                                  ctypes.c_uint32, i32, i32, vp]
+        L.bmmgpu_dev_multiply_partial.restype = ctypes.c_int
+        L.bmmgpu_host_levels.argtypes = [u64, ctypes.c_uint32, i32]
+        L.bmmgpu_host_levels.restype = ctypes.c_int
         L.bmmgpu_debug_wave_stats.argtypes = [_u64p, _u64p]
         L.bmmgpu_debug_wave_stats.restype = ctypes.c_int
         L.bmmgpu_device_count.restype = ctypes.c_int

@@ -24,10 +24,14 @@
 // All passes are HBM-streaming XOR kernels: bytes moved, not XORs, bound them.
 #include <algorithm>
 #include <array>
+#include <atomic>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -1185,6 +1189,129 @@ int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_
     return kOk;
 }
 
+int dev_multiply_partial(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
+                         uint64_t ldc, uint64_t n, int algo, int dh, uint32_t first, uint32_t stride, int leaf_log2,
+                         int kernel, cudaStream_t s);
+int host_levels_for(uint64_t n, uint32_t parts, int e);
+
+namespace {
+// Host threads of one multi-device call meet here between phases; a failed thread still
+// arrives, so the others never wait forever.
+struct PhaseBarrier {
+    std::mutex mu;
+    std::condition_variable cv;
+    size_t parties, waiting = 0, gen = 0;
+    explicit PhaseBarrier(size_t n) : parties(n) {}
+    void wait() {
+        std::unique_lock<std::mutex> lk(mu);
+        const size_t g = gen;
+        if (++waiting == parties) {
+            waiting = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+}  // namespace
+
+// Fast GF(2) product on several devices (one host thread each): every device holds A and
+// Bt and computes the partial product of its share of the 7^dh host-layer sub-instances
+// (dev_multiply_partial, dealt round robin); then device g owns output-row slab g
+// (bmmgpu_slab_rows) and XOR-folds the other devices' partials of that slab, pulled by
+// peer copies over NVLink, before copying it home.  The only exchange is that fold:
+// (G - 1) / G of n^2 / 8 bytes in and out per device.
+int alt_multiply_multi(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, int dh,
+                       const std::vector<int>& phys, int kernel, int leaf_log2, double* timing_ms) {
+    const uint32_t G = uint32_t(phys.size());
+    const uint64_t w = n / 64, rows_bt = round_up(n, 256);
+    std::vector<uint64_t*> partial(G, nullptr);
+    std::vector<int> status(G, kOk);
+    std::vector<std::string> errors(G);
+    std::vector<float> ms(G, 0.f);
+    std::atomic<bool> failed{false};
+    PhaseBarrier bar(G);
+    void* stats = call_stats();
+    auto work = [&](uint32_t g) {
+        adopt_call_stats(stats);
+        int st = kOk;
+        StreamSet ss;
+        DevMem dA, dB, dBt, dC, tmp;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        uint64_t r0 = 0, r1 = 0;
+        auto fail = [&](int code) {
+            status[g] = code;
+            errors[g] = bmmgpu_last_error();
+            failed = true;
+        };
+        auto phase1 = [&]() -> int {
+            BMMGPU_CUDA_TRY(cudaSetDevice(phys[g]));
+            int r;
+            if ((r = ss.acquire(1))) return r;
+            const cudaStream_t s = ss[0];
+            if ((r = dA.alloc(n * w * 8, s)) || (r = dB.alloc(n * w * 8, s)) || (r = dBt.alloc(rows_bt * w * 8, s)) ||
+                (r = dC.alloc(n * w * 8, s)))
+                return r;
+            BMMGPU_CUDA_TRY(memcpy_counted(dA.p, A, n * w * 8, cudaMemcpyHostToDevice, s));
+            BMMGPU_CUDA_TRY(memcpy_counted(dB.p, B, n * w * 8, cudaMemcpyHostToDevice, s));
+            BMMGPU_CUDA_TRY(cudaEventCreate(&e0));
+            BMMGPU_CUDA_TRY(cudaEventCreate(&e1));
+            BMMGPU_CUDA_TRY(cudaEventRecord(e0, s));
+            if ((r = launch_transpose(dB.u(), w, n, n, dBt.u(), rows_bt, w, s))) return r;
+            dB.release();
+            if ((r = dev_multiply_partial(dA.u(), w, dBt.u(), w, dC.u(), w, n, algo, dh, g, G, leaf_log2, kernel, s)))
+                return r;
+            BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
+            partial[g] = dC.u();
+            return kOk;
+        };
+        auto phase2 = [&]() -> int {
+            const cudaStream_t s = ss[0];
+            bmmgpu_slab_rows(n, G, g, 64, &r0, &r1);
+            if (r1 > r0) {
+                int r;
+                if ((r = tmp.alloc((r1 - r0) * w * 8, s))) return r;
+                for (uint32_t d = 0; d < G; ++d) {
+                    if (d == g) continue;
+                    BMMGPU_CUDA_TRY(cudaMemcpyPeerAsync(tmp.p, phys[g], partial[d] + r0 * w, phys[d],
+                                                        (r1 - r0) * w * 8, s));
+                    if ((r = bmmgpu_dev_fold(dC.u() + r0 * w, w, tmp.u(), w, r1 - r0, w, BMMGPU_GF2_XOR_AND, s)))
+                        return r;
+                }
+            }
+            BMMGPU_CUDA_TRY(cudaEventRecord(e1, s));
+            if (r1 > r0)
+                BMMGPU_CUDA_TRY(memcpy2d_counted(C + r0 * w, w * 8, dC.u() + r0 * w, w * 8, w * 8, r1 - r0,
+                                                 cudaMemcpyDeviceToHost, s));
+            BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
+            cudaEventElapsedTime(&ms[g], e0, e1);
+            return kOk;
+        };
+        if ((st = phase1())) fail(st);
+        bar.wait();  // every partial is complete (or someone failed)
+        if (!failed && (st = phase2())) fail(st);
+        bar.wait();  // nobody reads this device's partial any more
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (ss.n) cudaStreamSynchronize(ss[0]);
+        adopt_call_stats(nullptr);
+    };
+    std::vector<std::thread> threads;
+    for (uint32_t g = 0; g < G; ++g) threads.emplace_back(work, g);
+    for (auto& t : threads) t.join();
+    float worst = 0.f;
+    for (uint32_t g = 0; g < G; ++g) {
+        if (status[g]) {
+            set_error("device " + std::to_string(phys[g]) + " (part " + std::to_string(g) + "): " + errors[g]);
+            return status[g];
+        }
+        worst = std::max(worst, ms[g]);
+    }
+    if (timing_ms) *timing_ms = worst;
+    return kOk;
+}
+
 int dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc, uint64_t n,
                  int algo, int leaf_log2, int kernel, cudaStream_t s) {
     if (n < 64 || (n & (n - 1))) {
@@ -1199,6 +1326,182 @@ int dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, uint64_t ldbt, uint6
     const int e = alt_levels(n, leaf_log2);
     if (e == 0) return launch_cubic(kernel, dA, lda, dBt, ldbt, dC, ldc, n, n, n / 64, true, false, s, 1, 0, 0, 0);
     return alt_multiply_device(dA, lda, dBt, ldbt, dC, ldc, n, algo, e, choose_serial_levels(n, e), kernel, s);
+}
+
+// ------------------------------------------------ host layer on devices
+// The top `dh` recursion levels as 7^dh independent sub-instances (reference pipeline
+// coordinate / generate_into / aggregate, pipeline.cpp:108-179, 198-369, and the paper's
+// Alg. 3): sub-instance h = (h_1 .. h_dh) multiplies
+//     T_h = sum_q prod_l M_A[h_l][q_l] A_q      S_h = sum_q prod_l M_B[h_l][q_l] Bt_q
+// (A_q: the sub-block of A at quadrant digits q = (q_1 .. q_dh), level 1 outermost), and
+// its product Q_h goes into every C sub-block q with prod_l G[q_l][h_l] = 1.  With the
+// basis changes folded into M_A = alpha.phi, M_B = beta.psi (Bt quadrant order) and
+// G = chi.gamma, as in alt_serial, this is alt_serial's top dh levels flattened, so any
+// subset of sub-instances gives an exact partial product and the XOR of the partials of
+// a partition of the 7^dh sub-instances is A.B.  Sub-instances dealt to devices or ranks
+// need no exchange until that final XOR.
+namespace {
+
+constexpr int kMaxHostLevels = 4;  // 4^4 source sub-blocks per generated operand
+struct BlockList {
+    uint64_t off[1 << (2 * kMaxHostLevels)];  // word offsets of the selected sub-blocks
+    uint32_t count;
+};
+
+// out = XOR of the listed sub-blocks of `in` (ls rows x ws words each, row stride ld_in).
+template <int V>
+__global__ void __launch_bounds__(256) gather_xor_kernel(const uint64_t* __restrict__ in, uint64_t ld_in,
+                                                         uint64_t total, uint32_t sh_wv, BlockList blocks,
+                                                         uint64_t* __restrict__ out, uint64_t ld_out) {
+    using W = Words<V>;
+    using T = typename W::T;
+    for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t w = (idx & ((1ull << sh_wv) - 1)) * V, r = idx >> sh_wv;
+        const uint64_t* base = in + r * ld_in + w;
+        T v = W::zero();
+        for (uint32_t i = 0; i < blocks.count; ++i) v = W::x(v, *reinterpret_cast<const T*>(base + blocks.off[i]));
+        *reinterpret_cast<T*>(out + r * ld_out + w) = v;
+    }
+}
+
+// every listed sub-block of C ^= q_in (distinct targets: no two threads touch one word).
+template <int V>
+__global__ void __launch_bounds__(256) scatter_list_kernel(const uint64_t* __restrict__ q_in, uint64_t ld_q,
+                                                           uint64_t total, uint32_t sh_wv, BlockList blocks,
+                                                           uint64_t* C, uint64_t ldc) {
+    using W = Words<V>;
+    using T = typename W::T;
+    for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t w = (idx & ((1ull << sh_wv) - 1)) * V, r = idx >> sh_wv;
+        const T v = *reinterpret_cast<const T*>(q_in + r * ld_q + w);
+        uint64_t* base = C + r * ldc + w;
+        for (uint32_t i = 0; i < blocks.count; ++i) {
+            T* p = reinterpret_cast<T*>(base + blocks.off[i]);
+            *p = W::x(*p, v);
+        }
+    }
+}
+
+// Offsets of the sub-blocks q = (q_1 .. q_dh) with prod_l bit(coef(l, q_l)) = 1, for a
+// matrix of n rows and row stride ld: sub-block rows = n >> dh.
+template <class Coef>
+BlockList block_list(int dh, uint64_t n, uint64_t ld, Coef coef) {
+    BlockList b{};
+    const uint64_t ls = n >> dh;
+    for (uint32_t q = 0; q < (1u << (2 * dh)); ++q) {
+        bool on = true;
+        uint64_t br = 0, bc = 0;
+        for (int l = 0; l < dh && on; ++l) {
+            const uint32_t ql = (q >> (2 * (dh - 1 - l))) & 3;  // level l + 1, outermost first
+            on = coef(l, ql);
+            br = 2 * br + (ql >> 1);
+            bc = 2 * bc + (ql & 1);
+        }
+        if (on) b.off[b.count++] = br * ls * ld + bc * (ls / 64);
+    }
+    return b;
+}
+
+int launch_block_list(bool scatter, const uint64_t* src, uint64_t ld_src, uint64_t* dst, uint64_t ld_dst,
+                      uint64_t ls, const BlockList& b, cudaStream_t s) {
+    const uint64_t ws = ls / 64;
+    bool v2 = ws % 2 == 0 && ld_src % 2 == 0 && ld_dst % 2 == 0 && aligned16(src) && aligned16(dst);
+    for (uint32_t i = 0; i < b.count; ++i) v2 = v2 && b.off[i] % 2 == 0;
+    const int V = v2 ? 2 : 1;
+    const uint64_t total = ls * (ws / V);
+    const uint32_t sh = uint32_t(__builtin_ctzll(ws / V));
+    if (scatter) {
+        if (!b.count) return kOk;
+        if (V == 2)
+            scatter_list_kernel<2><<<grid_for(total), 256, 0, s>>>(src, ld_src, total, sh, b, dst, ld_dst);
+        else
+            scatter_list_kernel<1><<<grid_for(total), 256, 0, s>>>(src, ld_src, total, sh, b, dst, ld_dst);
+    } else if (V == 2) {
+        gather_xor_kernel<2><<<grid_for(total), 256, 0, s>>>(src, ld_src, total, sh, b, dst, ld_dst);
+    } else {
+        gather_xor_kernel<1><<<grid_for(total), 256, 0, s>>>(src, ld_src, total, sh, b, dst, ld_dst);
+    }
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaGetLastError());
+    return kOk;
+}
+
+}  // namespace
+
+// Recursion levels of the host layer for n on `parts` devices / ranks when the caller
+// does not fix them: the smallest dh whose deal is within 3 % of even (ceil(7^dh / parts)
+// sub-instances on the busiest part against 7^dh / parts), keeping sub-instances of at
+// least 2^13 (the fast product's own leaves stay at 4096) and at least one level below.
+int host_levels_for(uint64_t n, uint32_t parts, int e) {
+    if (parts <= 1) return 0;
+    int best = 1;
+    for (int dh = 1; dh <= kMaxHostLevels && dh < e && (n >> dh) >= 8192; ++dh) {
+        uint64_t subs = 1;
+        for (int l = 0; l < dh; ++l) subs *= 7;
+        best = dh;
+        if (double((subs + parts - 1) / parts) <= 1.03 * double(subs) / parts) break;
+    }
+    return best;
+}
+
+// dC = the XOR of sub-instances first, first + stride, ... of the top dh levels
+// (see above).  dA / dBt are only read; dC (n x n/64, stride ldc) is overwritten.
+int dev_multiply_partial(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
+                         uint64_t ldc, uint64_t n, int algo, int dh, uint32_t first, uint32_t stride, int leaf_log2,
+                         int kernel, cudaStream_t s) {
+    const Scheme* sc = scheme_for(algo);
+    if (!sc) {
+        set_error("no bilinear scheme for this algorithm");
+        return kEinval;
+    }
+    if (n < 64 || (n & (n - 1))) {
+        set_error("fast algorithms need n = 64 * 2^k");
+        return kEshape;
+    }
+    if (stride == 0 || first >= stride) {
+        set_error("partial product: need 0 <= first < stride");
+        return kEinval;
+    }
+    kernel = resolve_kernel(kernel);
+    const int e = alt_levels(n, leaf_log2);
+    if (dh < 0 || dh > kMaxHostLevels || (dh > 0 && dh > e - 1)) {
+        set_error("partial product: host levels must leave at least one recursion level below them (and <= 4)");
+        return kEinval;
+    }
+    BMMGPU_CUDA_TRY(cudaMemset2DAsync(dC, ldc * 8, 0, (n / 64) * 8, n, s));
+    count_launch();
+    if (dh == 0) {
+        if (first != 0) return kOk;  // one sub-instance: the whole product
+        if (e == 0) return launch_cubic(kernel, dA, lda, dBt, ldbt, dC, ldc, n, n, n / 64, true, false, s, 1, 0, 0, 0);
+        return alt_multiply_device(dA, lda, dBt, ldbt, dC, ldc, n, algo, e, choose_serial_levels(n, e), kernel, s);
+    }
+    const Masks7 ma = fused_expand(sc->alpha, sc->phi, sc->n_phi, false);
+    const Masks7 mb = fused_expand(sc->beta, sc->psi, sc->n_psi, true);
+    const Masks4 mg = fused_compress(sc);
+    uint64_t subs = 1;
+    for (int l = 0; l < dh; ++l) subs *= 7;
+    const uint64_t ls = n >> dh, lw = ls / 64;
+    const int e_sub = e - dh;
+    int st;
+    DevMem T, S, Q;
+    if ((st = T.alloc(ls * lw * 8, s)) || (st = S.alloc(ls * lw * 8, s)) || (st = Q.alloc(ls * lw * 8, s))) return st;
+    const int e_serial = choose_serial_levels(ls, e_sub);
+    for (uint64_t i = first; i < subs; i += stride) {
+        int h[kMaxHostLevels];
+        uint64_t r = i;
+        for (int l = dh - 1; l >= 0; --l, r /= 7) h[l] = int(r % 7);
+        const BlockList la = block_list(dh, n, lda, [&](int l, uint32_t q) { return (ma.m[h[l]] >> q) & 1; });
+        const BlockList lb = block_list(dh, n, ldbt, [&](int l, uint32_t q) { return (mb.m[h[l]] >> q) & 1; });
+        const BlockList lc = block_list(dh, n, ldc, [&](int l, uint32_t q) { return (mg.m[q] >> h[l]) & 1; });
+        if ((st = launch_block_list(false, dA, lda, T.u(), lw, ls, la, s)) ||
+            (st = launch_block_list(false, dBt, ldbt, S.u(), lw, ls, lb, s)) ||
+            (st = alt_multiply_device(T.u(), lw, S.u(), lw, Q.u(), lw, ls, algo, e_sub, e_serial, kernel, s)) ||
+            (st = launch_block_list(true, Q.u(), lw, dC, ldc, ls, lc, s)))
+            return st;
+    }
+    return kOk;
 }
 
 // ------------------------------------------------ interleaved basis change (K4)
@@ -1476,6 +1779,19 @@ extern "C" int bmmgpu_dev_multiply(uint64_t* dA, uint64_t lda, uint64_t* dBt, ui
                                    void* stream) {
     return bmmgpu::dev_multiply(dA, lda, dBt, ldbt, dC, ldc, n, algo, leaf_log2, kernel,
                                 static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int bmmgpu_dev_multiply_partial(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt,
+                                           uint64_t* dC, uint64_t ldc, uint64_t n, int32_t algo, int32_t host_levels,
+                                           uint32_t first, uint32_t stride, int32_t leaf_log2, int32_t kernel,
+                                           void* stream) {
+    return bmmgpu::dev_multiply_partial(dA, lda, dBt, ldbt, dC, ldc, n, algo, host_levels, first, stride, leaf_log2,
+                                        kernel, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int bmmgpu_host_levels(uint64_t n, uint32_t parts, int32_t leaf_log2) {
+    const int e = bmmgpu::alt_levels(n, leaf_log2);
+    return std::max(0, std::min({bmmgpu::host_levels_for(n, parts, e), 4, e - 1}));
 }
 
 extern "C" int bmmgpu_multiply_alt(const uint64_t* a_hat, const uint64_t* b_hat, uint64_t* c_hat, int32_t depth,

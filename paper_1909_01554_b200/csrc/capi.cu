@@ -36,6 +36,10 @@ int alt_multiply_host(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_
 int stream_kouter_slab(int device, uint64_t row_begin, uint64_t row_end, const uint64_t* A, const uint64_t* B,
                        uint64_t* C, uint64_t k, uint64_t n, bool gf2, int kernel, bool accumulate, uint64_t budget,
                        float* ms_out, int chunks);
+int alt_multiply_multi(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, int dh,
+                       const std::vector<int>& phys, int kernel, int leaf_log2, double* timing_ms);
+int host_levels_for(uint64_t n, uint32_t parts, int e);
+int alt_levels(uint64_t n, int leaf_log2);
 int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const uint64_t* A, const uint64_t* B,
                       uint64_t* C, uint64_t k, uint64_t n, bool gf2, int kernel, bool accumulate, uint64_t budget,
                       float* ms_out);
@@ -464,6 +468,10 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
     return kOk;
 }
 
+// Devices named by a device_mask.  Test hook: BMMGPU_LOGICAL_DEVICES=k makes k logical
+// devices, bit g running on physical device g % count, so the multi-device drivers
+// (one host thread and one set of buffers per logical device, peer copies between
+// them) run on a one-GPU box.
 std::vector<int> devices_of(uint32_t mask, int* status) {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
@@ -474,10 +482,12 @@ std::vector<int> devices_of(uint32_t mask, int* status) {
         *status = kEnodev;
         return devs;
     }
+    const int physical = count;
+    if (const char* lg = getenv("BMMGPU_LOGICAL_DEVICES")) count = std::max(1, std::min(32, atoi(lg)));
     if (mask == 0) mask = 1;
     for (int g = 0; g < 32 && g < count; ++g)
-        if (mask & (1u << g)) devs.push_back(g);
-    if (devs.empty() || (mask >> std::min(count, 31)) > 0) {
+        if (mask & (1u << g)) devs.push_back(g % physical);
+    if (devs.empty() || (count < 32 && (mask >> count) > 0)) {
         set_error("device_mask selects devices that do not exist");
         *status = kEinval;
         devs.clear();
@@ -742,6 +752,15 @@ int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t 
     std::vector<int> devs = devices_of(o.device_mask, &st);
     if (st) return st;
     BMMGPU_CUDA_TRY(cudaSetDevice(devs[0]));
+    if (devs.size() > 1) {
+        // several devices: the top host levels of the recursion are dealt across them
+        // (plan.d_host when the caller sets it, else the most even deal), and the partial
+        // products are XOR-folded slab by slab (alt_multiply_multi)
+        const int e = alt_levels(n, o.leaf_log2);
+        const int dh = plan->d_host > 0 ? std::max(0, std::min({int(plan->d_host), 4, e - 1}))
+                                        : bmmgpu_host_levels(n, uint32_t(devs.size()), o.leaf_log2);
+        return alt_multiply_multi(A, B, C, n, algo, dh, devs, o.kernel, o.leaf_log2, o.timing_ms);
+    }
     return alt_multiply_host(A, B, C, n, algo, plan, o.kernel, o.leaf_log2, o.timing_ms);
 }
 

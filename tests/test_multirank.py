@@ -1,6 +1,7 @@
 """CPU, world_size 2 over gloo: the multi-rank plumbing bench.py uses for
-N GPUs (one process per GPU, output-row slabs, no data exchange, max-over-ranks
-timing) and the slab partition rule of the C ABI."""
+N GPUs (one process per GPU, output-row slabs, max-over-ranks timing), the slab
+partition rule of the C ABI, and the fast product's one exchange step (all-to-all
+of row slabs + XOR fold of the partial products)."""
 from __future__ import annotations
 
 import os
@@ -36,6 +37,55 @@ def _worker(rank: int, world: int, port: int, n: int, q) -> None:
     if rank == 0:
         q.put((spans, t))
     d.close()
+
+
+def _exchange_worker(rank: int, world: int, port: int, q) -> None:
+    import sys
+    sys.path.insert(0, str(ROOT))
+    os.environ.update({"RANK": str(rank), "LOCAL_RANK": str(rank), "WORLD_SIZE": str(world),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import torch
+    import bench
+    d = bench.Dist()
+    n, w = 1280, 3
+    slabs = [bench.shard_rows(n, r, world, 256) for r in range(world)]
+    g = torch.Generator().manual_seed(100 + rank)
+    P = torch.randint(-2**62, 2**62, (n, w), dtype=torch.int64, generator=g)  # this rank's partial product
+    r0, r1 = slabs[rank]
+    R = torch.empty((world * (r1 - r0), w), dtype=torch.int64)
+
+    def fold(k):
+        R[: r1 - r0] ^= R[k * (r1 - r0):(k + 1) * (r1 - r0)]
+    bench.slab_exchange_xor(P, R, slabs, rank, world, True, fold)
+    q.put((rank, r0, r1, R[: r1 - r0].clone()))
+    d.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partial_products_exchange_and_fold(world):
+    """The multi-rank fast product's exchange step on CPU over gloo: after the all-to-all of
+    row slabs and the XOR fold, rank r holds slab r of the XOR of every rank's partial."""
+    import torch
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, w = 1280, 3
+    total = torch.zeros((n, w), dtype=torch.int64)
+    for r in range(world):
+        g = torch.Generator().manual_seed(100 + r)
+        total ^= torch.randint(-2**62, 2**62, (n, w), dtype=torch.int64, generator=g)
+    covered = 0
+    for rank, r0, r1, slab in got:
+        assert torch.equal(slab, total[r0:r1]), rank
+        covered += r1 - r0
+    assert covered == n
 
 
 @pytest.mark.parametrize("world,n", [(2, 131072), (2, 1000), (2, 256)])
@@ -90,10 +140,11 @@ def test_bench_two_ranks_share_one_gpu():
 
 
 @pytest.mark.gpu
-def test_alt_tile_partition_two_ranks():
-    """The multi-GPU fast product (4 x 4 output tiles, each the XOR of 4 alt-basis block
-    products, round robin over ranks): two ranks sharing one GPU, every tile of rank 0
-    checked against the tensor-core cubic product."""
+def test_alt_subinstance_deal_two_ranks():
+    """The multi-GPU fast product (host-layer sub-instances dealt round robin over ranks,
+    partial products XOR-folded after one all-to-all of output-row slabs): two ranks
+    sharing one GPU, every rank's slab checked against the tensor-core cubic product and
+    by Freivalds."""
     import json
     import os
     import subprocess
@@ -101,11 +152,12 @@ def test_alt_tile_partition_two_ranks():
     env = dict(os.environ, BMM_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2", "--workload",
-           "c4s-gf2-altsi-16384", "--leaf-log2", "9", "--steps", "3", "--warmup", "3", "--check"]
+           "c4s-gf2-altsi-16384", "--leaf-log2", "9", "--steps", "3", "--warmup", "3"]
     r = subprocess.run(cmd, cwd=str(ROOT), env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
-    assert d["n_gpus"] == 2 and d["config"]["tiles_per_rank0"] == 8 and d["tiles_checked_rank0"] == 8
+    assert d["n_gpus"] == 2 and d["config"]["host_levels"] == 1 and d["config"]["subinstances_rank0"] == 4
+    assert d["parity"]["ok"] is True and d["parity"]["slab_equals_cubic_product"] is True
     assert d["value"] > 0 and d["gpu_launches"] > 0
 
 

@@ -18,7 +18,7 @@ for v in 2 0 1; do
   cp build/variants/libbmmgpu_pack16_$v.so paper_1909_01554_b200/libbmmgpu.so
   n=30; [ $v = 2 ] && n=50
   for i in $(seq 1 $n); do
-    timeout 150 python -m pytest tests/test_multirank.py -q -m gpu -k alt_tile_partition 2>&1 | tail -1
+    timeout 150 python -m pytest tests/test_multirank.py -q -m gpu -k alt_subinstance_deal 2>&1 | tail -1
   done > gpurun_out/race_twoproc_v$v.txt
 done
 cp /tmp/orig.so paper_1909_01554_b200/libbmmgpu.so
