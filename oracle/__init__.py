@@ -159,6 +159,7 @@ class Reference:
         L.bmmref_from_interleaved.argtypes = [_i32, _i32, _vp, _vp]
         L.bmmref_basis_change.argtypes = [_vp, _i32, _i32, _i32]
         L.bmmref_multiply_alt.argtypes = [_vp, _vp, _vp, _i32, _i32, _i32, _i32]
+        L.bmmref_coordinate.argtypes = [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]
         L.bmmref_kernel64.argtypes = [_vp, _vp, _vp, _i32]
         L.bmmref_kernel64.restype = None
         L.bmmref_predicted_additions.argtypes = [_i32, _i32, _i32]
@@ -188,6 +189,13 @@ class Reference:
         cnt = np.zeros(4, dtype=np.uint64)
         self._ok(self.L.bmmref_multiply(_p(a), _p(b), _p(c), n, algo, d_host, d_serial, d_parallel, workers, ring,
                                         _p(cnt) if counts else None))
+        return (c, cnt) if counts else c
+
+    def coordinate(self, a_hat, b_hat, d_host, d_serial, d_parallel, workers=1, scheme=1, counts=False):
+        c = np.zeros_like(a_hat)
+        cnt = np.zeros(4, dtype=np.uint64)
+        self._ok(self.L.bmmref_coordinate(_p(a_hat), _p(b_hat), _p(c), d_host, d_serial, d_parallel, workers, scheme,
+                                          _p(cnt) if counts else None))
         return (c, cnt) if counts else c
 
     def kernel64(self, a, bt, ring):

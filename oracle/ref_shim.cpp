@@ -15,6 +15,7 @@
 #include "bmm/counter.hpp"
 #include "bmm/decomposition.hpp"
 #include "bmm/engine.hpp"
+#include "bmm/pipeline.hpp"
 #include "bmm/plan.hpp"
 
 using namespace bmm;
@@ -177,6 +178,37 @@ int bmmref_multiply_alt(const std::uint64_t* a_hat, const std::uint64_t* b_hat, 
         b.words.assign(b_hat, b_hat + words);
         BitVectorTensor c = multiply_alt(a, b, d, plan);
         std::memcpy(c_hat, c.words.data(), words * 8);
+    });
+}
+
+// pipeline::coordinate (pipeline.cpp:198-369) on hat vectors of depth d_host + d_serial +
+// d_parallel; counts: optional [ands, xors, ors, kernels]
+int bmmref_coordinate(const std::uint64_t* a_hat, const std::uint64_t* b_hat, std::uint64_t* c_hat, int d_host,
+                      int d_serial, int d_parallel, int workers, int scheme, std::uint64_t* counts) {
+    return guard([&] {
+        const Decomposition& d = builtin(static_cast<Builtin>(scheme));
+        LayerPlan plan;
+        plan.d_host = d_host;
+        plan.d_serial = d_serial;
+        plan.d_parallel = d_parallel;
+        plan.workers = 1;
+        const int depth = d_host + d_serial + d_parallel;
+        const std::uint64_t words = (std::uint64_t{64} << depth) * (std::uint64_t{64} << depth) / 64;
+        BitVectorTensor a, b;
+        a.mode_lengths.assign(depth, 4);
+        a.mode_lengths.push_back(kBlockBits);
+        b.mode_lengths = a.mode_lengths;
+        a.words.assign(a_hat, a_hat + words);
+        b.words.assign(b_hat, b_hat + words);
+        OpCounter ctr;
+        BitVectorTensor c = pipeline::coordinate(a, b, d, plan, workers, counts ? &ctr : nullptr);
+        std::memcpy(c_hat, c.words.data(), words * 8);
+        if (counts) {
+            counts[0] = ctr.word_ands;
+            counts[1] = ctr.word_xors;
+            counts[2] = ctr.word_ors;
+            counts[3] = ctr.kernel_invocations;
+        }
     });
 }
 

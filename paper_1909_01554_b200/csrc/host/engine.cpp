@@ -4,6 +4,7 @@
 // OpCounter tallies are filled with the reference algorithm's exact counts.
 #include "bmm/engine.hpp"
 
+#include <algorithm>
 #include <bit>
 #include <stdexcept>
 #include <string>
@@ -219,8 +220,16 @@ BitMatrix multiply(const BitMatrix& a, const BitMatrix& b, Algo algo, const Laye
     const Decomposition& d = decomposition_for(algo);
     BitMatrix c = BitMatrix::zeros(a.rows, a.rows);
     bmmgpu_plan gp{plan.d_host, plan.d_serial, plan.d_parallel, plan.d_inner, plan.workers};
+    // With host levels the reference runs pipeline::coordinate with plan.workers emulated
+    // accelerators (engine.cpp:375-378); here the workers are GPUs: the host-layer
+    // sub-instances are dealt over min(workers, devices) of them (bmmgpu_multiply).
+    bmmgpu_opts opts{};
+    if (plan.d_host > 0) {
+        const int g = std::max(1, std::min(plan.workers, bmmgpu_device_count()));
+        opts.device_mask = g >= 32 ? 0xffffffffu : (1u << g) - 1;
+    }
     check(bmmgpu_multiply(a.words.data(), b.words.data(), c.words.data(), a.rows, algo_id(d.which), &gp,
-                          BMMGPU_GF2_XOR_AND, nullptr));
+                          BMMGPU_GF2_XOR_AND, &opts));
     if (counter) {
         const int depth = plan.depth();
         const std::uint64_t kernels = ipow(7, depth);

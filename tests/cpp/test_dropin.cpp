@@ -310,6 +310,53 @@ void pipeline_gpu_cases() {
         CHECK(multiply(a, b, Algo::AltChaining, p2, Semiring::Gf2XorAnd) == want);
         CHECK(multiply(a, b, Algo::StrassenWinograd, p3, Semiring::Gf2XorAnd) == want);
     });
+    run("pipeline::coordinate reproduces the reference's coordinate: outputs and counters", [] {
+        // golden.json "coordinate" (tests/golden/make_golden.py): the UNMODIFIED reference
+        // pipeline::coordinate (oracle/_ref) on random hat vectors; FNV-1a 64 of the words,
+        // popcount, first word, [ands, xors, ors, kernels]
+        struct Case {
+            Builtin scheme;
+            int dh, ds, dp;
+            std::uint64_t sa, sb;
+            int workers;
+            std::uint64_t fnv, pop, w0, ands, xors, kernels;
+        };
+        const Case cases[] = {
+            {Builtin::AltSelfInverse, 1, 1, 1, 91, 92, 2, 0x7f4f81e0a1b8fd5dull, 131116, 0x83504072ff41a65cull,
+             1404928, 75520, 343},
+            {Builtin::AltSelfInverse, 2, 0, 1, 93, 94, 3, 0x98f5af40a0eac06dull, 131043, 0x923ca9d89b861ecfull,
+             1404928, 89344, 343},
+            {Builtin::AltChaining, 2, 1, 1, 95, 96, 4, 0xa8c1d735a31de502ull, 523824, 0xa3ba6ca3a933ad6eull,
+             9834496, 665856, 2401},
+            {Builtin::StrassenWinograd, 1, 0, 2, 97, 98, 2, 0x3f02636b72614b94ull, 130888, 0x834f9b39d59c6636ull,
+             1404928, 102592, 343},
+        };
+        for (const Case& k : cases) {
+            const int depth = k.dh + k.ds + k.dp;
+            const std::uint64_t n = std::uint64_t(64) << depth;
+            std::vector<std::uint64_t> modes(depth, 4);
+            modes.push_back(kBlockBits);
+            BitVectorTensor a, b;
+            a.mode_lengths = b.mode_lengths = modes;
+            a.words = BitMatrix::random(1, n * n, k.sa).words;
+            b.words = BitMatrix::random(1, n * n, k.sb).words;
+            OpCounter c;
+            pipeline::PipelineStats st;
+            const BitVectorTensor got =
+                pipeline::coordinate(a, b, builtin(k.scheme), plan_for(k.ds, k.dp, k.dh), k.workers, &c, &st);
+            std::uint64_t h = 0xcbf29ce484222325ull, pop = 0;
+            for (std::uint64_t w : got.words) {
+                pop += std::popcount(w);
+                for (int i = 0; i < 8; ++i) h = (h ^ ((w >> (8 * i)) & 0xff)) * 0x100000001b3ull;
+            }
+            CHECK(h == k.fnv && pop == k.pop && got.words[0] == k.w0);
+            CHECK(c.word_ands == k.ands && c.word_xors == k.xors && c.word_ors == 0 && c.kernel_invocations == k.kernels);
+            bool once = st.lock_violations == 0;
+            for (auto v : {&st.prepared_left, &st.prepared_right, &st.aggregated})
+                for (auto x : *v) once = once && x == 1;
+            CHECK(once);
+        }
+    });
     run("multiply: OpCounter tallies with host levels equal the reference's", [] {
         // expected [word_xors] of the UNMODIFIED reference multiply at n = 512 (depth 3), read
         // from oracle/_ref (bmmref_multiply with counts); d_host > 0 goes through its

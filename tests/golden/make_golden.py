@@ -136,6 +136,18 @@ def main() -> None:
         C["multiply_alt"].append({"d_serial": ds, "d_parallel": dp, "a_seed": sa, "b_seed": sb, "scheme": scheme,
                                   **digest(c)})
 
+    # pipeline::coordinate (the host layer) on hat vectors: outputs and op counts
+    C["coordinate"] = []
+    for scheme, dh, ds, dp, sa, sb, workers in [(1, 1, 1, 1, 91, 92, 2), (1, 2, 0, 1, 93, 94, 3),
+                                                (2, 2, 1, 1, 95, 96, 4), (0, 1, 0, 2, 97, 98, 2)]:
+        depth = dh + ds + dp
+        n = 64 << depth
+        ah = ref.random(1, n * n, sa)
+        bh = ref.random(1, n * n, sb)
+        c, cnt = ref.coordinate(ah, bh, dh, ds, dp, workers, scheme, counts=True)
+        C["coordinate"].append({"d_host": dh, "d_serial": ds, "d_parallel": dp, "a_seed": sa, "b_seed": sb,
+                                "scheme": scheme, "workers": workers, "counts": [int(x) for x in cnt], **digest(c)})
+
     C["predicted_additions"] = []
     for scheme in (0, 1, 2):
         for depth in (1, 2, 3, 4):
