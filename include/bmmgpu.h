@@ -27,6 +27,7 @@ extern "C" {
 #define BMMGPU_OK 0
 #define BMMGPU_EINVAL 1
 #define BMMGPU_ESHAPE 3
+#define BMMGPU_EFORMAT 4 /* malformed BMM1 file -> bmm::FormatError */
 #define BMMGPU_ECUDA 5
 #define BMMGPU_ENODEV 6
 
@@ -110,6 +111,16 @@ int bmmgpu_multiply_alt(const uint64_t* a_hat, const uint64_t* b_hat, uint64_t* 
  * yates.cpp:143-172). */
 int bmmgpu_basis_change(uint64_t* words, uint64_t total_words, int32_t levels, int32_t algo, int32_t factor,
                         int32_t inverse);
+
+/* BMM1 files (reference bitmatrix.cpp:187-233: "BMM1", rows, cols as LE u64, then
+ * rows * ceil(cols/64) LE words) straight between disk and caller storage with parallel
+ * positioned I/O (`threads` <= 0: one per host core).  Read into page-locked memory
+ * (bmmgpu_host_alloc) the matrix goes to the GPU without a staging copy.  Same checks
+ * and messages as the reference reader; malformed files give BMMGPU_EFORMAT.
+ * bmmgpu_bmm1_read needs n_words == rows * ceil(cols/64) of the file. */
+int bmmgpu_bmm1_info(const char* path, uint64_t* rows, uint64_t* cols);
+int bmmgpu_bmm1_read(const char* path, uint64_t* words, uint64_t n_words, int32_t threads);
+int bmmgpu_bmm1_write(const char* path, uint64_t rows, uint64_t cols, const uint64_t* words, int32_t threads);
 
 /* -------------------------------------------------------- device-resident API
  * Pointers are device memory on the current CUDA device; `stream` is a

@@ -159,6 +159,8 @@ class Reference:
         L.bmmref_from_interleaved.argtypes = [_i32, _i32, _vp, _vp]
         L.bmmref_basis_change.argtypes = [_vp, _i32, _i32, _i32]
         L.bmmref_multiply_alt.argtypes = [_vp, _vp, _vp, _i32, _i32, _i32, _i32]
+        L.bmmref_read_bmm1.argtypes = [ctypes.c_char_p, _vp, _vp, _vp]
+        L.bmmref_write_bmm1.argtypes = [ctypes.c_char_p, _u64, _u64, _vp]
         L.bmmref_coordinate.argtypes = [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]
         L.bmmref_kernel64.argtypes = [_vp, _vp, _vp, _i32]
         L.bmmref_kernel64.restype = None
@@ -190,6 +192,16 @@ class Reference:
         self._ok(self.L.bmmref_multiply(_p(a), _p(b), _p(c), n, algo, d_host, d_serial, d_parallel, workers, ring,
                                         _p(cnt) if counts else None))
         return (c, cnt) if counts else c
+
+    def read_bmm1(self, path: str):
+        rows, cols = ctypes.c_uint64(), ctypes.c_uint64()
+        self._ok(self.L.bmmref_read_bmm1(path.encode(), ctypes.byref(rows), ctypes.byref(cols), None))
+        w = np.zeros(rows.value * ((cols.value + 63) // 64), dtype=np.uint64)
+        self._ok(self.L.bmmref_read_bmm1(path.encode(), ctypes.byref(rows), ctypes.byref(cols), _p(w)))
+        return rows.value, cols.value, w
+
+    def write_bmm1(self, path: str, rows: int, cols: int, words: np.ndarray) -> None:
+        self._ok(self.L.bmmref_write_bmm1(path.encode(), rows, cols, _p(words)))
 
     def coordinate(self, a_hat, b_hat, d_host, d_serial, d_parallel, workers=1, scheme=1, counts=False):
         c = np.zeros_like(a_hat)

@@ -23,7 +23,7 @@ HOST_LIB_PATH = _HERE / "libbmm_b200.so"
 
 __all__ = [
     "Semiring", "Algo", "Kernel", "LayerPlan", "BitMatrix", "ShapeError", "FormatError", "EngineError",
-    "multiply_cubic", "multiply", "lib", "device_count", "granularity",
+    "multiply_cubic", "multiply", "lib", "device_count", "granularity", "read_bmm1", "write_bmm1", "PinnedWords",
 ]
 
 
@@ -109,6 +109,16 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_dev_multiply_partial.restype = ctypes.c_int
         L.bmmgpu_host_levels.argtypes = [u64, ctypes.c_uint32, i32]
         L.bmmgpu_host_levels.restype = ctypes.c_int
+        L.bmmgpu_bmm1_info.argtypes = [ctypes.c_char_p, _u64p, _u64p]
+        L.bmmgpu_bmm1_info.restype = ctypes.c_int
+        L.bmmgpu_bmm1_read.argtypes = [ctypes.c_char_p, vp, u64, i32]
+        L.bmmgpu_bmm1_read.restype = ctypes.c_int
+        L.bmmgpu_bmm1_write.argtypes = [ctypes.c_char_p, u64, u64, vp, i32]
+        L.bmmgpu_bmm1_write.restype = ctypes.c_int
+        L.bmmgpu_host_alloc.argtypes = [u64, ctypes.POINTER(ctypes.c_void_p)]
+        L.bmmgpu_host_alloc.restype = ctypes.c_int
+        L.bmmgpu_host_free.argtypes = [vp]
+        L.bmmgpu_host_free.restype = ctypes.c_int
         L.bmmgpu_debug_wave_stats.argtypes = [_u64p, _u64p]
         L.bmmgpu_debug_wave_stats.restype = ctypes.c_int
         L.bmmgpu_device_count.restype = ctypes.c_int
@@ -127,6 +137,8 @@ def _check(status: int) -> None:
     msg = lib().bmmgpu_last_error().decode(errors="replace")
     if status == 3:
         raise ShapeError(msg)
+    if status == 4:
+        raise FormatError(msg)
     if status == 1:
         raise ValueError(msg)  # std::invalid_argument
     raise EngineError(msg)
@@ -218,6 +230,50 @@ class BitMatrix:
     def __eq__(self, other: object) -> bool:
         return (isinstance(other, BitMatrix) and self.rows == other.rows and self.cols == other.cols
                 and np.array_equal(self.words, other.words))
+
+
+def read_bmm1(path: str, out: np.ndarray | None = None, threads: int = 0) -> BitMatrix:
+    """bmm::read_bmm1 (reference bitmatrix.cpp:187-233): the same checks and messages
+    (FormatError), read with parallel positioned I/O straight into `out` when given (e.g.
+    page-locked memory from `pinned_words`, so the words go to the GPU without a copy)."""
+    rows, cols = ctypes.c_uint64(), ctypes.c_uint64()
+    L = lib()
+    if L.bmmgpu_bmm1_info(str(path).encode(), ctypes.byref(rows), ctypes.byref(cols)) != 0:
+        raise FormatError(L.bmmgpu_last_error().decode())
+    n = rows.value * ((cols.value + 63) // 64)
+    words = np.zeros(n, dtype=np.uint64) if out is None else out[:n]
+    if words.size != n or not words.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"destination needs {n} contiguous words")
+    _check(L.bmmgpu_bmm1_read(str(path).encode(), words.ctypes.data, n, threads))
+    return BitMatrix(rows.value, cols.value, words)
+
+
+def write_bmm1(m: BitMatrix, path: str, threads: int = 0) -> None:
+    """bmm::write_bmm1 (reference bitmatrix.cpp:218-233), parallel positioned writes."""
+    L = lib()
+    _check(L.bmmgpu_bmm1_write(str(path).encode(), m.rows, m.cols, m.words.ctypes.data, threads))
+
+
+class PinnedWords:
+    """Page-locked host words (bmmgpu_host_alloc): `.words` is a numpy view; free() or
+    garbage collection releases them."""
+
+    def __init__(self, n: int) -> None:
+        self._p = ctypes.c_void_p()
+        _check(lib().bmmgpu_host_alloc(max(8, 8 * n), ctypes.byref(self._p)))
+        self.words = np.ctypeslib.as_array((ctypes.c_uint64 * max(1, n)).from_address(self._p.value))[:n]
+
+    def free(self) -> None:
+        if self._p.value:
+            self.words = None
+            lib().bmmgpu_host_free(self._p)
+            self._p = ctypes.c_void_p()
+
+    def __del__(self) -> None:
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 _host_lib: ctypes.CDLL | None = None

@@ -322,6 +322,9 @@ __device__ __forceinline__ void drain_accumulator2(uint32_t tbase, uint32_t (&wo
 #ifndef BMMGPU_GF2_PACK16
 #define BMMGPU_GF2_PACK16 2  // 0 off; 1 Bt-permuted (fails the two-process tile test intermittently); 2 drain-only
 #endif
+#ifndef BMMGPU_GF2_DRAIN_COLS
+#define BMMGPU_GF2_DRAIN_COLS 32  // columns per .pack::16b TMEM load of the GF(2) drain: 32 or 64
+#endif
 // Output column o of a 32-column group sits at accumulator column 2o (o < 16) or
 // 2(o - 16) + 1.  Expander thread t of the group takes Bt row rho(t) so that both its
 // packed-ring reads (row rho & 7) and its operand stores (slot & 7) stay distinct across
@@ -376,6 +379,35 @@ __device__ __forceinline__ void drain_accumulator_gf2_pack16(uint32_t tbase, uin
         }
         words[g + 1] = pack_pairs16(vb);
         if (g + 2 < kGroups) umma::tmem_ld_wait_regs16(va);
+    }
+}
+
+// The same drain with 64-column loads (32 registers per buffer): the drain of a short-K
+// tile waits on TMEM load round trips (tcgen05.wait::ld completes all outstanding loads,
+// so only one load can overlap the packing), and halving their number halves that wait.
+__device__ __forceinline__ void drain_accumulator_gf2_pack16_x64(uint32_t tbase, uint32_t (&words)[P_EPI_COLS / 32],
+                                                                 uint32_t acc_empty_leader, uint32_t lane) {
+    constexpr int kLoads = P_EPI_COLS / 64;
+    static_assert(kLoads % 2 == 0, "double-buffered 64-column loads");
+    uint32_t va[32], vb[32];
+    umma::tmem_ld32_pack16(tbase, va);
+    umma::tmem_ld_wait_regs(va);
+#pragma unroll
+    for (int g = 0; g < kLoads; g += 2) {
+        umma::tmem_ld32_pack16(tbase + 64 * (g + 1), vb);
+        words[2 * g] = pack_pairs16(half16(va, 0));
+        words[2 * g + 1] = pack_pairs16(half16(va, 1));
+        umma::tmem_ld_wait_regs(vb);
+        if (g + 2 < kLoads) {
+            umma::tmem_ld32_pack16(tbase + 64 * (g + 2), va);
+        } else {
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
+        }
+        words[2 * g + 2] = pack_pairs16(half16(vb, 0));
+        words[2 * g + 3] = pack_pairs16(half16(vb, 1));
+        if (g + 2 < kLoads) umma::tmem_ld_wait_regs(va);
     }
 }
 
@@ -717,7 +749,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                          3072 + 4 * local + 1);
                 const uint32_t tbase = tmem + ((quarter * 32) << 16) + half * P_EPI_COLS;
                 if (kGf2)
-                    if (BMMGPU_GF2_PACK16)
+                    if (BMMGPU_GF2_PACK16 && BMMGPU_GF2_DRAIN_COLS == 64)
+                        drain_accumulator_gf2_pack16_x64(tbase, words, acc_empty_leader, lane);
+                    else if (BMMGPU_GF2_PACK16)
                         drain_accumulator_gf2_pack16(tbase, words, acc_empty_leader, lane);
                     else if (BMMGPU_DRAIN_BATCH == 2)
                         drain_accumulator2<true>(tbase, words, acc_empty_leader, lane);
