@@ -56,8 +56,14 @@ WORKLOADS = {
     # K-chunks, partial products XOR/OR-folded on device, C tiles back to host).
     "c5-bool-ooc-524288": (524288, BOOL, 0, "Boolean n=2^19 out-of-core from host (configs[4] scaled to 1 GPU)"),
     "c5-gf2-ooc-524288": (524288, GF2, 0, "GF(2) n=2^19 out-of-core from host (configs[4] scaled to 1 GPU)"),
+    # the same GF(2) product with alternative-basis block products inside the output tiles
+    # (csrc/alt_tiles.cu): C[I, J] = XOR_K A[I, K] . B[K, J], each block product the
+    # device-resident alt-si recursion, tiles streamed from host memory
+    "c5-gf2-altooc-524288": (524288, GF2, 2, "GF(2) n=2^19 out-of-core, alt-si block products in output tiles "
+                                             "(configs[4] scaled to 1 GPU)"),
     # a small instance of the same out-of-core path (tests; run with a small --device-budget)
     "c5s-gf2-ooc-32768": (32768, GF2, 0, "GF(2) n=2^15 out-of-core from host (test size)"),
+    "c5s-gf2-altooc-32768": (32768, GF2, 2, "GF(2) n=2^15 out-of-core alt-si tiles (test size)"),
 }
 OOC_BUDGET = 40 << 30  # device bytes the out-of-core workloads may use (operands are 3 x 32 GiB)
 DEFAULT_WORKLOAD = "c3-bool-cubic-131072"
@@ -518,7 +524,18 @@ def run_ooc(args, dist: Dist) -> None:
     dev = dist.device
     torch.cuda.set_device(dev)
     w = n // 64
-    r0, r1 = shard_rows(n, dist.rank, dist.world, 256)
+    if algo == 0:
+        r0, r1 = shard_rows(n, dist.rank, dist.world, 256)
+        tile_log2, p0, p1 = 0, 0, 0
+    else:
+        # output row panels of b x b tiles, a contiguous run of panels per rank
+        b = min(131072, n // max(2, dist.world)) if not args.alt_tile_log2 else 1 << args.alt_tile_log2
+        T = n // b
+        if T % dist.world:
+            raise SystemExit(f"{T} tile panels do not split over {dist.world} ranks")
+        tile_log2 = b.bit_length() - 1
+        p0, p1 = dist.rank * T // dist.world, (dist.rank + 1) * T // dist.world
+        r0, r1 = p0 * b, p1 * b
     m = r1 - r0
     t_gen = time.perf_counter()
     hA = torch.empty(max(m, 1) * w, dtype=torch.int64, pin_memory=True)
@@ -550,7 +567,13 @@ def run_ooc(args, dist: Dist) -> None:
     def step() -> float:
         dist.barrier()
         s0 = time.perf_counter()
-        check(lib.bmmgpu_cubic(hA.data_ptr(), hB.data_ptr(), hC.data_ptr(), m, n, n, ring, ctypes.byref(opts)))
+        if algo == 0:
+            check(lib.bmmgpu_cubic(hA.data_ptr(), hB.data_ptr(), hC.data_ptr(), m, n, n, ring, ctypes.byref(opts)))
+        else:
+            # the library addresses A and C as whole n x n matrices and touches only this
+            # rank's panel rows: hand it base pointers r0 rows before the slab buffers
+            check(lib.bmmgpu_multiply_panels(hA.data_ptr() - r0 * w * 8, hB.data_ptr(), hC.data_ptr() - r0 * w * 8,
+                                             n, algo, tile_log2, p0, p1, ctypes.byref(opts)))
         return time.perf_counter() - s0
 
     for _ in range(args.warmup):
@@ -589,22 +612,36 @@ def run_ooc(args, dist: Dist) -> None:
         ok = parity["ok"]
     peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())
     kms = blk_ms.value / args.steps
-    achieved = eff_bops(m, n, n) / (kms * 1e-3)
+    if algo == 0:
+        launch_bops, kname = eff_bops(m, n, n), "cubic_umma2_kernel (K-chunk products of the tile driver)"
+    else:
+        # leaf layers of the (n/b)^2 (m/b) block products: 7^e products of L = b >> e each
+        bt = 1 << tile_log2
+        depth = (bt // 64).bit_length() - 1
+        e_levels = max(0, min(depth, depth + 6 - (args.leaf_log2 or 12)))
+        leaf = bt >> e_levels
+        launch_bops = (m // bt) * (n // bt) ** 2 * 7**e_levels * eff_bops(leaf, leaf, leaf)
+        kname = (f"cubic_umma2_kernel (leaf layers of {(m // bt) * (n // bt) ** 2} alt-si block products of {bt}: "
+                 f"7^{e_levels} products of {leaf}^3 each)")
+    achieved = launch_bops / (kms * 1e-3)
     if dist.rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "n3_rate": n3_rate(value, n), "dtype": "e2m1",
                 "data": "synthetic (BitMatrix::random seeds 1, 2, mt19937_64), pinned host memory",
                 "config": {"workload": args.workload, "desc": desc, "n": n, "ring": "gf2" if ring else "boolean",
-                           "algo": "cubic", "rows_per_rank": m, "device_budget_bytes": budget,
-                           "driver": "out-of-core tiles (force_streaming=1)",
+                           "algo": ["cubic", "sw", "alt-si", "alt-chain"][algo], "rows_per_rank": m,
+                           "device_budget_bytes": budget if algo == 0 else None,
+                           "driver": ("out-of-core tiles (force_streaming=1)" if algo == 0 else
+                                      f"out-of-core alt tiles (bmmgpu_multiply_panels, b = 2^{tile_log2}, "
+                                      f"panels [{p0}, {p1}) on rank 0)"),
                            "value_is": "end to end from pinned host buffers (the operands exceed the budget)",
                            "input_generation_s": t_gen,
                            "parallelism": f"output row slabs x{dist.world}, no exchange"},
                 "roofline": {"bound": "tensor", "achieved": achieved / 1e12,
                              "peak": peaks["umma_mxf4_bops"] / 1e12, "unit": "Tbop/s",
                              "frac": achieved / peaks["umma_mxf4_bops"], "traffic": None,
-                             "kernel": "cubic_umma2_kernel (K-chunk products of the tile driver)",
+                             "kernel": kname,
                              "kernel_ms": kms, "kernel_launches_per_step": blk_launches.value / args.steps,
                              "kernel_share_of_step": kms / (t * 1e3)},
                 "cpu_baseline": None,
@@ -612,7 +649,8 @@ def run_ooc(args, dist: Dist) -> None:
                         "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value),
                         "h2d_note": "counted by the library (bmmgpu_last_copy_bytes): A once, B once per "
                                     "resident row panel of the plan",
-                        "path": "bmmgpu_cubic (include/bmmgpu.h) from pinned host buffers, per rank"},
+                        "path": ("bmmgpu_cubic" if algo == 0 else "bmmgpu_multiply_panels") +
+                                " (include/bmmgpu.h) from pinned host buffers, per rank"},
                 "spot_check": ok, "parity": parity, "clocks": clocks, "gpu_launches": int(launches * args.steps)}
         print(json.dumps(line), flush=True)
     if shared_b is not None:
@@ -993,6 +1031,8 @@ def main() -> None:
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--kernel", choices=sorted(KERNEL_IDS), default="auto")
     ap.add_argument("--leaf-log2", dest="leaf_log2", type=int, default=0)
+    ap.add_argument("--alt-tile-log2", dest="alt_tile_log2", type=int, default=0,
+                    help="out-of-core alt workloads: log2 of the output tile side (0: min(2^17, n / ranks))")
     ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=3)
     ap.add_argument("--cpu-reps", dest="cpu_reps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")

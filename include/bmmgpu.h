@@ -91,9 +91,20 @@ int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, 
  * With several devices in opts->device_mask the top host levels of the recursion
  * (plan.d_host, or an automatic choice when it is 0) are dealt across the devices,
  * one host thread each, and the partial products are XOR-folded slab by slab over
- * peer copies (bmmgpu_dev_multiply_partial). */
+ * peer copies (bmmgpu_dev_multiply_partial).  Operands beyond the device budget (or
+ * opts->force_streaming == 1) run out of core: b x b output tiles (b = 2^17, or n/2),
+ * each the XOR of n/b alternative-basis block products of tiles streamed from host
+ * memory, row panels of tiles dealt over the devices. */
 int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int32_t algo,
                     const bmmgpu_plan* plan, int32_t semiring, const bmmgpu_opts* opts);
+
+/* The out-of-core fast product restricted to output row panels [panel_begin, panel_end)
+ * of its b x b tiles (b = 2^tile_log2; tile_log2 = 0: the default, 2^17 or n/2): C rows
+ * [panel_begin * b, panel_end * b) = those rows of A . B, over the devices of
+ * opts->device_mask.  Only those rows of A and C are read / written, all of B is, so
+ * ranks of one node can split a product by panels with B in shared host memory. */
+int bmmgpu_multiply_panels(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int32_t algo,
+                           int32_t tile_log2, uint64_t panel_begin, uint64_t panel_end, const bmmgpu_opts* opts);
 
 /* bmm::multiply_alt on interleaved vectors already in the scheme's basis (host
  * buffers of 4^depth * 64 words laid out [4]*depth [4096]; right operand blocks
@@ -111,6 +122,25 @@ int bmmgpu_multiply_alt(const uint64_t* a_hat, const uint64_t* b_hat, uint64_t* 
  * yates.cpp:143-172). */
 int bmmgpu_basis_change(uint64_t* words, uint64_t total_words, int32_t levels, int32_t algo, int32_t factor,
                         int32_t inverse);
+
+/* Layout conversions of the bmm:: API (reference bitmatrix.cpp:97-173, the CLI's
+ * `transform`, tools/bmm_cli.cpp:210-234) on the device, streamed through it in
+ * Morton-aligned super-tiles for host buffers of any size:
+ *   BMMGPU_LAYOUT_TRANSPOSE_BLOCKS64: rows x cols (multiples of 64) row-major matrix,
+ *     every 64 x 64 block transposed in place (src == dst allowed) -> transpose_blocks64;
+ *   BMMGPU_LAYOUT_TO_INTERLEAVED[_RIGHT]: n x n row-major (n = 64 * 2^depth) -> n^2/64
+ *     words of 64-word blocks in Morton order (right operand: blocks transposed)
+ *     -> to_interleaved(m, plan, Left|Result / Right);
+ *   BMMGPU_LAYOUT_FROM_INTERLEAVED[_RIGHT]: the inverse -> from_interleaved.
+ * Interleave conversions are out of place.  Errors: BMMGPU_ESHAPE with the reference's
+ * messages.  bmmgpu_dev_layout: the same on device buffers, on `stream`. */
+#define BMMGPU_LAYOUT_TRANSPOSE_BLOCKS64 0
+#define BMMGPU_LAYOUT_TO_INTERLEAVED 1
+#define BMMGPU_LAYOUT_TO_INTERLEAVED_RIGHT 2
+#define BMMGPU_LAYOUT_FROM_INTERLEAVED 3
+#define BMMGPU_LAYOUT_FROM_INTERLEAVED_RIGHT 4
+int bmmgpu_layout(const uint64_t* src, uint64_t* dst, uint64_t rows, uint64_t cols, int32_t op,
+                  const bmmgpu_opts* opts);
 
 /* BMM1 files (reference bitmatrix.cpp:187-233: "BMM1", rows, cols as LE u64, then
  * rows * ceil(cols/64) LE words) straight between disk and caller storage with parallel
@@ -153,6 +183,10 @@ int bmmgpu_dev_cubic_batched(const uint64_t* dA, uint64_t lda, uint64_t sA, cons
                              uint64_t sB, uint64_t* dC, uint64_t ldc, uint64_t sC, uint64_t batch, uint64_t m_pad,
                              uint64_t n_pad, uint64_t kw, int32_t semiring, int32_t kernel, int32_t accumulate,
                              void* stream);
+
+/* bmmgpu_layout on device buffers (see above), on `stream`. */
+int bmmgpu_dev_layout(const uint64_t* d_src, uint64_t* d_dst, uint64_t rows, uint64_t cols, int32_t op,
+                      void* stream);
 
 /* dst (+)= src over rows x words (XOR for GF(2), OR for Boolean), device memory,
  * row strides ldd / lds words: the integration of partial products of a K-split or

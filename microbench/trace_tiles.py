@@ -49,3 +49,5 @@ r = np.array(rows)
 for k, col in zip(["mma_tail (commit->epi sees full)", "drain", "handoff (done->mma sees empty)",
                    "first full after empty", "stage period"], r.T):
     print(f"{k:36s} median {np.median(col):8.0f} ns")
+per_tile = [full[S * (i + 1)] - full[S * i] for i in range(1, 512 // S - 1)]
+print(f"{'tile period (first stage to first stage)':36s} median {np.median(per_tile):8.0f} ns")

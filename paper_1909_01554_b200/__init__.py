@@ -119,6 +119,10 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_host_alloc.restype = ctypes.c_int
         L.bmmgpu_host_free.argtypes = [vp]
         L.bmmgpu_host_free.restype = ctypes.c_int
+        L.bmmgpu_layout.argtypes = [vp, vp, u64, u64, i32, ctypes.POINTER(_Opts)]
+        L.bmmgpu_layout.restype = ctypes.c_int
+        L.bmmgpu_dev_layout.argtypes = [vp, vp, u64, u64, i32, vp]
+        L.bmmgpu_dev_layout.restype = ctypes.c_int
         L.bmmgpu_debug_wave_stats.argtypes = [_u64p, _u64p]
         L.bmmgpu_debug_wave_stats.restype = ctypes.c_int
         L.bmmgpu_device_count.restype = ctypes.c_int
@@ -254,6 +258,59 @@ def write_bmm1(m: BitMatrix, path: str, threads: int = 0) -> None:
     _check(L.bmmgpu_bmm1_write(str(path).encode(), m.rows, m.cols, m.words.ctypes.data, threads))
 
 
+class Operand(enum.IntEnum):
+    """bmm::Operand (reference bitmatrix.hpp): right operands store their blocks transposed."""
+    Left = 0
+    Right = 1
+    Result = 2
+
+
+LAYOUT_TRANSPOSE_BLOCKS64, LAYOUT_TO_INTERLEAVED, LAYOUT_TO_INTERLEAVED_RIGHT = 0, 1, 2
+LAYOUT_FROM_INTERLEAVED, LAYOUT_FROM_INTERLEAVED_RIGHT = 3, 4
+
+
+def layout(src: np.ndarray, dst: np.ndarray, rows: int, cols: int, op: int, device_mask: int = 0) -> None:
+    """bmmgpu_layout: one of the layout conversions on host buffers (pinned or pageable),
+    streamed through the GPU (csrc/layout.cu)."""
+    if src.dtype != np.uint64 or dst.dtype != np.uint64 or not (src.flags["C_CONTIGUOUS"] and dst.flags["C_CONTIGUOUS"]):
+        raise ValueError("layout needs C-contiguous uint64 buffers")
+    need = rows * ((cols + 63) // 64)
+    if src.size < need or dst.size < need:
+        raise ValueError(f"layout needs {need} words in each buffer")
+    o = _opts(0, device_mask=device_mask)
+    _check(lib().bmmgpu_layout(src.ctypes.data, dst.ctypes.data, rows, cols, int(op), ctypes.byref(o)))
+
+
+def transpose_blocks64(m: BitMatrix) -> None:
+    """bmm::transpose_blocks64 (reference bitmatrix.cpp:97-110), in place, on the GPU."""
+    if m.rows % 64 or m.cols % 64:
+        raise ShapeError("block transpose needs dimensions divisible by 64")
+    if m.words.size:
+        layout(m.words, m.words, m.rows, m.cols, LAYOUT_TRANSPOSE_BLOCKS64)
+
+
+def to_interleaved(m: BitMatrix, plan: LayerPlan, which: Operand, out: np.ndarray | None = None) -> np.ndarray:
+    """bmm::to_interleaved (reference bitmatrix.cpp:112-148): the words of the
+    BitVectorTensor with modes [4]*depth + [4096], on the GPU."""
+    n = plan.matrix_dim()
+    if m.rows != n or m.cols != n:
+        raise ShapeError("matrix does not match plan dimension")
+    t = np.empty(n * n // 64, dtype=np.uint64) if out is None else out
+    layout(_contig(m), t, n, n, LAYOUT_TO_INTERLEAVED_RIGHT if which == Operand.Right else LAYOUT_TO_INTERLEAVED)
+    return t
+
+
+def from_interleaved(t: np.ndarray, plan: LayerPlan, which: Operand, out: np.ndarray | None = None) -> BitMatrix:
+    """bmm::from_interleaved (reference bitmatrix.cpp:150-173), on the GPU."""
+    n = plan.matrix_dim()
+    if t.size != n * n // 64:
+        raise ShapeError("tensor does not match plan shape")
+    w = np.empty(n * n // 64, dtype=np.uint64) if out is None else out
+    layout(np.ascontiguousarray(t, dtype=np.uint64), w, n, n,
+           LAYOUT_FROM_INTERLEAVED_RIGHT if which == Operand.Right else LAYOUT_FROM_INTERLEAVED)
+    return BitMatrix(n, n, w)
+
+
 class PinnedWords:
     """Page-locked host words (bmmgpu_host_alloc): `.words` is a numpy view; free() or
     garbage collection releases them."""
@@ -344,9 +401,12 @@ def multiply_cubic(a: BitMatrix, b: BitMatrix, ring: Semiring, workers: int = 1,
 
 def multiply(a: BitMatrix, b: BitMatrix, algo: Algo, plan: LayerPlan, ring: Semiring, *,
              kernel: int = Kernel.AUTO, leaf_log2: int = 0, timing: ctypes.c_double | None = None,
-             out: BitMatrix | None = None) -> BitMatrix:
+             out: BitMatrix | None = None, device_mask: int = 0, device_budget: int = 0,
+             force_streaming: bool = False) -> BitMatrix:
     """bmm::multiply (reference engine.cpp:351-382) on the GPU.  `out` may supply
-    the result storage (e.g. pinned host memory)."""
+    the result storage (e.g. pinned host memory).  Operands beyond `device_budget` (0: the
+    free HBM) or `force_streaming` run out of core: output tiles of alternative-basis
+    block products streamed from host memory (csrc/alt_tiles.cu)."""
     if algo == Algo.Cubic:
         return multiply_cubic(a, b, ring, plan.workers, kernel=kernel, timing=timing)
     if ring == Semiring.BooleanOrAnd:
@@ -365,5 +425,7 @@ def multiply(a: BitMatrix, b: BitMatrix, algo: Algo, plan: LayerPlan, ring: Semi
         raise ShapeError("output shape mismatch")
     p = _Plan(plan.d_host, plan.d_serial, plan.d_parallel, plan.d_inner, plan.workers)
     _check(lib().bmmgpu_multiply(_contig(a).ctypes.data, _contig(b).ctypes.data, c.words.ctypes.data, n, int(algo),
-                                 ctypes.byref(p), int(ring), ctypes.byref(_opts(kernel, leaf_log2, timing))))
+                                 ctypes.byref(p), int(ring),
+                                 ctypes.byref(_opts(kernel, leaf_log2, timing, device_mask=device_mask,
+                                                    device_budget=device_budget, force_streaming=force_streaming))))
     return c

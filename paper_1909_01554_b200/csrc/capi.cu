@@ -40,6 +40,9 @@ int alt_multiply_multi(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64
                        const std::vector<int>& phys, int kernel, int leaf_log2, double* timing_ms);
 int host_levels_for(uint64_t n, uint32_t parts, int e);
 int alt_levels(uint64_t n, int leaf_log2);
+int alt_multiply_tiles(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo,
+                       const std::vector<int>& devs, int kernel, int leaf_log2, double* timing_ms, uint64_t b,
+                       uint64_t p0, uint64_t p1);
 int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const uint64_t* A, const uint64_t* B,
                       uint64_t* C, uint64_t k, uint64_t n, bool gf2, int kernel, bool accumulate, uint64_t budget,
                       float* ms_out);
@@ -752,6 +755,17 @@ int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t 
     std::vector<int> devs = devices_of(o.device_mask, &st);
     if (st) return st;
     BMMGPU_CUDA_TRY(cudaSetDevice(devs[0]));
+    {
+        // Operands beyond HBM (configs[4]): output tiles of alt-basis block products
+        // streamed from host memory (alt_tiles.cu).  In core the recursion needs about six
+        // n^2/8 arrays (A, B, Bt, C and the level buffers of the breadth-first part).
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        const uint64_t budget = o.device_budget ? o.device_budget : uint64_t(free_b);
+        const double need = 6.0 * double(n) * double(n) / 8.0;
+        if (o.force_streaming == 1 || need > double(budget))
+            return alt_multiply_tiles(A, B, C, n, algo, devs, o.kernel, o.leaf_log2, o.timing_ms, 0, 0, 0);
+    }
     if (devs.size() > 1) {
         // several devices: the top host levels of the recursion are dealt across them
         // (plan.d_host when the caller sets it, else the most even deal), and the partial

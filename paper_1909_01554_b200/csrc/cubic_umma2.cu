@@ -21,10 +21,10 @@
 // Why persistent: one launch walks every tile (static round robin over the
 // 74 SM pairs, raster groups of 12 row tiles), so TMEM allocation, barrier setup
 // and scale-factor fill happen once, the producers stream the next tile's stages
-// while the current tile's accumulator drains, and the MMA pauses only for the
-// drain (the accumulator takes 256 of the 512 TMEM columns and the constant scale
-// regions the rest, so there is one accumulator).  This is what makes the short-K
-// leaf products of the alternative-basis recursion efficient.
+// while the current tile's accumulator drains, and the MMAs of the next tile start as
+// soon as 32 columns are drained: the pair's tiles alternate between two accumulators
+// that overlap in 32 columns (the block scales take the last 32 of the 512).  This is
+// what makes the short-K leaf products of the alternative-basis recursion efficient.
 //
 // Roles per CTA (480 threads):
 //   loader (warp 13, one lane; TMA): per superstage of 4 stages (1024 K bits) one
@@ -50,9 +50,9 @@
 //     bias MMA and then 4 MMAs per stage, commits each stage to both CTAs' empty
 //     barriers and each tile to both CTAs' acc_full barriers.
 //   epilogue (warps 9-12): drain the CTA's 128 accumulator rows with double-buffered
-//     32-column TMEM loads (optional GF(2) variant: .pack::16b, Bt rows permuted so a
-//     register carries two output columns), release the accumulator (acc_empty) as soon as the last
-//     load lands, pack the bits (funnel-shift chains / AND + shift-add), store.
+//     32-column TMEM loads (GF(2): .pack::16b, two columns per register), the group that
+//     overlaps the other accumulator first (then `ovl`), release the accumulator
+//     (acc_empty) as soon as the last load lands, pack the bits, store.
 // Measured (ncu, microbench/trace_tiles.py, time_leaf.py): the tensor pipe is 98-99%
 // active on long K, held at ~1.8 GHz by the board power cap; on 4096-bit leaves each
 // tile boundary costs ~0.5 us (drain, bias MMA, commit / restart latency) against a
@@ -79,14 +79,11 @@ constexpr int P_REGION = P_ROWS * 128;    // bytes of one operand per stage (16 
 constexpr int P_STAGE = 2 * P_REGION;
 constexpr int P_PRODUCERS = 256;          // expanders: two threads per row of A and of Bt
 constexpr int P_MMA_WARP = P_PRODUCERS / 32;
-#ifndef BMMGPU_EPI_WARPS
-#define BMMGPU_EPI_WARPS 4  // 8 (two per TMEM lane quarter) measured no faster, and spills at 96 registers
-#endif
-constexpr int P_EPI_WARPS = BMMGPU_EPI_WARPS;     // 4: one per TMEM lane quarter; 8: two, 128 columns each
-constexpr int P_EPI_COLS = 256 * 4 / P_EPI_WARPS;  // accumulator columns one epilogue warp drains
-static_assert(P_EPI_WARPS == 4 || P_EPI_WARPS == 8, "epilogue warps cover the 4 lane quarters evenly");
+// 4 epilogue warps, one per TMEM lane quarter (8, two per quarter, measured no faster and
+// spilled at 96 registers)
+constexpr int P_EPI_WARPS = 4;
 constexpr int P_LOADER_WARP0 = P_MMA_WARP + 1 + P_EPI_WARPS;  // after the MMA warp and the epilogue warps
-constexpr int P_LOADERS = P_EPI_WARPS == 8 ? 32 : 64;  // cp.async loader threads (TMA: one lane)
+constexpr int P_LOADERS = 64;  // cp.async loader threads (TMA: one lane)
 constexpr int P_THREADS = P_PRODUCERS + 32 + 32 * P_EPI_WARPS + P_LOADERS;
 #ifndef BMMGPU_SST_SLOTS
 #define BMMGPU_SST_SLOTS 2
@@ -101,9 +98,11 @@ constexpr int P_CONST = P_REGION;
 constexpr size_t P_SMEM =
     size_t(P_STAGES) * P_STAGE + size_t(P_SST_SLOTS) * P_SST + P_CONST + 1024;  // + alignment slack
 constexpr uint32_t P_TMEM_COLS = 512;
-constexpr uint32_t P_SF_EVEN = 256;
-constexpr uint32_t P_SF_ODD = 384;
-constexpr uint32_t P_SF_BIAS = 480;  // 2^9 block scales of the bias MMA
+// Block scales (UE8M0, uniform): an M128 / N128-per-CTA operand's scales take 4 TMEM
+// columns (rows 32 q + i in lane i, replicated over the 4 lane quarters); 8 each.
+constexpr uint32_t P_SF_EVEN = 480;  // 1.0
+constexpr uint32_t P_SF_ODD = 488;   // 2.0
+constexpr uint32_t P_SF_BIAS = 496;  // 2^9 block scales of the bias MMA
 constexpr uint32_t P_MAX_PAIRS = 74;  // 148 SMs
 
 static_assert(P_SMEM <= 232448 - 1024, "stage ring exceeds shared memory");
@@ -244,41 +243,28 @@ __device__ __forceinline__ uint32_t pack_counts16(const uint32_t (&v)[16]) {
     return __byte_perm(a, b, 0x0073);  // [a.byte3, b.byte3, -, -]
 }
 
-// The epilogue warp's 32 lanes x P_EPI_COLS columns of the accumulator -> words per lane,
-// 16 columns per TMEM load with two register buffers: chunk c + 1 is in flight while
-// chunk c is packed, and the accumulator goes back to the leader's MMA lane as soon as
-// the last chunk has landed.  Short-K tiles (the 4096-bit leaves of the fast recursion)
-// wait on this drain.
-template <bool kGf2>
-__device__ __forceinline__ void drain_accumulator(uint32_t tbase, uint32_t (&words)[P_EPI_COLS / 32],
-                                                  uint32_t acc_empty_leader, uint32_t lane) {
-    constexpr int kChunks = P_EPI_COLS / 16;
-    uint32_t va[16], vb[16];
-    umma::tmem_ld16(tbase, va);
-    umma::tmem_ld_wait_regs16(va);
-#pragma unroll
-    for (int c = 0; c < kChunks; c += 2) {
-        umma::tmem_ld16(tbase + 16 * (c + 1), vb);
-        const uint32_t lo = pack_counts16<kGf2>(va);
-        umma::tmem_ld_wait_regs16(vb);
-        if (c + 2 < kChunks) {
-            umma::tmem_ld16(tbase + 16 * (c + 2), va);
-        } else {
-            umma::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
-        }
-        words[c >> 1] = __byte_perm(lo, pack_counts16<kGf2>(vb), 0x5410);
-        if (c + 2 < kChunks) umma::tmem_ld_wait_regs16(va);
-    }
-}
-
-// Same drain with 32-column groups (two 16-column loads per buffer): the drain of a
-// short-K tile is bound by the TMEM load round trips (one in flight while the other
-// buffer is packed), so halving their number shortens it; 64 buffer registers.
-#ifndef BMMGPU_DRAIN_BATCH
-#define BMMGPU_DRAIN_BATCH 2  // 1: 16-column groups
+// Two accumulators that overlap in 32 columns (X = [0, 256), Y = [224, 480); the block
+// scales take [480, 512)): the pair's tiles alternate X, Y, X, ... so the MMAs of tile
+// j + 1 need only the overlap drained from tile j.  The epilogue drains the overlap group
+// first (X: tile columns 224..255, Y: tile columns 0..31), signals `ovl`, then the rest,
+// then `acc_empty` of that accumulator.  The drain reads TMEM at ~64 B/clk per SM -- a
+// whole 256-column accumulator is ~1000 clk with 16-bit reads, ~2000 with 32-bit -- so with
+// one accumulator the tensor pipe idled ~12 % of a 4096-bit leaf tile; now it waits for one
+// 32-column group.  kRot: drain order 7, 0, 1, .., 6 (X) instead of 0 .. 7 (Y); compile-time
+// so `words` stays in registers.
+#ifndef BMMGPU_ACC2
+#define BMMGPU_ACC2 1  // 0: one accumulator (the MMAs wait for the whole drain)
 #endif
+constexpr uint32_t P_ACC_Y = BMMGPU_ACC2 ? 224 : 0;  // TMEM column of accumulator Y
+template <bool kRot>
+__device__ __forceinline__ constexpr int drain_group(int i) {
+    return kRot ? (i + 7) & 7 : i;
+}
+__device__ __forceinline__ void drain_signal(uint32_t bar_leader, uint32_t lane) {
+    umma::fence_before_sync();
+    __syncwarp();
+    if (lane == 0) umma::mbar_arrive_cluster(bar_leader);
+}
 __device__ __forceinline__ uint32_t (&half16(uint32_t (&v)[32], int h))[16] {
     return *reinterpret_cast<uint32_t(*)[16]>(&v[16 * h]);
 }
@@ -286,60 +272,41 @@ template <bool kGf2>
 __device__ __forceinline__ uint32_t pack_counts32(uint32_t (&v)[32]) {
     return __byte_perm(pack_counts16<kGf2>(half16(v, 0)), pack_counts16<kGf2>(half16(v, 1)), 0x5410);
 }
-template <bool kGf2>
-__device__ __forceinline__ void drain_accumulator2(uint32_t tbase, uint32_t (&words)[P_EPI_COLS / 32],
-                                                   uint32_t acc_empty_leader, uint32_t lane) {
-    constexpr int kGroups = P_EPI_COLS / 32;
+
+// 32-bit TMEM reads in 32-column groups (two 16-column loads per buffer), double buffered:
+// group i + 1 is in flight while group i is packed.
+template <bool kGf2, bool kRot>
+__device__ __forceinline__ void drain_accumulator2(uint32_t tacc, uint32_t (&words)[8], uint32_t ovl_leader,
+                                                   uint32_t empty_leader, uint32_t lane) {
     uint32_t va[32], vb[32];
-    umma::tmem_ld16(tbase, half16(va, 0));
-    umma::tmem_ld16(tbase + 16, half16(va, 1));
+    umma::tmem_ld16(tacc + 32 * drain_group<kRot>(0), half16(va, 0));
+    umma::tmem_ld16(tacc + 32 * drain_group<kRot>(0) + 16, half16(va, 1));
     umma::tmem_ld_wait_regs(va);
+    drain_signal(ovl_leader, lane);
 #pragma unroll
-    for (int g = 0; g < kGroups; g += 2) {
-        umma::tmem_ld16(tbase + 32 * (g + 1), half16(vb, 0));
-        umma::tmem_ld16(tbase + 32 * (g + 1) + 16, half16(vb, 1));
-        words[g] = pack_counts32<kGf2>(va);
+    for (int i = 0; i < 8; i += 2) {
+        umma::tmem_ld16(tacc + 32 * drain_group<kRot>(i + 1), half16(vb, 0));
+        umma::tmem_ld16(tacc + 32 * drain_group<kRot>(i + 1) + 16, half16(vb, 1));
+        words[drain_group<kRot>(i)] = pack_counts32<kGf2>(va);
         umma::tmem_ld_wait_regs(vb);
-        if (g + 2 < kGroups) {
-            umma::tmem_ld16(tbase + 32 * (g + 2), half16(va, 0));
-            umma::tmem_ld16(tbase + 32 * (g + 2) + 16, half16(va, 1));
+        if (i + 2 < 8) {
+            umma::tmem_ld16(tacc + 32 * drain_group<kRot>(i + 2), half16(va, 0));
+            umma::tmem_ld16(tacc + 32 * drain_group<kRot>(i + 2) + 16, half16(va, 1));
         } else {
-            umma::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
+            drain_signal(empty_leader, lane);
         }
-        words[g + 1] = pack_counts32<kGf2>(vb);
-        if (g + 2 < kGroups) umma::tmem_ld_wait_regs(va);
+        words[drain_group<kRot>(i + 1)] = pack_counts32<kGf2>(vb);
+        if (i + 2 < 8) umma::tmem_ld_wait_regs(va);
     }
 }
 
-// GF(2) needs bit 0 of each count only, so the drain reads the accumulator with
-// .pack::16b (the low halves of two columns per register: half the TMEM bytes and
-// half the loads).  The expanders place Bt row 32 G + 16 h + i of a tile at
-// accumulator column 32 G + 2 i + h, so register i of a 32-column load holds output
-// columns i (bit 0) and 16 + i (bit 16) and one AND + shift-add per register builds the
-// word in output order.
+// GF(2) needs bit 0 of each count only, so its drain reads the accumulator with
+// .pack::16b (the low halves of two columns per register: half the TMEM bytes).  Register
+// i of a 32-column load holds column 2i (bit 0) and 2i + 1 (bit 16); one AND + shift-add per
+// register gathers them and an outer perfect shuffle restores column order.
 #ifndef BMMGPU_GF2_PACK16
-#define BMMGPU_GF2_PACK16 2  // 0 off; 1 Bt-permuted (fails the two-process tile test intermittently); 2 drain-only
+#define BMMGPU_GF2_PACK16 1  // 0: 32-bit reads for GF(2) too
 #endif
-#ifndef BMMGPU_GF2_DRAIN_COLS
-#define BMMGPU_GF2_DRAIN_COLS 32  // columns per .pack::16b TMEM load of the GF(2) drain: 32 or 64
-#endif
-// Output column o of a 32-column group sits at accumulator column 2o (o < 16) or
-// 2(o - 16) + 1.  Expander thread t of the group takes Bt row rho(t) so that both its
-// packed-ring reads (row rho & 7) and its operand stores (slot & 7) stay distinct across
-// each 8 lanes -- no shared-memory bank conflicts: lanes 8q .. 8q+3 take rows 4q .. 4q+3,
-// lanes 8q+4 .. 8q+7 rows 16 + 4(q ^ 1) .. +3.
-__device__ __forceinline__ uint32_t gf2_bt_row(uint32_t r) {
-    if (BMMGPU_GF2_PACK16 != 1) return r;
-    const uint32_t t = r & 31u, q = t >> 3, j = t & 7u;
-    return (r & ~31u) | (j < 4 ? 4 * q + j : 16 + 4 * (q ^ 1u) + (j - 4));
-}
-__device__ __forceinline__ uint32_t gf2_column_slot(uint32_t o) {
-    if (BMMGPU_GF2_PACK16 != 1) return o;
-    const uint32_t t = o & 31u;
-    return (o & ~31u) | (t < 16 ? 2 * t : 2 * (t - 16) + 1);
-}
 __device__ __forceinline__ uint32_t pack_pairs16(const uint32_t (&v)[16]) {
     uint32_t a = 0, b = 0;  // two chains
 #pragma unroll
@@ -348,66 +315,32 @@ __device__ __forceinline__ uint32_t pack_pairs16(const uint32_t (&v)[16]) {
         b += (v[i + 1] & 0x00010001u) << (i + 1);
     }
     uint32_t x = a | b;
-    if (BMMGPU_GF2_PACK16 == 2) {
-        // natural column order (no Bt permutation): bit i = column 2i, bit 16 + i =
-        // column 2i + 1 -> interleave the halves (outer perfect shuffle)
-        uint32_t t;
-        t = (x ^ (x >> 8)) & 0x0000FF00u; x ^= t ^ (t << 8);
-        t = (x ^ (x >> 4)) & 0x00F000F0u; x ^= t ^ (t << 4);
-        t = (x ^ (x >> 2)) & 0x0C0C0C0Cu; x ^= t ^ (t << 2);
-        t = (x ^ (x >> 1)) & 0x22222222u; x ^= t ^ (t << 1);
-    }
+    // bit i = column 2i, bit 16 + i = column 2i + 1 -> interleave the halves
+    uint32_t t;
+    t = (x ^ (x >> 8)) & 0x0000FF00u; x ^= t ^ (t << 8);
+    t = (x ^ (x >> 4)) & 0x00F000F0u; x ^= t ^ (t << 4);
+    t = (x ^ (x >> 2)) & 0x0C0C0C0Cu; x ^= t ^ (t << 2);
+    t = (x ^ (x >> 1)) & 0x22222222u; x ^= t ^ (t << 1);
     return x;
 }
-__device__ __forceinline__ void drain_accumulator_gf2_pack16(uint32_t tbase, uint32_t (&words)[P_EPI_COLS / 32],
-                                                             uint32_t acc_empty_leader, uint32_t lane) {
-    constexpr int kGroups = P_EPI_COLS / 32;
+template <bool kRot>
+__device__ __forceinline__ void drain_accumulator_gf2_pack16(uint32_t tacc, uint32_t (&words)[8], uint32_t ovl_leader,
+                                                             uint32_t empty_leader, uint32_t lane) {
     uint32_t va[16], vb[16];
-    umma::tmem_ld16_pack16(tbase, va);
+    umma::tmem_ld16_pack16(tacc + 32 * drain_group<kRot>(0), va);
     umma::tmem_ld_wait_regs16(va);
+    drain_signal(ovl_leader, lane);
 #pragma unroll
-    for (int g = 0; g < kGroups; g += 2) {
-        umma::tmem_ld16_pack16(tbase + 32 * (g + 1), vb);
-        words[g] = pack_pairs16(va);
+    for (int i = 0; i < 8; i += 2) {
+        umma::tmem_ld16_pack16(tacc + 32 * drain_group<kRot>(i + 1), vb);
+        words[drain_group<kRot>(i)] = pack_pairs16(va);
         umma::tmem_ld_wait_regs16(vb);
-        if (g + 2 < kGroups) {
-            umma::tmem_ld16_pack16(tbase + 32 * (g + 2), va);
-        } else {
-            umma::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
-        }
-        words[g + 1] = pack_pairs16(vb);
-        if (g + 2 < kGroups) umma::tmem_ld_wait_regs16(va);
-    }
-}
-
-// The same drain with 64-column loads (32 registers per buffer): the drain of a short-K
-// tile waits on TMEM load round trips (tcgen05.wait::ld completes all outstanding loads,
-// so only one load can overlap the packing), and halving their number halves that wait.
-__device__ __forceinline__ void drain_accumulator_gf2_pack16_x64(uint32_t tbase, uint32_t (&words)[P_EPI_COLS / 32],
-                                                                 uint32_t acc_empty_leader, uint32_t lane) {
-    constexpr int kLoads = P_EPI_COLS / 64;
-    static_assert(kLoads % 2 == 0, "double-buffered 64-column loads");
-    uint32_t va[32], vb[32];
-    umma::tmem_ld32_pack16(tbase, va);
-    umma::tmem_ld_wait_regs(va);
-#pragma unroll
-    for (int g = 0; g < kLoads; g += 2) {
-        umma::tmem_ld32_pack16(tbase + 64 * (g + 1), vb);
-        words[2 * g] = pack_pairs16(half16(va, 0));
-        words[2 * g + 1] = pack_pairs16(half16(va, 1));
-        umma::tmem_ld_wait_regs(vb);
-        if (g + 2 < kLoads) {
-            umma::tmem_ld32_pack16(tbase + 64 * (g + 2), va);
-        } else {
-            umma::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) umma::mbar_arrive_cluster(acc_empty_leader);
-        }
-        words[2 * g + 2] = pack_pairs16(half16(vb, 0));
-        words[2 * g + 3] = pack_pairs16(half16(vb, 1));
-        if (g + 2 < kLoads) umma::tmem_ld_wait_regs(va);
+        if (i + 2 < 8)
+            umma::tmem_ld16_pack16(tacc + 32 * drain_group<kRot>(i + 2), va);
+        else
+            drain_signal(empty_leader, lane);
+        words[drain_group<kRot>(i + 1)] = pack_pairs16(vb);
+        if (i + 2 < 8) umma::tmem_ld_wait_regs16(va);
     }
 }
 
@@ -429,8 +362,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     __shared__ __align__(8) uint64_t empty_bar[P_STAGES];
     __shared__ __align__(8) uint64_t pk_full_bar[P_SST_SLOTS];
     __shared__ __align__(8) uint64_t pk_empty_bar[P_SST_SLOTS];
-    __shared__ __align__(8) uint64_t acc_full_bar;
-    __shared__ __align__(8) uint64_t acc_empty_bar;
+    __shared__ __align__(8) uint64_t acc_full_bar[2];   // per accumulator (X, Y)
+    __shared__ __align__(8) uint64_t acc_empty_bar[2];
+    __shared__ __align__(8) uint64_t ovl_bar;           // overlap columns of the last tile drained
     __shared__ uint32_t tmem_base_sh;
 
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -449,8 +383,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             umma::mbar_init(&pk_full_bar[s], kTma ? 1 : P_LOADERS);
             umma::mbar_init(&pk_empty_bar[s], P_PRODUCERS / 32);  // every expander warp, every superstage
         }
-        umma::mbar_init(&acc_full_bar, 1);
-        umma::mbar_init(&acc_empty_bar, 2 * P_EPI_WARPS);
+        for (int i = 0; i < 2; ++i) {
+            umma::mbar_init(&acc_full_bar[i], 1);
+            umma::mbar_init(&acc_empty_bar[i], 2 * P_EPI_WARPS);
+        }
+        umma::mbar_init(&ovl_bar, 2 * P_EPI_WARPS);
         umma::mbar_fence_init();
     }
     umma::fence_before_sync();
@@ -459,11 +396,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     const uint32_t tmem = tmem_base_sh;
     if (warp < 4) {
         const uint32_t lane_base = (warp * 32) << 16;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) umma::tmem_st32_fill(tmem + lane_base + P_SF_EVEN + 32 * c, 0x7F7F7F7Fu);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) umma::tmem_st32_fill(tmem + lane_base + P_SF_ODD + 32 * c, 0x80808080u);
-        umma::tmem_st32_fill(tmem + lane_base + P_SF_BIAS, 0x88888888u);  // 2^9
+        umma::tmem_st8_fill(tmem + lane_base + P_SF_EVEN, 0x7F7F7F7Fu);
+        umma::tmem_st8_fill(tmem + lane_base + P_SF_ODD, 0x80808080u);
+        umma::tmem_st8_fill(tmem + lane_base + P_SF_BIAS, 0x88888888u);  // 2^9
         umma::tmem_st_wait();
     }
     {
@@ -490,8 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         // expands and stores each stage into the tensor-core ring.
         const uint32_t grp = warp >> 2, r = tid & (P_ROWS - 1), rsw = r & 7;
         // Bt row this thread expands and the operand row (accumulator column) it goes to
-        const uint32_t rbt = kGf2 ? gf2_bt_row(r) : r, rb = kGf2 ? gf2_column_slot(rbt) : r;
-        const uint32_t rbsw = rbt & 7;
+        const uint32_t rbt = r, rb = r, rbsw = r & 7;
         const uint32_t full_leader0 = umma::mapa_shared(smem_u32(&full_bar[0]), 0);
         const uint8_t* pkrow = smem + size_t(P_STAGES) * P_STAGE + r * 128;
         const uint8_t* pkrow_b = smem + size_t(P_STAGES) * P_STAGE + rbt * 128 + P_SST_OP;
@@ -565,15 +499,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             const long long p_t0 = clock64();
 #endif
             for (uint32_t t = pair; t < total_tiles; t += n_pairs, ++local) {
-                // the accumulator must have been drained by both CTAs' epilogues
                 // the tile's first stage is usually staged long before the accumulator comes
-                // back: wait for it first so the MMAs issue right after acc_empty
+                // back: wait for it first so the MMAs issue right after the accumulator is free.
+                // Accumulator (local & 1) must have been drained by both CTAs' epilogues from
+                // tile local - 2, and the overlap columns from tile local - 1.
+                const uint32_t buf = BMMGPU_ACC2 ? (local & 1) : 0;
                 if (local > 0 && n_stages > 0) umma::mbar_wait(&full_bar[s], full_parity);
-                if (local > 0) PWAIT(4, umma::mbar_wait(&acc_empty_bar, (local - 1) & 1));
+                if (BMMGPU_ACC2) {
+                    if (local > 0) PWAIT(4, umma::mbar_wait(&ovl_bar, (local - 1) & 1));
+                    if (local > 1) PWAIT(4, umma::mbar_wait(&acc_empty_bar[buf], ((local >> 1) - 1) & 1));
+                } else if (local > 0) {
+                    PWAIT(4, umma::mbar_wait(&acc_empty_bar[(local - 1) & 1], ((local - 1) >> 1) & 1));
+                }
+                const uint32_t dacc = tmem + (buf ? P_ACC_Y : 0);
                 TRACE_AT(pair == 0 && lane == 0 && local < 512, 3072 + 4 * local + 3);
                 umma::fence_after_sync();
                 if (umma::elect_one() && !PROBE(32))  // preset the accumulator to 2^23
-                    umma::mma_mxf4_pair(tmem, desc_const, desc_const, idesc, tmem + P_SF_BIAS, tmem + P_SF_BIAS, 0u);
+                    umma::mma_mxf4_pair(dacc, desc_const, desc_const, idesc, tmem + P_SF_BIAS, tmem + P_SF_BIAS, 0u);
                 __syncwarp();
                 for (uint64_t k = 0; k < (PROBE(128) ? 0 : n_stages); ++k, ++it, s = (s + 1 == P_STAGES) ? (full_parity ^= 1, 0) : s + 1) {
                     PWAIT(3, umma::mbar_wait(&full_bar[s], full_parity));
@@ -589,14 +531,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                             if (PROBE(32)) continue;
                             // + 32 bytes per K = 64 step
                             // always accumulate onto the bias
-                            umma::mma_mxf4_pair(tmem, da0 + 2 * j, db0 + 2 * j, idesc, sf, sf, 1u);
+                            umma::mma_mxf4_pair(dacc, da0 + 2 * j, db0 + 2 * j, idesc, sf, sf, 1u);
                         }
                         umma::mma_commit_pair(&empty_bar[s], 0x3);
                     }
                     __syncwarp();
                     TRACE_AT(pair == 0 && lane == 0 && it < 512, 512 + it);
                 }
-                if (umma::elect_one()) umma::mma_commit_pair(&acc_full_bar, 0x3);
+                if (umma::elect_one()) umma::mma_commit_pair(&acc_full_bar[local & 1], 0x3);
                 TRACE_AT(pair == 0 && lane == 0 && local < 512, 3072 + 4 * local + 0);
                 __syncwarp();
             }
@@ -726,53 +668,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #endif
         PSTORE(6, 7, lt == 0);
     } else {
-        // ------------------------------------------------ epilogue (warps 9 .. 8 + P_EPI_WARPS):
-        // warp w may access TMEM lanes 32 (w % 4) ..; with 8 warps each lane quarter has two,
-        // draining columns [0, 128) and [128, 256), which halves the drain the next tile's
-        // MMAs wait on.
-        constexpr int kWords = P_EPI_COLS / 32;
+        // ------------------------------------------------ epilogue (warps 9 .. 12): warp w drains
+        // TMEM lanes 32 (w % 4) .. of the tile's accumulator (local & 1), overlap group first.
         const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
-        const uint32_t half = (warp - (P_MMA_WARP + 1)) / 4;
-        const uint32_t acc_empty_leader = umma::mapa_shared(smem_u32(&acc_empty_bar), 0);
+        const uint32_t ovl_leader = umma::mapa_shared(smem_u32(&ovl_bar), 0);
+        const uint32_t empty_leader0 = umma::mapa_shared(smem_u32(&acc_empty_bar[0]), 0);
         uint32_t local = 0;
         for (uint32_t t = pair; t < total_tiles; t += n_pairs, ++local) {
             uint32_t b, tm, tn;
             map.decode(t, b, tm, tn);
-            uint32_t words[kWords];
-            if (n_stages > 0) {
-                if (epi_sleep_ns > 0)
-                    umma::mbar_wait_sleep(&acc_full_bar, local & 1, epi_sleep_ns);
+            uint32_t words[8];
+            const uint32_t buf = local & 1;
+            if (epi_sleep_ns > 0)
+                umma::mbar_wait_sleep(&acc_full_bar[buf], (local >> 1) & 1, epi_sleep_ns);
+            else
+                umma::mbar_wait(&acc_full_bar[buf], (local >> 1) & 1);
+            umma::fence_after_sync();
+            TRACE_AT(pair == 0 && rank == 0 && quarter == 0 && lane == 0 && local < 512, 3072 + 4 * local + 1);
+            const uint32_t ybuf = BMMGPU_ACC2 ? buf : 0;
+            const uint32_t tacc = tmem + ((quarter * 32) << 16) + (ybuf ? P_ACC_Y : 0);
+            const uint32_t empty_leader = empty_leader0 + 8 * buf;
+            if (kGf2 && BMMGPU_GF2_PACK16) {
+                if (ybuf)
+                    drain_accumulator_gf2_pack16<false>(tacc, words, ovl_leader, empty_leader, lane);
                 else
-                    umma::mbar_wait(&acc_full_bar, local & 1);
-                umma::fence_after_sync();
-                TRACE_AT(pair == 0 && rank == 0 && quarter == 0 && half == 0 && lane == 0 && local < 512,
-                         3072 + 4 * local + 1);
-                const uint32_t tbase = tmem + ((quarter * 32) << 16) + half * P_EPI_COLS;
-                if (kGf2)
-                    if (BMMGPU_GF2_PACK16 && BMMGPU_GF2_DRAIN_COLS == 64)
-                        drain_accumulator_gf2_pack16_x64(tbase, words, acc_empty_leader, lane);
-                    else if (BMMGPU_GF2_PACK16)
-                        drain_accumulator_gf2_pack16(tbase, words, acc_empty_leader, lane);
-                    else if (BMMGPU_DRAIN_BATCH == 2)
-                        drain_accumulator2<true>(tbase, words, acc_empty_leader, lane);
-                    else
-                        drain_accumulator<true>(tbase, words, acc_empty_leader, lane);
+                    drain_accumulator_gf2_pack16<true>(tacc, words, ovl_leader, empty_leader, lane);
+            } else if (kGf2) {
+                if (ybuf)
+                    drain_accumulator2<true, false>(tacc, words, ovl_leader, empty_leader, lane);
                 else
-                    if (BMMGPU_DRAIN_BATCH == 2)
-                        drain_accumulator2<false>(tbase, words, acc_empty_leader, lane);
-                    else
-                        drain_accumulator<false>(tbase, words, acc_empty_leader, lane);
-                TRACE_AT(pair == 0 && rank == 0 && quarter == 0 && half == 0 && lane == 0 && local < 512,
-                         3072 + 4 * local + 2);
+                    drain_accumulator2<true, true>(tacc, words, ovl_leader, empty_leader, lane);
             } else {
-#pragma unroll
-                for (int c = 0; c < kWords; ++c) words[c] = 0;
+                if (ybuf)
+                    drain_accumulator2<false, false>(tacc, words, ovl_leader, empty_leader, lane);
+                else
+                    drain_accumulator2<false, true>(tacc, words, ovl_leader, empty_leader, lane);
             }
+            TRACE_AT(pair == 0 && rank == 0 && quarter == 0 && lane == 0 && local < 512, 3072 + 4 * local + 2);
             const uint64_t row = uint64_t(tm) * P_BM + rank * P_ROWS + quarter * 32 + lane;
-            uint4* dst = reinterpret_cast<uint4*>(C + b * map.sC + row * ldc + uint64_t(tn) * (P_BN / 64)) +
-                         half * (kWords / 4);
+            uint4* dst = reinterpret_cast<uint4*>(C + b * map.sC + row * ldc + uint64_t(tn) * (P_BN / 64));
 #pragma unroll
-            for (int i = 0; i < kWords / 4; ++i) {
+            for (int i = 0; i < 2; ++i) {
                 uint4 w = make_uint4(words[4 * i], words[4 * i + 1], words[4 * i + 2], words[4 * i + 3]);
                 if (accumulate) {
                     const uint4 o = dst[i];

@@ -226,6 +226,10 @@ __device__ __forceinline__ void tmem_st16_fill(uint32_t taddr, uint32_t x) {
         "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
         "r"(x));
 }
+// 32 lanes x 8 columns store of one 32-bit value per lane and column.
+__device__ __forceinline__ void tmem_st8_fill(uint32_t taddr, uint32_t x) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(x));
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------------------------ descriptors

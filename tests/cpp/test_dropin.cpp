@@ -434,6 +434,36 @@ void host_cases() {
         CHECK(throws<FormatError>([&] { (void)read_bmm1("does/not/exist.bmm"); }));
         std::remove(path.c_str());
     });
+    run("pad_pow2", [] {
+        BitMatrix small = BitMatrix::random(50, 50, 2);
+        BitMatrix padded = pad_pow2(small);
+        CHECK(padded.rows == 64 && padded.cols == 64 && !padded.get(63, 0));
+        CHECK(pad_pow2(BitMatrix::random(100, 200, 3)).rows == 256);
+        BitMatrix exact = BitMatrix::random(128, 128, 4);
+        CHECK(pad_pow2(exact) == exact);
+    });
+    run("auto_plan", [] {
+        LayerPlan p = LayerPlan::auto_plan(4096, 2);
+        CHECK(p.d_serial == 3 && p.d_parallel == 3 && p.matrix_dim() == 4096 && p.workers == 2);
+        CHECK(LayerPlan::auto_plan(16384, 0).workers == 1);
+        CHECK(throws<ShapeError>([] { (void)LayerPlan::auto_plan(96, 1); }));
+    });
+    run("predicted additions and builtins", [] {
+        // reference test_decomposition.cpp:267-294
+        CHECK(predicted_additions(builtin(Builtin::AltSelfInverse), 1, CostPart::LinearCombinations) == 12);
+        CHECK(predicted_additions(builtin(Builtin::AltSelfInverse), 1, CostPart::BasisChanges) == 6);
+        CHECK(predicted_additions(builtin(Builtin::StrassenWinograd), 1, CostPart::LinearCombinations) == 15);
+        CHECK(&decomposition_for(Algo::AltSelfInverse) == &builtin(Builtin::AltSelfInverse));
+        CHECK(throws<std::invalid_argument>([] { (void)decomposition_for(Algo::Cubic); }));
+        CHECK(builtin(Builtin::AltChaining).traits.supports_chaining);
+        CHECK(!builtin(Builtin::AltSelfInverse).traits.supports_chaining);
+    });
+    pipeline_host_cases();
+}
+
+// ------------------------------------------------------------------ gpu cases
+void gpu_cases() {
+    // layout conversions run on the GPU (csrc/layout.cu)
     run("block transpose per bit and involution", [] {
         BitMatrix m = BitMatrix::random(128, 192, 9), t = m;
         transpose_blocks64(t);
@@ -473,35 +503,6 @@ void host_cases() {
         }
         CHECK(throws<ShapeError>([&] { (void)to_interleaved(BitMatrix::zeros(64, 64), p, Operand::Left); }));
     });
-    run("pad_pow2", [] {
-        BitMatrix small = BitMatrix::random(50, 50, 2);
-        BitMatrix padded = pad_pow2(small);
-        CHECK(padded.rows == 64 && padded.cols == 64 && !padded.get(63, 0));
-        CHECK(pad_pow2(BitMatrix::random(100, 200, 3)).rows == 256);
-        BitMatrix exact = BitMatrix::random(128, 128, 4);
-        CHECK(pad_pow2(exact) == exact);
-    });
-    run("auto_plan", [] {
-        LayerPlan p = LayerPlan::auto_plan(4096, 2);
-        CHECK(p.d_serial == 3 && p.d_parallel == 3 && p.matrix_dim() == 4096 && p.workers == 2);
-        CHECK(LayerPlan::auto_plan(16384, 0).workers == 1);
-        CHECK(throws<ShapeError>([] { (void)LayerPlan::auto_plan(96, 1); }));
-    });
-    run("predicted additions and builtins", [] {
-        // reference test_decomposition.cpp:267-294
-        CHECK(predicted_additions(builtin(Builtin::AltSelfInverse), 1, CostPart::LinearCombinations) == 12);
-        CHECK(predicted_additions(builtin(Builtin::AltSelfInverse), 1, CostPart::BasisChanges) == 6);
-        CHECK(predicted_additions(builtin(Builtin::StrassenWinograd), 1, CostPart::LinearCombinations) == 15);
-        CHECK(&decomposition_for(Algo::AltSelfInverse) == &builtin(Builtin::AltSelfInverse));
-        CHECK(throws<std::invalid_argument>([] { (void)decomposition_for(Algo::Cubic); }));
-        CHECK(builtin(Builtin::AltChaining).traits.supports_chaining);
-        CHECK(!builtin(Builtin::AltSelfInverse).traits.supports_chaining);
-    });
-    pipeline_host_cases();
-}
-
-// ------------------------------------------------------------------ gpu cases
-void gpu_cases() {
     run("kernel64 matches the bitwise definition", [] {
         const BitMatrix a = BitMatrix::random(64, 64, 11), b = BitMatrix::random(64, 64, 12);
         BitMatrix bt = b;

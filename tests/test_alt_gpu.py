@@ -249,3 +249,43 @@ def test_multiply_alt_hat_vectors_match_reference_digests(engine, oracle, golden
                                            ctypes.byref(opts)) == 0, lib.bmmgpu_last_error()
             assert f"{oracle.fnv1a64(ch):016x}" == c["fnv"], (c, leaf)
             assert oracle.popcount(ch) == c["pop"] and f"{int(ch[0]):016x}" == c["w0"]
+
+
+@pytest.mark.parametrize("n,tile,leaf", [(1024, 8, 6), (2048, 9, 7), (2048, 10, 8), (4096, 11, 9), (1024, 10, 7), (1024, 9, 12)])
+def test_out_of_core_tiles_equal_cubic(engine, oracle, monkeypatch, n, tile, leaf):
+    """The out-of-core fast product (alt_tiles.cu: C tiles = XOR over K of alt-basis block
+    products of tiles streamed from host memory), forced at small n with small tiles, from
+    pageable and page-locked buffers, for every scheme: the bits of the cubic product."""
+    import torch
+    bmm = engine
+    monkeypatch.setenv("BMMGPU_ALT_TILE", str(tile))
+    a = oracle.random(n, n, 91)
+    b = oracle.random(n, n, 92)
+    want = oracle.multiply_cubic(a, b, n, n, n, GF2)
+    for algo in (bmm.Algo.StrassenWinograd, bmm.Algo.AltSelfInverse, bmm.Algo.AltChaining):
+        got = bmm.multiply(bmm.BitMatrix(n, n, a), bmm.BitMatrix(n, n, b), algo, bmm.LayerPlan.auto_plan(n, 1),
+                           bmm.Semiring.Gf2XorAnd, leaf_log2=leaf, force_streaming=True)
+        assert np.array_equal(got.words, want), (algo, n, tile)
+    ha = torch.from_numpy(a.view(np.int64)).pin_memory()
+    hb = torch.from_numpy(b.view(np.int64)).pin_memory()
+    hc = torch.zeros(n * n // 64, dtype=torch.int64).pin_memory()
+    got = bmm.multiply(bmm.BitMatrix(n, n, ha.numpy().view(np.uint64)), bmm.BitMatrix(n, n, hb.numpy().view(np.uint64)),
+                       bmm.Algo.AltSelfInverse, bmm.LayerPlan.auto_plan(n, 1), bmm.Semiring.Gf2XorAnd,
+                       leaf_log2=leaf, force_streaming=True, out=bmm.BitMatrix(n, n, hc.numpy().view(np.uint64)))
+    assert np.array_equal(got.words, want)
+
+
+def test_out_of_core_tiles_by_budget(engine, oracle, monkeypatch):
+    """A device budget below six n^2/8 arrays selects the out-of-core driver without the
+    force flag (golden n = 4096 alt-si product of the reference's seeds)."""
+    bmm = engine
+    monkeypatch.setenv("BMMGPU_ALT_TILE", "11")
+    n = 4096
+    a = oracle.random(n, n, 1)
+    b = oracle.random(n, n, 2)
+    want = oracle.multiply_cubic(a, b, n, n, n, GF2)
+    got = bmm.multiply(bmm.BitMatrix(n, n, a), bmm.BitMatrix(n, n, b), bmm.Algo.AltSelfInverse,
+                       bmm.LayerPlan.auto_plan(n, 1), bmm.Semiring.Gf2XorAnd, leaf_log2=9,
+                       device_budget=6 * n * n // 8 - 1)
+    assert np.array_equal(got.words, want)
+    assert engine.lib().bmmgpu_last_launch_count() > 8  # 2 x 2 tiles x 2 K-blocks

@@ -180,3 +180,24 @@ def test_out_of_core_two_ranks_share_host_b():
     d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
     assert d["n_gpus"] == 2 and d["spot_check"] is True and d["config"]["rows_per_rank"] == 16384
     assert {f for f in os.listdir("/dev/shm") if f.startswith("bmm_B_32768")} <= before  # nothing left behind
+
+
+@pytest.mark.gpu
+def test_out_of_core_alt_tiles_two_ranks():
+    """Out-of-core fast product under two ranks: each rank runs its run of output row
+    panels (bmmgpu_multiply_panels, alt-si block products in 4096-bit tiles) with B in
+    shared host memory; every slab is checked by Freivalds and numpy rows / a column."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, BMM_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29537", "bench.py", "--gpus", "2", "--workload",
+           "c5s-gf2-altooc-32768", "--steps", "1", "--warmup", "1", "--alt-tile-log2", "12", "--leaf-log2", "10",
+           "--check"]
+    r = subprocess.run(cmd, cwd=str(ROOT), env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d["n_gpus"] == 2 and d["spot_check"] is True and d["config"]["rows_per_rank"] == 16384
+    assert d["parity"]["freivalds_64_columns"] is True and d["config"]["algo"] == "alt-si"
