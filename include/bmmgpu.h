@@ -77,6 +77,12 @@ typedef struct bmmgpu_plan {
 
 /* ---------------------------------------------------------------- host API */
 
+/* Optional warm-up of the devices in device_mask (0 = device 0): loads every kernel (one
+ * tiny product of each kind), fills the stream pool and, with reserve_bytes > 0, grows the
+ * device's stream-ordered memory pool by that much, so the first timed call costs what
+ * later calls cost.  Calls without it stay correct; they pay the warm-up once. */
+int bmmgpu_init(uint32_t device_mask, uint64_t reserve_bytes);
+
 /* C (m x n) = A (m x k) . B (k x n) over the semiring.  Host row-major buffers
  * (A: m*ceil(k/64) words, B: k*ceil(n/64), C: m*ceil(n/64), written in full,
  * pad bits zero).  Any shape, including non-multiples of 64 and empty

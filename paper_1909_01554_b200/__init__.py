@@ -119,6 +119,10 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_host_alloc.restype = ctypes.c_int
         L.bmmgpu_host_free.argtypes = [vp]
         L.bmmgpu_host_free.restype = ctypes.c_int
+        L.bmmgpu_init.argtypes = [ctypes.c_uint32, u64]
+        L.bmmgpu_init.restype = ctypes.c_int
+        L.bmmgpu_multiply_panels.argtypes = [vp, vp, vp, u64, i32, i32, u64, u64, ctypes.POINTER(_Opts)]
+        L.bmmgpu_multiply_panels.restype = ctypes.c_int
         L.bmmgpu_layout.argtypes = [vp, vp, u64, u64, i32, ctypes.POINTER(_Opts)]
         L.bmmgpu_layout.restype = ctypes.c_int
         L.bmmgpu_dev_layout.argtypes = [vp, vp, u64, u64, i32, vp]
@@ -146,6 +150,12 @@ def _check(status: int) -> None:
     if status == 1:
         raise ValueError(msg)  # std::invalid_argument
     raise EngineError(msg)
+
+
+def init(device_mask: int = 0, reserve_bytes: int = 0) -> None:
+    """bmmgpu_init: load every kernel and warm the stream / memory pools of the devices in
+    `device_mask` (0: device 0), optionally reserving `reserve_bytes` of HBM in the pool."""
+    _check(lib().bmmgpu_init(device_mask, reserve_bytes))
 
 
 def device_count() -> int:

@@ -43,6 +43,9 @@ namespace bmmgpu {
 
 int launch_transpose(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
                      uint64_t kw, cudaStream_t stream);
+int launch_cubic_fold(const uint64_t* dApar, uint64_t ld_a, uint64_t s_a, const uint64_t* dBtpar, uint64_t ld_b,
+                      uint64_t s_b, uint64_t parents, uint64_t L, uint32_t ma, uint32_t mb, uint64_t* dQ, uint64_t ldq,
+                      uint64_t s_q, cudaStream_t stream);
 int launch_transpose_ld(const uint64_t* dB, uint64_t ldb, uint64_t k, uint64_t n, uint64_t* dBt, uint64_t n_pad,
                         uint64_t kw, uint64_t ldbt, cudaStream_t stream);
 int launch_cubic(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC,
@@ -357,6 +360,12 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
     uint64_t gm, gn, gk;
     if ((st = granularity(kernel, &gm, &gn, &gk))) return st;
     const uint64_t L = n >> e;
+    // Level shifting (reference fused_block_stage, engine.cpp:202-228): with the tensor-core
+    // kernel and tile-aligned leaves the last expand level runs inside the leaf launch (K2
+    // fold mode forms each leaf operand from its parent's quadrants), so level e is never
+    // materialised.  BMMGPU_ALT_FOLD=1 turns it on (read per call: tests switch it).
+    const char* fold_env = getenv("BMMGPU_ALT_FOLD");
+    const bool fold = fold_env && *fold_env == '1' && resolve_kernel(kernel) == BMMGPU_KERNEL_UMMA_F4 && L % 256 == 0;
     // Leaf panels padded to the kernel's tiles (pads stay zero).
     const uint64_t t_rows = round_up(L, gm), s_rows = round_up(L, gn);
     const uint64_t kwl = round_up(L / 64, gk / 64);
@@ -388,11 +397,13 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
     s_ld[0] = ldbt;
     t_bs[0] = s_bs[0] = 0;
     const std::vector<int> lv = pass_levels(e);
+    const std::vector<int> lv_expand = fold ? pass_levels(e - 1) : lv;
 
     // Expand, one or two levels per pass, freeing each parent level once consumed.
     const uint64_t* tin = dA;
     const uint64_t* sin = dBt;
-    for (size_t i = 0; i + 1 < lv.size(); ++i) {
+    for (size_t i = 0; i + 1 < lv_expand.size(); ++i) {
+        const std::vector<int>& lv = lv_expand;
         const int l0 = lv[i], l1 = lv[i + 1];
         const uint64_t Pn = pow7(l1);
         const size_t tb = size_t(Pn * t_bs[l1] * 8), sb = size_t(Pn * s_bs[l1] * 8);
@@ -419,15 +430,33 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
     DevMem Q;
     const uint64_t q_bs = t_rows * cwl;
     if ((st = Q.alloc(size_t(batch * q_bs * 8), s))) return st;
-    for (uint64_t b0 = 0; b0 < batch; b0 += 65535) {
+    if (fold) {
+        // leaf 7 p + h from parent p of level e - 1 (the operands themselves when e = 1)
+        uint32_t pma = 0, pmb = 0;
+        for (int h = 0; h < 7; ++h) {
+            pma |= uint32_t(ma.m[h]) << (4 * h);
+            pmb |= uint32_t(mb.m[h]) << (4 * h);
+        }
+        const int lp = e - 1;
+        if ((st = launch_cubic_fold(tin, t_ld[lp], t_bs[lp], sin, s_ld[lp], s_bs[lp], pow7(lp), L, pma, pmb, Q.u(), cwl,
+                                    q_bs, s)))
+            return st;
+        if (lp > 0) {
+            T[lp].release();
+            S[lp].release();
+        }
+    }
+    for (uint64_t b0 = 0; b0 < (fold ? 0 : batch); b0 += 65535) {
         const uint64_t nb = std::min<uint64_t>(65535, batch - b0);
         if ((st = launch_cubic(kernel, T[e].u() + b0 * t_bs[e], kwl, S[e].u() + b0 * s_bs[e], kwl,
                                Q.u() + b0 * q_bs, cwl, t_rows, s_rows, kwl, true, false, s, nb, t_bs[e], s_bs[e],
                                q_bs)))
             return st;
     }
-    T[e].release();
-    S[e].release();
+    if (!fold) {
+        T[e].release();
+        S[e].release();
+    }
 
     // Compress back up the same levels into dC.
     DevMem cur = std::move(Q), nxt;

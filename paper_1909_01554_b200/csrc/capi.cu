@@ -288,6 +288,34 @@ int launch_cubic_kernel(int kernel, const uint64_t* dA, uint64_t lda, const uint
                         uint64_t* dC, uint64_t ldc, uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2,
                         bool accumulate, cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch,
                         uint64_t sC_batch);
+int launch_cubic_umma_fold(const uint64_t* dApar, uint64_t ld_a, uint64_t s_a, const uint64_t* dBtpar, uint64_t ld_b,
+                           uint64_t s_b, uint64_t parents, uint64_t L, uint32_t ma, uint32_t mb, uint64_t* dQ,
+                           uint64_t ldq, uint64_t s_q, bool gf2, cudaStream_t stream);
+
+// Level-shifted leaf layer (K2 fold mode), bracketed by the block timer like launch_cubic.
+int launch_cubic_fold(const uint64_t* dApar, uint64_t ld_a, uint64_t s_a, const uint64_t* dBtpar, uint64_t ld_b,
+                      uint64_t s_b, uint64_t parents, uint64_t L, uint32_t ma, uint32_t mb, uint64_t* dQ, uint64_t ldq,
+                      uint64_t s_q, cudaStream_t stream) {
+    bool timed;
+    {
+        std::lock_guard<std::mutex> lk(g_timer.mu);
+        timed = g_timer.on;
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed) {
+        BMMGPU_CUDA_TRY(cudaEventCreate(&e0));
+        BMMGPU_CUDA_TRY(cudaEventCreate(&e1));
+        BMMGPU_CUDA_TRY(cudaEventRecord(e0, stream));
+    }
+    const int st = launch_cubic_umma_fold(dApar, ld_a, s_a, dBtpar, ld_b, s_b, parents, L, ma, mb, dQ, ldq, s_q, true,
+                                          stream);
+    if (timed) {
+        BMMGPU_CUDA_TRY(cudaEventRecord(e1, stream));
+        std::lock_guard<std::mutex> lk(g_timer.mu);
+        g_timer.spans.emplace_back(e0, e1);
+    }
+    return st;
+}
 
 // The tensor-core kernels count in fp32 (exact below 2^23 terms): longer inner
 // dimensions run as K-chunks folded into C with the accumulate flag -- the

@@ -91,12 +91,18 @@ constexpr int P_THREADS = P_PRODUCERS + 32 + 32 * P_EPI_WARPS + P_LOADERS;
 constexpr int P_SST_SLOTS = BMMGPU_SST_SLOTS;  // packed ring slots, one superstage (4 stages) each
 constexpr int P_SST_OP = P_ROWS * 128;         // one operand of a superstage: 128 rows x 128 bytes
 constexpr int P_SST = 2 * P_SST_OP;            // 32 KB
+// Level-shifted leaves (kFold): the packed region is a ring of units, one TMA box of one
+// parent quadrant for one superstage: 128 rows x 128 bytes with the 128-byte swizzle (4 KB
+// boxes of one stage each measured 2.6x slower: the TMA row-request rate, not bytes).
+constexpr int P_UNIT = P_ROWS * 128;           // 16 KB
+// as many units as shared memory leaves after the operand ring and the bias constants
+constexpr int P_UNITS = int((232448 - 2048 - size_t(P_STAGES) * P_STAGE - P_REGION - 1024) / P_UNIT);
+constexpr int P_PACKED = P_UNITS * P_UNIT > P_SST_SLOTS * P_SST ? P_UNITS * P_UNIT : P_SST_SLOTS * P_SST;
 static_assert(P_STAGES % 2 == 0, "the two expander groups alternate ring slots");
 // One K = 64 operand region of constants for the bias MMA (rows of 32 e2m1 ones, then
 // zeros); A and Bt of the bias MMA both read it.
 constexpr int P_CONST = P_REGION;
-constexpr size_t P_SMEM =
-    size_t(P_STAGES) * P_STAGE + size_t(P_SST_SLOTS) * P_SST + P_CONST + 1024;  // + alignment slack
+constexpr size_t P_SMEM = size_t(P_STAGES) * P_STAGE + size_t(P_PACKED) + P_CONST + 1024;  // + alignment slack
 constexpr uint32_t P_TMEM_COLS = 512;
 // Block scales (UE8M0, uniform): an M128 / N128-per-CTA operand's scales take 4 TMEM
 // columns (rows 32 q + i in lane i, replicated over the 4 lane quarters); 8 each.
@@ -346,13 +352,23 @@ __device__ __forceinline__ void drain_accumulator_gf2_pack16(uint32_t tacc, uint
 
 // kTma: the packed superstages arrive by TMA (one 3-D tiled box per operand, 128-byte
 // swizzle, K tail zero-filled by the bounds check) instead of the cp.async loader warps.
-template <bool kTma>
+// kFold (level shifting, reference engine.cpp:202-228 fused_block_stage / PAPER.md "shifting
+// levels between layers"): product b of the batch is leaf h = b % 7 of parent p = b / 7, and
+// its operands are never materialised -- per superstage the loader brings the parent
+// quadrants the fused alpha.phi / beta.psi row of h selects (one 128-row x 128-byte TMA box
+// each, into a ring of P_UNITS units) and the expanders XOR them in registers before the
+// e2m1 expansion.  Masks: 4 bits per child, child h at bits 4h.
+struct FoldSpec {
+    uint32_t ma, mb;  // A / Bt quadrant masks of the 7 children
+    uint32_t L;       // leaf rows (the parent is 2L x 2L; quadrant q at rows (q >> 1) L, words (q & 1) L / 64)
+};
+template <bool kTma, bool kFold>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     cubic_umma2_kernel(const uint64_t* __restrict__ A, uint64_t lda, const uint64_t* __restrict__ Bt, uint64_t ldbt,
                        uint64_t* __restrict__ C, uint64_t ldc, uint64_t kw, int flags, TileMap map,
                        uint32_t total_tiles, uint32_t epi_sleep_ns, unsigned long long* wave_ctr,
                        const __grid_constant__ CUtensorMap tmA,
-                       const __grid_constant__ CUtensorMap tmB) {
+                       const __grid_constant__ CUtensorMap tmB, FoldSpec fold) {
     extern __shared__ uint8_t smem_raw[];
     // semiring as a runtime flag: one compiled main loop serves both (a template
     // parameter let the two instantiations schedule the producer loop differently)
@@ -365,6 +381,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     __shared__ __align__(8) uint64_t acc_full_bar[2];   // per accumulator (X, Y)
     __shared__ __align__(8) uint64_t acc_empty_bar[2];
     __shared__ __align__(8) uint64_t ovl_bar;           // overlap columns of the last tile drained
+    __shared__ __align__(8) uint64_t unit_full_bar[kFold ? P_UNITS : 1];
+    __shared__ __align__(8) uint64_t unit_empty_bar[kFold ? P_UNITS : 1];
     __shared__ uint32_t tmem_base_sh;
 
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -388,6 +406,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             umma::mbar_init(&acc_empty_bar[i], 2 * P_EPI_WARPS);
         }
         umma::mbar_init(&ovl_bar, 2 * P_EPI_WARPS);
+        if (kFold)
+            for (int u = 0; u < P_UNITS; ++u) {
+                umma::mbar_init(&unit_full_bar[u], 1);
+                umma::mbar_init(&unit_empty_bar[u], P_PRODUCERS / 32);  // every expander warp
+            }
         umma::mbar_fence_init();
     }
     umma::fence_before_sync();
@@ -404,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     {
         // bias operand: row r holds 32 e2m1 ones (0x22 bytes) in its logical 16-byte chunk 0
         // (physical chunk 0 ^ (r & 7) of the 128-byte swizzle), zeros elsewhere
-        uint8_t* cst = smem + size_t(P_STAGES) * P_STAGE + size_t(P_SST_SLOTS) * P_SST;
+        uint8_t* cst = smem + size_t(P_STAGES) * P_STAGE + size_t(P_PACKED);
         for (uint32_t i = tid; i < uint32_t(P_CONST / 16); i += blockDim.x) {
             const uint32_t r = i >> 3, phys = i & 7;
             const uint32_t v = (phys ^ (r & 7)) == 0 ? 0x22222222u : 0u;
@@ -416,7 +439,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     umma::cluster_sync();  // barriers of both CTAs initialised, TMEM of both allocated and scaled
     umma::fence_after_sync();
 
-    if (warp < P_PRODUCERS / 32) {
+    if (kFold && warp < P_PRODUCERS / 32) {
+        // ------------------------------------------------ expanders, level-shifted leaves: as the
+        // plain expanders (group grp takes 2 of the 4 stages of a superstage), but a
+        // superstage's packed bits are the XOR of its units -- the selected parent quadrants
+        // of A, then of Bt, in the loader's order; each unit is freed once every expander
+        // warp has read its rows from it.
+        const uint32_t grp = warp >> 2, r = tid & (P_ROWS - 1), rsw = r & 7;
+        const uint32_t full_leader0 = umma::mapa_shared(smem_u32(&full_bar[0]), 0);
+        const uint8_t* urow = smem + size_t(P_STAGES) * P_STAGE + r * 128;
+        uint64_t base = 0;  // global stage index of stage 0 of the current tile
+        uint64_t un = 0;    // units consumed
+        for (uint32_t t = pair; t < total_tiles; t += n_pairs, base += n_stages) {
+            uint32_t b, tm, tn;
+            map.decode(t, b, tm, tn);
+            const uint32_t h = b % 7, ma = (fold.ma >> (4 * h)) & 15u, mb = (fold.mb >> (4 * h)) & 15u;
+            const uint32_t wa = __popc(ma), wab = wa + __popc(mb);
+            const uint32_t sub0 = (uint32_t(base) ^ grp) & 1;
+            for (uint64_t k0 = 0; k0 < n_stages; k0 += 4, un += wab) {
+                uint4 v[2][4];  // [stage][A lo, A hi, Bt lo, Bt hi]
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) v[j][c] = make_uint4(0, 0, 0, 0);
+                for (uint32_t i = 0; i < wab; ++i) {
+                    const uint64_t ui = un + i;
+                    const uint32_t u = uint32_t(ui % P_UNITS);
+                    umma::mbar_wait(&unit_full_bar[u], uint32_t((ui / P_UNITS) & 1));
+                    const uint8_t* q = urow + size_t(u) * P_UNIT;
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const uint32_t c = 2 * (sub0 + 2 * j);
+                        const uint4 x0 = *reinterpret_cast<const uint4*>(q + ((c ^ rsw) << 4));
+                        const uint4 x1 = *reinterpret_cast<const uint4*>(q + (((c + 1) ^ rsw) << 4));
+                        if (i < wa) {
+                            v[j][0] = make_uint4(v[j][0].x ^ x0.x, v[j][0].y ^ x0.y, v[j][0].z ^ x0.z, v[j][0].w ^ x0.w);
+                            v[j][1] = make_uint4(v[j][1].x ^ x1.x, v[j][1].y ^ x1.y, v[j][1].z ^ x1.z, v[j][1].w ^ x1.w);
+                        } else {
+                            v[j][2] = make_uint4(v[j][2].x ^ x0.x, v[j][2].y ^ x0.y, v[j][2].z ^ x0.z, v[j][2].w ^ x0.w);
+                            v[j][3] = make_uint4(v[j][3].x ^ x1.x, v[j][3].y ^ x1.y, v[j][3].z ^ x1.z, v[j][3].w ^ x1.w);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) umma::mbar_arrive(&unit_empty_bar[u]);
+                }
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const uint64_t k = k0 + sub0 + 2 * j;
+                    if (k >= n_stages) break;
+                    const uint64_t it = base + k;
+                    const uint32_t s = uint32_t(it % P_STAGES);
+                    if (it >= P_STAGES) umma::mbar_wait(&empty_bar[s], uint32_t((it / P_STAGES - 1) & 1));
+                    uint8_t* sa = smem + size_t(s) * P_STAGE;
+                    expand_store_sw128(sa, r, 0, v[j][0]);
+                    expand_store_sw128(sa, r, 1, v[j][1]);
+                    expand_store_sw128(sa + P_REGION, r, 0, v[j][2]);
+                    expand_store_sw128(sa + P_REGION, r, 1, v[j][3]);
+                    umma::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) umma::mbar_arrive_cluster(full_leader0 + s * 8);
+                }
+            }
+        }
+    } else if (warp < P_PRODUCERS / 32) {
         // ------------------------------------------------ expanders: two groups of 4 warps take
         // alternate stages (global stage parity = group), thread r of a group owns row r of A
         // and of Bt.  While one group drains its stores through the proxy fence the other
@@ -489,7 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             constexpr uint32_t idesc = umma::idesc_mxf4(P_BM, P_BN);
             const uint64_t desc_base = umma::smem_desc_sw128(smem_u32(smem), 1024);
             const uint64_t desc_const = umma::smem_desc_sw128(
-                smem_u32(smem + size_t(P_STAGES) * P_STAGE + size_t(P_SST_SLOTS) * P_SST), 1024);
+                smem_u32(smem + size_t(P_STAGES) * P_STAGE + size_t(P_PACKED)), 1024);
             uint64_t it = 0;
             int s = 0;
             uint32_t full_parity = 0;
@@ -546,6 +631,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             pw[5] = clock64() - p_t0;
 #endif
             PSTORE(3, 5, lane == 0);
+        }
+    } else if (kFold && warp >= P_LOADER_WARP0) {
+        // ------------------------------------------------ loader, level-shifted leaves: per superstage
+        // one 128-row x 128-byte box (4 stages) per selected parent quadrant, A then Bt.
+        if (tid == P_LOADER_WARP0 * 32) {
+            umma::tma_prefetch_desc(&tmA);
+            umma::tma_prefetch_desc(&tmB);
+            uint8_t* units = smem + size_t(P_STAGES) * P_STAGE;
+            const int32_t kq = int32_t(fold.L / 64);
+            uint64_t un = 0;
+            for (uint32_t t = pair; t < total_tiles; t += n_pairs) {
+                uint32_t b, tm, tn;
+                map.decode(t, b, tm, tn);
+                const uint32_t h = b % 7, par = b / 7;
+                const uint32_t ma = (fold.ma >> (4 * h)) & 15u, mb = (fold.mb >> (4 * h)) & 15u;
+                const int32_t ra = int32_t(tm * P_BM + rank * P_ROWS), rb = int32_t(tn * P_BN + rank * P_ROWS);
+                for (uint64_t k0 = 0; k0 < n_stages; k0 += 4)
+                    for (uint32_t i = 0; i < 8; ++i) {
+                        const uint32_t q = i & 3, m = i < 4 ? ma : mb;
+                        if (!((m >> q) & 1)) continue;
+                        const uint32_t u = uint32_t(un % P_UNITS);
+                        if (un >= P_UNITS) umma::mbar_wait(&unit_empty_bar[u], uint32_t((un / P_UNITS - 1) & 1));
+                        umma::mbar_arrive_expect_tx(&unit_full_bar[u], P_UNIT);
+                        const int32_t kc = int32_t(k0 * 4) + int32_t(q & 1) * kq;
+                        const int32_t row = (i < 4 ? ra : rb) + int32_t(q >> 1) * int32_t(fold.L);
+                        umma::tma_load_3d(units + size_t(u) * P_UNIT, i < 4 ? &tmA : &tmB, kc, row, int32_t(par),
+                                          &unit_full_bar[u]);
+                        ++un;
+                    }
+            }
         }
     } else if (kTma && warp >= P_LOADER_WARP0) {
         // ------------------------------------------------ loader: one thread issues two TMA boxes per superstage
@@ -818,7 +933,7 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
     const bool tma = !(ld_env && !strcmp(ld_env, "cpasync")) &&
                      make_operand_map(&tmA, dA, kw, m_pad, lda, batch, sA_batch) &&
                      make_operand_map(&tmB, dBt, kw, n_pad, ldbt, batch, sB_batch);
-    auto kern = tma ? cubic_umma2_kernel<true> : cubic_umma2_kernel<false>;
+    auto kern = tma ? cubic_umma2_kernel<true, false> : cubic_umma2_kernel<false, false>;
     BMMGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P_SMEM)));
     const char* probe = getenv("BMMGPU_UMMA_PROBE");
     const uint64_t n_stages_l = kw * 64 / P_KBITS;
@@ -844,7 +959,64 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
         g_wave_aligned_launches.fetch_add(1, std::memory_order_relaxed);
     }
     kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dA, lda, dBt, ldbt, dC, ldc, kw, flags, map,
-                                                             uint32_t(total), epi_sleep, wave_ctr, tmA, tmB);
+                                                             uint32_t(total), epi_sleep, wave_ctr, tmA, tmB,
+                                                             FoldSpec{0, 0, 0});
+    count_launch();
+    BMMGPU_CUDA_TRY(cudaGetLastError());
+    return kOk;
+}
+
+// Tensor map of a parent array for the level-shifted leaves: [parents][2L rows][ld words],
+// box 16 words (one superstage, 128 bytes) x 128 rows x 1, 128-byte swizzle = the unit layout.
+static bool make_parent_map(CUtensorMap* m, const uint64_t* base, uint64_t L, uint64_t ld, uint64_t parents,
+                            uint64_t s_parent) {
+    const EncodeTiledFn fn = encode_tiled();
+    if (!fn || L % 256 || ld % 2 || (parents > 1 && s_parent % 2) || (reinterpret_cast<uintptr_t>(base) & 15))
+        return false;
+    if (s_parent == 0) parents = 1;
+    const cuuint64_t dims[3] = {2 * L / 64, 2 * L, parents};
+    const cuuint64_t strides[2] = {ld * 8, (parents > 1 ? s_parent : 2 * L * ld) * 8};
+    const cuuint32_t box[3] = {16, uint32_t(P_ROWS), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CUtensorMapL2promotion(BMMGPU_L2_PROMOTION),
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Level-shifted leaf layer: the 7 * parents products Q[7 p + h] = T_h . S_h^T of L x L
+// leaves whose operands T_h = XOR_{q in ma_h} A_p quadrant q, S_h = XOR_{q in mb_h} Bt_p
+// quadrant q are formed inside the kernel from the parents (2L x 2L, row strides
+// ld_a / ld_b, parent strides s_a / s_b; s = 0: one parent).  Q row-major L x L / 64 per
+// product, stride ldq, product stride s_q.  Returns kEinval when the shapes do not allow
+// it (L not a multiple of 256, unaligned strides): the caller materialises the leaves.
+int launch_cubic_umma_fold(const uint64_t* dApar, uint64_t ld_a, uint64_t s_a, const uint64_t* dBtpar, uint64_t ld_b,
+                           uint64_t s_b, uint64_t parents, uint64_t L, uint32_t ma, uint32_t mb, uint64_t* dQ,
+                           uint64_t ldq, uint64_t s_q, bool gf2, cudaStream_t stream) {
+    CUtensorMap tmA{}, tmB{};
+    if (L % P_BM || ldq % 4 || L / 64 >= (uint64_t(1) << 17) ||
+        !make_parent_map(&tmA, dApar, L, ld_a, parents, s_a) || !make_parent_map(&tmB, dBtpar, L, ld_b, parents, s_b)) {
+        set_error("umma2 fold: shapes not supported");
+        return kEinval;
+    }
+    const uint64_t kw = L / 64;
+    const uint64_t m_tiles = L / P_BM, per_prod = m_tiles * m_tiles, total = per_prod * 7 * parents;
+    if (total > 0xffffffffull) {
+        set_error("umma2 fold: too many tiles");
+        return kEinval;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t pairs = std::min<uint64_t>(total, std::min<uint64_t>(P_MAX_PAIRS, std::max(1, sms / 2)));
+    TileMap map{uint32_t(m_tiles), uint32_t(m_tiles), uint32_t(per_prod), 0, 0, s_q};
+    auto kern = cubic_umma2_kernel<true, true>;
+    BMMGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P_SMEM)));
+    const uint64_t n_stages = kw * 64 / P_KBITS;
+    const uint32_t epi_sleep = n_stages >= 128 ? BMMGPU_EPI_SLEEP : n_stages >= 32 ? 64 : 0;
+    const int flags = gf2 ? 2 : 0;
+    kern<<<unsigned(2 * pairs), P_THREADS, P_SMEM, stream>>>(dApar, ld_a, dBtpar, ld_b, dQ, ldq, kw, flags, map,
+                                                             uint32_t(total), epi_sleep, nullptr, tmA, tmB,
+                                                             FoldSpec{ma, mb, uint32_t(L)});
     count_launch();
     BMMGPU_CUDA_TRY(cudaGetLastError());
     return kOk;

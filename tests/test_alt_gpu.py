@@ -289,3 +289,22 @@ def test_out_of_core_tiles_by_budget(engine, oracle, monkeypatch):
                        device_budget=6 * n * n // 8 - 1)
     assert np.array_equal(got.words, want)
     assert engine.lib().bmmgpu_last_launch_count() > 8  # 2 x 2 tiles x 2 K-blocks
+
+
+@pytest.mark.parametrize("leaf", [8, 9, 10, 12])
+def test_level_shifted_leaves_match_reference(engine, oracle, golden, monkeypatch, leaf):
+    """K2 fold mode (BMMGPU_ALT_FOLD=1: the last expand level formed inside the leaf
+    kernel from the parents' quadrants, reference fused_block_stage engine.cpp:202-228)
+    gives the reference's bits for every scheme; at leaf 12 with n = 4096 the parents are
+    the operands themselves (e = 1)."""
+    monkeypatch.setenv("BMMGPU_ALT_FOLD", "1")
+    test_fast_products_match_reference(engine, oracle, golden, leaf)
+    bmm = engine
+    for n, seed in ((4096, 1), (2048, 7)):
+        a = oracle.random(n, n, seed)
+        b = oracle.random(n, n, seed + 1)
+        want = oracle.multiply_cubic(a, b, n, n, n, GF2)
+        for algo in (bmm.Algo.StrassenWinograd, bmm.Algo.AltSelfInverse, bmm.Algo.AltChaining):
+            got = bmm.multiply(bmm.BitMatrix(n, n, a), bmm.BitMatrix(n, n, b), algo, bmm.LayerPlan.auto_plan(n, 1),
+                               bmm.Semiring.Gf2XorAnd, leaf_log2=leaf)
+            assert np.array_equal(got.words, want), (algo, n, leaf)

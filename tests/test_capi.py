@@ -37,6 +37,19 @@ def test_library_exports_every_declared_symbol():
     assert b"sm_100a" in lib.bmmgpu_version()
 
 
+def test_python_mirror_declares_every_signature():
+    """Every entry point with parameters has ctypes argtypes in the mirror (an undeclared
+    one would pass 64-bit pointers and sizes as C ints)."""
+    import paper_1909_01554_b200 as bmm
+    lib = bmm.lib()
+    text = HEADER.read_text()
+    for name in _declared():
+        params = re.search(rf"{name}\s*\(([^)]*)\)", text).group(1).strip()
+        if params in ("", "void"):
+            continue
+        assert getattr(lib, name).argtypes is not None, name
+
+
 def test_dropin_library_exports_the_bmm_api():
     import paper_1909_01554_b200 as bmm
     ctypes.CDLL(str(bmm.HOST_LIB_PATH))
@@ -61,10 +74,10 @@ def test_kernels_are_sm100a_native():
     # STTM), the pair's TMEM allocator and commit barriers, 3-D tensor-map loads
     fns = sass.split("Function : ")
     k2 = [f for f in fns if "cubic_umma2_kernel" in f.splitlines()[0]]
-    assert len(k2) == 2, "the TMA and the cp.async-loader instantiations"
+    assert len(k2) == 3, "the TMA, the cp.async-loader and the level-shifted (fold) instantiations"
     for op in ("UTCOMMA.2CTA", "LDTM", "STTM", "UTCATOMSWS.2CTA", "UTCBAR.2CTA"):
         assert all(op in f for f in k2), op
-    assert any("UTMALDG.3D" in f for f in k2)
+    assert sum("UTMALDG.3D" in f for f in k2) == 2  # TMA loaders: plain and fold
 
 
 @pytest.mark.skipif(HAS_GPU, reason="checks the no-device path")
@@ -117,3 +130,19 @@ def test_random_generator_matches_oracle(oracle):
     for rows, cols, seed in [(130, 130, 7), (64, 64, 5), (3, 700, 9), (1000, 1, 4)]:
         m = bmm.BitMatrix.random(rows, cols, seed)
         assert np.array_equal(m.words, oracle.random(rows, cols, seed))
+
+
+@pytest.mark.gpu
+def test_init_warms_the_device_and_products_stay_exact(engine, oracle):
+    """bmmgpu_init (every kernel once, stream pool, 1 GiB pool reserve) leaves the engine
+    in a state where products are unchanged (alt-si through the level-shifted leaves)."""
+    import numpy as np
+    engine.init(0, 1 << 30)
+    n = 1024
+    a = oracle.random(n, n, 5)
+    b = oracle.random(n, n, 6)
+    got = engine.multiply(engine.BitMatrix(n, n, a), engine.BitMatrix(n, n, b), engine.Algo.AltSelfInverse,
+                          engine.LayerPlan.auto_plan(n, 1), engine.Semiring.Gf2XorAnd, leaf_log2=8)
+    assert np.array_equal(got.words, oracle.multiply_cubic(a, b, n, n, n, 1))
+    with pytest.raises(ValueError):
+        engine.init(1 << 30, 0)  # a device that does not exist

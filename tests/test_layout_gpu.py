@@ -53,7 +53,7 @@ def test_layout_shape_errors(engine):
         engine.transpose_blocks64(engine.BitMatrix.zeros(64, 100))
     with pytest.raises(engine.ShapeError):
         engine.to_interleaved(engine.BitMatrix.zeros(64, 64), engine.LayerPlan(0, 0, 1, 1, 1), engine.Operand.Left)
-    w = np.zeros(64 * 96 // 64, dtype=np.uint64)
+    w = np.zeros(96 * 2, dtype=np.uint64)
     with pytest.raises(engine.ShapeError):  # interleave needs n = 64 * 2^d
         engine.layout(w, w.copy(), 96, 96, engine.LAYOUT_TO_INTERLEAVED)
     with pytest.raises(ValueError):  # interleave is out of place
