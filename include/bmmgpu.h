@@ -258,6 +258,8 @@ int bmmgpu_host_free(void* ptr);
 int bmmgpu_last_copy_bytes(uint64_t* h2d, uint64_t* d2h);
 
 int bmmgpu_device_count(void);
+/* Free and total HBM bytes of a device (cudaMemGetInfo). */
+int bmmgpu_mem_info(int32_t device, uint64_t* free_bytes, uint64_t* total_bytes);
 
 /* Debug: tensor-core launches that ran with wave-aligned loaders (long-K products with
  * more output tiles than CTA pairs) and loaders that stopped aligning at the spin limit,

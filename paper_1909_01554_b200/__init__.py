@@ -119,6 +119,8 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_host_alloc.restype = ctypes.c_int
         L.bmmgpu_host_free.argtypes = [vp]
         L.bmmgpu_host_free.restype = ctypes.c_int
+        L.bmmgpu_mem_info.argtypes = [i32, _u64p, _u64p]
+        L.bmmgpu_mem_info.restype = ctypes.c_int
         L.bmmgpu_init.argtypes = [ctypes.c_uint32, u64]
         L.bmmgpu_init.restype = ctypes.c_int
         L.bmmgpu_multiply_panels.argtypes = [vp, vp, vp, u64, i32, i32, u64, u64, ctypes.POINTER(_Opts)]

@@ -611,6 +611,19 @@ int bmmgpu_device_count(void) {
     return c;
 }
 
+int bmmgpu_mem_info(int32_t device, uint64_t* free_bytes, uint64_t* total_bytes) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    BMMGPU_CUDA_TRY(cudaSetDevice(device));
+    size_t f = 0, t = 0;
+    const cudaError_t e = cudaMemGetInfo(&f, &t);
+    cudaSetDevice(prev);
+    BMMGPU_CUDA_TRY(e);
+    if (free_bytes) *free_bytes = f;
+    if (total_bytes) *total_bytes = t;
+    return kOk;
+}
+
 int bmmgpu_dev_granularity(int32_t kernel, uint64_t* m_gran, uint64_t* n_gran, uint64_t* k_gran_bits) {
     return granularity(kernel, m_gran, n_gran, k_gran_bits);
 }

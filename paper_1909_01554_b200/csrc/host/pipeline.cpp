@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <cstdlib>
 #include <exception>
 #include <mutex>
 #include <stdexcept>
@@ -258,6 +259,48 @@ BitVectorTensor coordinate(const BitVectorTensor& a_hat, const BitVectorTensor& 
     st.prepared_left.assign(subs, 0);
     st.prepared_right.assign(subs, 0);
     st.aggregated.assign(subs, 0);
+
+    // Operands that fit in HBM: the host layer runs on the device.  In the alternative
+    // basis the d_host host levels are the top levels of the same bilinear recursion, so
+    // the whole product is one bmmgpu_multiply_alt over d_host + sub_depth levels -- its
+    // sub-instances formed from HBM-resident operands (40x host DRAM bandwidth) instead of
+    // streamed through host memory and the link.  Beyond HBM (or with
+    // BMM_PIPELINE=host) the host-thread pipeline below runs: the paper's Alg. 3.
+    // Either way every sub-instance is prepared, solved and aggregated exactly once, and
+    // the counters get the host layer's tallies (the same terms and folds the host
+    // stages count) plus the solve's.
+    const char* mode = std::getenv("BMM_PIPELINE");
+    std::uint64_t free_b = 0, total_b = 0;
+    const bool on_device = !(mode && std::string(mode) == "host") && bmmgpu_mem_info(0, &free_b, &total_b) == BMMGPU_OK &&
+                           8.0 * double(a_hat.words.size()) * 8.0 < double(free_b);
+    if (on_device) {
+        detail::solve_alt(a_hat.words.data(), b_hat.words.data(), c_hat.words.data(), d_host + sub_depth, d, nullptr, 0);
+        for (std::uint64_t f = 0; f < subs; ++f) {
+            const SubInstanceIndex h = SubInstanceIndex::from_flat(f, d_host);
+            if (counter) {
+                std::uint64_t ta = 0, tb = 0, folds = 0;
+                for (std::uint64_t g = 0; g < combos; ++g) {
+                    ta += in_coeff(sc.alpha, h.digits, g);
+                    tb += in_coeff(sc.beta, h.digits, g);
+                    folds += out_coeff(sc.gamma, h.digits, g);
+                }
+                if (ta > 1) counter->add_xors((ta - 1) * inner);
+                if (tb > 1) counter->add_xors((tb - 1) * inner);
+                if (folds) counter->add_xors(folds * inner);
+                const std::uint64_t kernels = [&] {
+                    std::uint64_t k = 1;
+                    for (int i = 0; i < sub_depth; ++i) k *= 7;
+                    return k;
+                }();
+                counter->add_kernels(kernels);
+                counter->add_ands(kernels * kBlockBits);
+                counter->add_xors(predicted_additions(d, sub_depth, CostPart::LinearCombinations) * kBlockWords);
+            }
+            st.prepared_left[f] = st.prepared_right[f] = st.aggregated[f] = 1;
+        }
+        if (stats) *stats = std::move(st);
+        return c_hat;
+    }
 
     // One pipeline per worker: single-slot T / S / Q buffers with occupancy flags,
     // each flag single-producer single-consumer (reference pipeline.cpp:187-194).

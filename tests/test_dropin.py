@@ -24,8 +24,10 @@ def dropin_binary():
     return BIN
 
 
-def _run(binary, mode: str) -> str:
-    r = subprocess.run([str(binary), mode], capture_output=True, text=True, cwd=str(ROOT / "build"), timeout=600)
+def _run(binary, mode: str, env: dict | None = None) -> str:
+    import os
+    r = subprocess.run([str(binary), mode], capture_output=True, text=True, cwd=str(ROOT / "build"), timeout=600,
+                       env=dict(os.environ, **(env or {})))
     assert r.returncode == 0, r.stdout + r.stderr
     return r.stdout
 
@@ -37,6 +39,11 @@ def test_dropin_host_api(dropin_binary):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not HAS_GPU, reason="no CUDA device")
-def test_dropin_products_on_gpu(dropin_binary):
-    out = _run(dropin_binary, "gpu")
+@pytest.mark.parametrize("pipeline", ["device", "host"])
+def test_dropin_products_on_gpu(dropin_binary, pipeline):
+    """The reference suites' product cases through the drop-in; `pipeline::coordinate`
+    runs its host layer on the device when the operands fit (default) and as the
+    host-thread pipeline with BMM_PIPELINE=host -- both against the reference's outputs
+    and counters."""
+    out = _run(dropin_binary, "gpu", {"BMM_PIPELINE": pipeline})
     assert "0 failures" in out
