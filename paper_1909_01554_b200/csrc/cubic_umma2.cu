@@ -140,7 +140,8 @@ __device__ __forceinline__ unsigned long long gtime() {
 // Isolation probes for the pipeline (results garbage; only with -DBMMGPU_PROBE,
 // BMMGPU_UMMA_PROBE=v sets flag bits 32*v; microbench/probe.sh):
 // 32 no MMAs, 64 no operand stores, 128 loaders only (expanders just drain the packed ring),
-// 256 expanders ignore the packed ring.
+// 256 expanders ignore the packed ring, 512 no proxy fence after the operand stores, 1024 no
+// Bt operand stores.
 // The probe build also accounts the cycles each role spends waiting (g_probe, 8
 // counters per CTA: expander warp 0 empty / packed-full waits / loop total, MMA
 // lane full / acc_empty waits / loop total, loader warp 0 packed-empty wait / total).
@@ -552,10 +553,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                     if (!PROBE(64 | 128)) {
                         expand_store_sw128(sa, r, 0, v[i][0]);
                         expand_store_sw128(sa, r, 1, v[i][1]);
-                        expand_store_sw128(sa + P_REGION, rb, 0, v[i][2]);
-                        expand_store_sw128(sa + P_REGION, rb, 1, v[i][3]);
+                        if (!PROBE(1024)) {
+                            expand_store_sw128(sa + P_REGION, rb, 0, v[i][2]);
+                            expand_store_sw128(sa + P_REGION, rb, 1, v[i][3]);
+                        }
                     }
-                    umma::fence_proxy_async_smem();
+                    if (!PROBE(512)) umma::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0 && !PROBE(128)) umma::mbar_arrive_cluster(full_leader0 + s * 8);
                     TRACE_AT(pair == 0 && (warp & 3) == 0 && lane == 0 && it < 512, (rank ? 2560 : 1536) + it);
