@@ -639,8 +639,8 @@ def run_ooc(args, dist: Dist) -> None:
                            "input_generation_s": t_gen,
                            "parallelism": f"output row slabs x{dist.world}, no exchange"},
                 "roofline": {"bound": "tensor", "achieved": achieved / 1e12,
-                             "peak": peaks["umma_mxf4_bops"] / 1e12, "unit": "Tbop/s",
-                             "frac": achieved / peaks["umma_mxf4_bops"], "traffic": None,
+                             "peak": peaks["umma_mxf4_bops_sustained"] / 1e12, "unit": "Tbop/s",
+                             "frac": achieved / peaks["umma_mxf4_bops_sustained"], "traffic": None,
                              "kernel": kname,
                              "kernel_ms": kms, "kernel_launches_per_step": blk_launches.value / args.steps,
                              "kernel_share_of_step": kms / (t * 1e3)},
@@ -655,6 +655,24 @@ def run_ooc(args, dist: Dist) -> None:
         print(json.dumps(line), flush=True)
     if shared_b is not None:
         shared_b.close()
+
+
+def k2_clock(lib, launch_macs: float, kms: float) -> dict:
+    """Effective SM clock of the last K2 launch (clock64 / globaltimer of CTA pair 0's MMA loop,
+    bmmgpu_debug_k2_clock) and the MACs per SM clock it implies: nvidia-smi's clocks.sm does not
+    show the power cap's clock slowdown, this does."""
+    import torch
+    cyc, ns = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    if lib.bmmgpu_debug_k2_clock(ctypes.byref(cyc), ctypes.byref(ns)) != 0 or not ns.value:
+        return {}
+    mhz = cyc.value / ns.value * 1e3
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    per_clk = launch_macs / (kms * 1e-3) / sms / (mhz * 1e6)
+    return {"sm_clock_effective_mhz": round(mhz, 1), "mac_per_sm_clock": round(per_clk, 1),
+            "frac_per_clock": round(per_clk / 16384.0, 4),
+            "per_clock_note": "achieved MACs per SM per effective clock against the tensor pipe's 16,384 "
+                              "(kind::mxf4 M256 N256 K64 pair); the rest of the gap to the peak is the SM "
+                              "clock under the power cap"}
 
 
 def slab_exchange_xor(P, R, slabs: list[tuple[int, int]], me: int, G: int, stage_on_host: bool, fold) -> None:
@@ -789,8 +807,8 @@ def run_alt_deal(args, dist: Dist) -> None:
                                           f"{dist.world} ranks, partial products XOR-folded after one all-to-all "
                                           "of output-row slabs",
                            "host_levels": dh, "subinstances_rank0": mine},
-                "roofline": {"bound": "tensor", "achieved": achieved / 1e12, "peak": peaks["umma_mxf4_bops"] / 1e12,
-                             "unit": "Tbop/s", "frac": achieved / peaks["umma_mxf4_bops"], "traffic": None,
+                "roofline": {"bound": "tensor", "achieved": achieved / 1e12, "peak": peaks["umma_mxf4_bops_sustained"] / 1e12,
+                             "unit": "Tbop/s", "frac": achieved / peaks["umma_mxf4_bops_sustained"], "traffic": None,
                              "kernel": f"cubic_umma2_kernel (leaf layer: 7^{e_sub} products of {leaf}^3 per "
                                        "sub-instance)",
                              "kernel_ms": kms, "kernel_share_of_step": kms / ms},
@@ -942,7 +960,7 @@ def run_ours(args, dist: Dist) -> None:
     # ---- roofline of the dominant kernel
     peaks = json.loads((ROOT / "profiles" / "peaks.json").read_text())
     resolved = kernel if kernel else 2  # AUTO = the tcgen05 CTA-pair kernel (csrc/capi.cu resolve_kernel)
-    peak = peaks["lop3_bops"] if resolved == 1 else peaks["umma_mxf4_bops"]
+    peak = peaks["lop3_bops"] if resolved == 1 else peaks["umma_mxf4_bops_sustained"]
     kname = {1: "cubic_lop3_kernel", 2: "cubic_umma2_kernel"}[resolved]
     if algo == 0:
         # algorithmic work of the one product launch: the slab's 2 m n k - m n
@@ -965,8 +983,14 @@ def run_ours(args, dist: Dist) -> None:
                 "peak": peak / 1e12, "unit": "Tbop/s", "frac": achieved / peak, "traffic": traffic,
                 "kernel": kname, "kernel_ms": kms, "kernel_launches_per_step": blk_launches.value / args.steps,
                 "kernel_share_of_step": kms / ms,
-                "peak_source": "profiles/peaks.json (measured issue rate, microbench/ubench.cu; "
-                               "MEASURED_PEAKS.json has no integer-ALU or fp4 figure)"}
+                "peak_source": ("profiles/peaks.json lop3_bops (measured LOP3 issue rate, microbench/ubench.cu)"
+                                if resolved == 1 else
+                                "profiles/peaks.json umma_mxf4_bops_sustained: the K2 MMA instruction back to "
+                                "back for seconds on K2-like operands under the power cap (microbench/"
+                                "ubench_sustained.cu, 16,375 MAC/SM-clock at an effective 1845 MHz); "
+                                "MEASURED_PEAKS.json has no integer-ALU or fp4 figure")}
+    if resolved != 1:
+        roofline.update(k2_clock(lib, launch_bops / 2.0, kms))
     mp = ROOT / "MEASURED_PEAKS.json"
     if mp.exists() and resolved != 1:
         # cross-check against the driver's bf16 GEMM figure: kind::mxf4 issues 4 MACs per

@@ -91,6 +91,14 @@ int bmmgpu_init(uint32_t device_mask, uint64_t reserve_bytes);
 int bmmgpu_cubic(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t m, uint64_t k, uint64_t n,
                  int32_t semiring, const bmmgpu_opts* opts);
 
+/* One 64 x 64 block product in the reference's operand form: out[i] bit k = the GF(2)
+ * dot product (parity of popcount) or Boolean dot product of row i of a (64 words, row
+ * major) with column k of B given column-major in bt (word k = column k).  One launch
+ * and one synchronisation through page-locked mapped memory (no stream lease, no copies
+ * beyond the 1.5 KB staging), so callers that loop over blocks pay the launch latency,
+ * not a full host-API product.  Replaces bmm::kernel64 (reference engine.cpp:34-56). */
+int bmmgpu_kernel64(const uint64_t* a, const uint64_t* bt, uint64_t* out, int32_t semiring);
+
 /* Fast product through a bilinear scheme: square n = 64 * 2^depth, plan.depth()
  * must equal depth.  Cubic algo dispatches to bmmgpu_cubic; Boolean with a fast
  * algo is BMMGPU_EINVAL.  Replaces bmm::multiply (reference engine.cpp:351-382).
@@ -265,6 +273,14 @@ int bmmgpu_mem_info(int32_t device, uint64_t* free_bytes, uint64_t* total_bytes)
  * more output tiles than CTA pairs) and loaders that stopped aligning at the spin limit,
  * since the library was loaded (the tests assert the mode runs and never times out). */
 int bmmgpu_debug_wave_stats(uint64_t* aligned_launches, uint64_t* loader_timeouts);
+
+/* Debug counter: K2 launches that kept operand A in tensor memory (long-K products,
+ * BMMGPU_TS_MIN_STAGES stages or more), since the library was loaded. */
+int bmmgpu_debug_ts_launches(uint64_t* launches);
+
+/* Debug: SM clock cycles (clock64) and nanoseconds (globaltimer) of CTA pair 0's MMA loop
+ * in the last K2 launch; cycles / ns is the effective SM clock under the power cap. */
+int bmmgpu_debug_k2_clock(uint64_t* cycles, uint64_t* ns);
 const char* bmmgpu_last_error(void);
 const char* bmmgpu_version(void);
 

@@ -59,5 +59,7 @@ if lib.bmmgpu_debug_umma2_probe(buf) == 0:
     leaders = range(0, 148, 2)
     out.update({"expander_wait_empty": frac(0, 2, range(148)), "expander_wait_packed": frac(1, 2, range(148)),
                 "mma_wait_full": frac(3, 5, leaders), "mma_wait_acc": frac(4, 5, leaders),
-                "loader_wait_packed_empty": frac(6, 7, range(148))})
+                "loader_wait_packed_empty": frac(6, 7, range(148)),
+                # effective SM clock: the MMA lane's loop cycles (clock64) over the last launch's time
+                "eff_mhz": round(sum(rows[c][5] for c in leaders) / len(leaders) / (ms * 1e3), 1)})
 print(json.dumps(out), flush=True)

@@ -129,6 +129,12 @@ def lib() -> ctypes.CDLL:
         L.bmmgpu_layout.restype = ctypes.c_int
         L.bmmgpu_dev_layout.argtypes = [vp, vp, u64, u64, i32, vp]
         L.bmmgpu_dev_layout.restype = ctypes.c_int
+        L.bmmgpu_debug_k2_clock.argtypes = [_u64p, _u64p]
+        L.bmmgpu_debug_k2_clock.restype = ctypes.c_int
+        L.bmmgpu_debug_ts_launches.argtypes = [_u64p]
+        L.bmmgpu_debug_ts_launches.restype = ctypes.c_int
+        L.bmmgpu_kernel64.argtypes = [vp, vp, vp, i32]
+        L.bmmgpu_kernel64.restype = ctypes.c_int
         L.bmmgpu_debug_wave_stats.argtypes = [_u64p, _u64p]
         L.bmmgpu_debug_wave_stats.restype = ctypes.c_int
         L.bmmgpu_device_count.restype = ctypes.c_int
@@ -388,6 +394,18 @@ def _contig(m: BitMatrix) -> np.ndarray:
     if w.size != m.rows * m.words_per_row():
         raise ShapeError("word storage does not match the shape")
     return w
+
+
+def kernel64(a: np.ndarray, b_transposed: np.ndarray, ring: Semiring) -> np.ndarray:
+    """One 64 x 64 block product in the reference's operand form (engine.cpp:34-56):
+    out[i] bit k = dot(row i of a, column k of B), B given column-major (word k = column k)."""
+    aw = np.ascontiguousarray(a, dtype=np.uint64)
+    bw = np.ascontiguousarray(b_transposed, dtype=np.uint64)
+    if aw.size != 64 or bw.size != 64:
+        raise ValueError("kernel64 takes 64 words per operand")
+    out = np.zeros(64, dtype=np.uint64)
+    _check(lib().bmmgpu_kernel64(aw.ctypes.data, bw.ctypes.data, out.ctypes.data, int(ring)))
+    return out
 
 
 def multiply_cubic(a: BitMatrix, b: BitMatrix, ring: Semiring, workers: int = 1, *, kernel: int = Kernel.AUTO,

@@ -21,7 +21,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 CUDA_HOME = Path(NVCC).resolve().parent.parent
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CUDA_SOURCES = ["capi.cu", "transpose.cu", "cubic_lop3.cu", "cubic_umma2.cu", "alt.cu", "stream.cu", "bmm1.cu", "layout.cu", "alt_tiles.cu", "init.cu"]
+CUDA_SOURCES = ["capi.cu", "transpose.cu", "cubic_lop3.cu", "cubic_umma2.cu", "alt.cu", "stream.cu", "bmm1.cu", "layout.cu", "alt_tiles.cu", "init.cu", "kernel64.cu"]
 HOST_SOURCES = ["host/bitmatrix.cpp", "host/engine.cpp", "host/pipeline.cpp"]
 
 LIB_GPU = HERE / "libbmmgpu.so"

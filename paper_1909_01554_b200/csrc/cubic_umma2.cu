@@ -110,6 +110,10 @@ constexpr uint32_t P_SF_EVEN = 480;  // 1.0
 constexpr uint32_t P_SF_ODD = 488;   // 2.0
 constexpr uint32_t P_SF_BIAS = 496;  // 2^9 block scales of the bias MMA
 constexpr uint32_t P_MAX_PAIRS = 74;  // 148 SMs
+// kTs (long-K launches): operand A of each stage lives in TMEM columns [P_TS_A + 32 s, + 32)
+// instead of shared memory, next to one accumulator at [0, 256).
+constexpr uint32_t P_TS_A = 256;
+static_assert(P_TS_A + 32 * P_STAGES <= P_SF_EVEN, "A ring overlaps the block scales");
 
 static_assert(P_SMEM <= 232448 - 1024, "stage ring exceeds shared memory");
 
@@ -121,6 +125,10 @@ __device__ unsigned long long g_trace[6144];
 // Loaders of wave-aligned launches that hit the spin limit and stopped aligning (debug
 // counter behind bmmgpu_debug_wave_stats; the tests assert it stays 0).
 __device__ unsigned long long g_wave_timeouts;
+// SM clock cycles (clock64) and nanoseconds (globaltimer) of pair 0's MMA loop in the last
+// launch: the effective SM clock under the board power cap, which nvidia-smi's sampled
+// clocks.sm does not show (bmmgpu_debug_k2_clock; bench.py reports it).
+__device__ unsigned long long g_clock_stat[2];
 #ifdef BMMGPU_TRACE
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -141,7 +149,9 @@ __device__ __forceinline__ unsigned long long gtime() {
 // BMMGPU_UMMA_PROBE=v sets flag bits 32*v; microbench/probe.sh):
 // 32 no MMAs, 64 no operand stores, 128 loaders only (expanders just drain the packed ring),
 // 256 expanders ignore the packed ring, 512 no proxy fence after the operand stores, 1024 no
-// Bt operand stores.
+// Bt operand stores, 2048 operand stores only while the ring fills the first time (the MMAs
+// then re-read valid e2m1 data: the MMA side with real operand values but no stores), 4096
+// the same for the A operand only (half the operand stores).
 // The probe build also accounts the cycles each role spends waiting (g_probe, 8
 // counters per CTA: expander warp 0 empty / packed-full waits / loop total, MMA
 // lane full / acc_empty waits / loop total, loader warp 0 packed-empty wait / total).
@@ -214,6 +224,17 @@ __device__ __forceinline__ void expand_store_sw128(uint8_t* region, int r, int g
     *reinterpret_cast<uint4*>(row + (((j0 + 1) ^ rr) << 4)) = make_uint4(y.x & M2, y.y & M2, y.z & M2, y.w & M2);
     *reinterpret_cast<uint4*>(row + (((j0 + 2) ^ rr) << 4)) = make_uint4(x.x & M1, x.y & M1, x.z & M1, x.w & M1);
     *reinterpret_cast<uint4*>(row + (((j0 + 3) ^ rr) << 4)) = make_uint4(y.x & M1, y.y & M1, y.z & M1, y.w & M1);
+}
+
+// The same expansion into 16 registers (logical chunks 4g .. 4g + 3 of the row, 4 words
+// each) for the TMEM form of operand A: w[o + 4 q + i] = word i of chunk q.
+__device__ __forceinline__ void expand_regs(const uint4& x, uint32_t (&w)[32], int o) {
+    constexpr uint32_t M2 = 0x22222222u, M1 = 0x11111111u;
+    const uint4 y = make_uint4(x.x >> 2, x.y >> 2, x.z >> 2, x.w >> 2);
+    w[o + 0] = x.x & M2, w[o + 1] = x.y & M2, w[o + 2] = x.z & M2, w[o + 3] = x.w & M2;
+    w[o + 4] = y.x & M2, w[o + 5] = y.y & M2, w[o + 6] = y.z & M2, w[o + 7] = y.w & M2;
+    w[o + 8] = x.x & M1, w[o + 9] = x.y & M1, w[o + 10] = x.z & M1, w[o + 11] = x.w & M1;
+    w[o + 12] = y.x & M1, w[o + 13] = y.y & M1, w[o + 14] = y.z & M1, w[o + 15] = y.w & M1;
 }
 
 // The accumulator never starts from zero: each tile's first MMA (accumulate = 0)
@@ -363,7 +384,7 @@ struct FoldSpec {
     uint32_t ma, mb;  // A / Bt quadrant masks of the 7 children
     uint32_t L;       // leaf rows (the parent is 2L x 2L; quadrant q at rows (q >> 1) L, words (q & 1) L / 64)
 };
-template <bool kTma, bool kFold>
+template <bool kTma, bool kFold, bool kTs = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     cubic_umma2_kernel(const uint64_t* __restrict__ A, uint64_t lda, const uint64_t* __restrict__ Bt, uint64_t ldbt,
                        uint64_t* __restrict__ C, uint64_t ldc, uint64_t kw, int flags, TileMap map,
@@ -375,6 +396,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     // parameter let the two instantiations schedule the producer loop differently)
     const bool kGf2 = (flags & 2) != 0;
     const bool accumulate = (flags & 1) != 0;
+    // two overlapping accumulators for short-K tiles; the TMEM-A form keeps one (its A ring
+    // takes the columns of the second) and runs only long-K launches, where a tile's drain
+    // is ~1 % of the tile
+    constexpr bool kAcc2 = BMMGPU_ACC2 && !kTs;
     __shared__ __align__(8) uint64_t full_bar[P_STAGES];
     __shared__ __align__(8) uint64_t empty_bar[P_STAGES];
     __shared__ __align__(8) uint64_t pk_full_bar[P_SST_SLOTS];
@@ -550,9 +575,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                         PWAIT(0, umma::mbar_wait(&empty_bar[s], uint32_t((it / P_STAGES - 1) & 1)));
                     TRACE_AT(pair == 0 && (warp & 3) == 0 && lane == 0 && it < 512, (rank ? 2048 : 1024) + it);
                     uint8_t* sa = smem + size_t(s) * P_STAGE;
-                    if (!PROBE(64 | 128)) {
-                        expand_store_sw128(sa, r, 0, v[i][0]);
-                        expand_store_sw128(sa, r, 1, v[i][1]);
+                    if (kTs) {
+                        // A -> this thread's TMEM lane (row r), 32 columns = the stage's 256 K
+                        // elements in logical chunk order; Bt -> shared memory as below.  The
+                        // empty barrier said the MMAs reading this slot completed.
+                        umma::fence_after_sync();
+                        uint32_t w[32];
+                        expand_regs(v[i][0], w, 0);
+                        expand_regs(v[i][1], w, 16);
+                        umma::tmem_st32(tmem + (((warp & 3) * 32) << 16) + P_TS_A + 32 * s, w);
+                        expand_store_sw128(sa + P_REGION, rb, 0, v[i][2]);
+                        expand_store_sw128(sa + P_REGION, rb, 1, v[i][3]);
+                        umma::tmem_st_wait();
+                        umma::fence_proxy_async_smem();
+                        umma::fence_before_sync();
+                        __syncwarp();
+                        if (lane == 0) umma::mbar_arrive_cluster(full_leader0 + s * 8);
+                        continue;
+                    }
+                    if (!PROBE(64 | 128) && !(PROBE(2048) && it >= P_STAGES)) {
+                        if (!(PROBE(4096) && it >= P_STAGES)) {
+                            expand_store_sw128(sa, r, 0, v[i][0]);
+                            expand_store_sw128(sa, r, 1, v[i][1]);
+                        }
                         if (!PROBE(1024)) {
                             expand_store_sw128(sa + P_REGION, rb, 0, v[i][2]);
                             expand_store_sw128(sa + P_REGION, rb, 1, v[i][3]);
@@ -586,14 +631,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             unsigned long long pw[8] = {};
             const long long p_t0 = clock64();
 #endif
+            long long clk0 = 0;
+            unsigned long long ns0 = 0;
+            if (pair == 0) {
+                clk0 = clock64();
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns0));
+            }
             for (uint32_t t = pair; t < total_tiles; t += n_pairs, ++local) {
                 // the tile's first stage is usually staged long before the accumulator comes
                 // back: wait for it first so the MMAs issue right after the accumulator is free.
                 // Accumulator (local & 1) must have been drained by both CTAs' epilogues from
                 // tile local - 2, and the overlap columns from tile local - 1.
-                const uint32_t buf = BMMGPU_ACC2 ? (local & 1) : 0;
+                const uint32_t buf = kAcc2 ? (local & 1) : 0;
                 if (local > 0 && n_stages > 0) umma::mbar_wait(&full_bar[s], full_parity);
-                if (BMMGPU_ACC2) {
+                if (kAcc2) {
                     if (local > 0) PWAIT(4, umma::mbar_wait(&ovl_bar, (local - 1) & 1));
                     if (local > 1) PWAIT(4, umma::mbar_wait(&acc_empty_bar[buf], ((local >> 1) - 1) & 1));
                 } else if (local > 0) {
@@ -617,9 +668,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                         for (int j = 0; j < 4; ++j) {
                             const uint32_t sf = tmem + ((j & 1) ? P_SF_ODD : P_SF_EVEN);
                             if (PROBE(32)) continue;
-                            // + 32 bytes per K = 64 step
+                            // + 32 bytes per K = 64 step (A in TMEM: + 8 columns)
                             // always accumulate onto the bias
-                            umma::mma_mxf4_pair(dacc, da0 + 2 * j, db0 + 2 * j, idesc, sf, sf, 1u);
+                            if (kTs)
+                                umma::mma_mxf4_pair_ts(dacc, tmem + P_TS_A + 32 * uint32_t(s) + 8 * j, db0 + 2 * j, idesc,
+                                                       sf, sf, 1u);
+                            else
+                                umma::mma_mxf4_pair(dacc, da0 + 2 * j, db0 + 2 * j, idesc, sf, sf, 1u);
                         }
                         umma::mma_commit_pair(&empty_bar[s], 0x3);
                     }
@@ -634,6 +689,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             pw[5] = clock64() - p_t0;
 #endif
             PSTORE(3, 5, lane == 0);
+            if (pair == 0 && lane == 0) {
+                unsigned long long ns1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns1));
+                g_clock_stat[0] = (unsigned long long)(clock64() - clk0);
+                g_clock_stat[1] = ns1 - ns0;
+            }
         }
     } else if (kFold && warp >= P_LOADER_WARP0) {
         // ------------------------------------------------ loader, level-shifted leaves: per superstage
@@ -803,7 +864,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                 umma::mbar_wait(&acc_full_bar[buf], (local >> 1) & 1);
             umma::fence_after_sync();
             TRACE_AT(pair == 0 && rank == 0 && quarter == 0 && lane == 0 && local < 512, 3072 + 4 * local + 1);
-            const uint32_t ybuf = BMMGPU_ACC2 ? buf : 0;
+            const uint32_t ybuf = kAcc2 ? buf : 0;
             const uint32_t tacc = tmem + ((quarter * 32) << 16) + (ybuf ? P_ACC_Y : 0);
             const uint32_t empty_leader = empty_leader0 + 8 * buf;
             if (kGf2 && BMMGPU_GF2_PACK16) {
@@ -854,6 +915,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #endif
 
 std::atomic<uint64_t> g_wave_aligned_launches{0};
+std::atomic<uint64_t> g_ts_launches{0};  // K2 launches with operand A in TMEM
+
+#ifndef BMMGPU_TS_MIN_STAGES
+#define BMMGPU_TS_MIN_STAGES 128  // launches with at least this many 256-bit stages use kTs (0: never)
+#endif
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -936,10 +1002,21 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
     const bool tma = !(ld_env && !strcmp(ld_env, "cpasync")) &&
                      make_operand_map(&tmA, dA, kw, m_pad, lda, batch, sA_batch) &&
                      make_operand_map(&tmB, dBt, kw, n_pad, ldbt, batch, sB_batch);
-    auto kern = tma ? cubic_umma2_kernel<true, false> : cubic_umma2_kernel<false, false>;
+    const uint64_t n_stages_l = kw * 64 / P_KBITS;
+    // Long-K launches keep operand A in TMEM (kTs): half the expanders' shared-memory stores,
+    // which under the board power cap is SM clock (c3: 1731 -> ~1810 MHz with A's stores
+    // removed, profiles/r02/probe_effclock2.txt); short-K tiles keep both operands in shared
+    // memory and the two overlapping accumulators.
+    static const uint64_t ts_min = [] {
+        const char* e = getenv("BMMGPU_TS_MIN_STAGES");
+        return e ? uint64_t(strtoull(e, nullptr, 10)) : uint64_t(BMMGPU_TS_MIN_STAGES);
+    }();
+    const bool ts = tma && ts_min > 0 && n_stages_l >= ts_min;
+    if (ts) g_ts_launches.fetch_add(1, std::memory_order_relaxed);
+    auto kern = ts ? cubic_umma2_kernel<true, false, true>
+                   : tma ? cubic_umma2_kernel<true, false> : cubic_umma2_kernel<false, false>;
     BMMGPU_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P_SMEM)));
     const char* probe = getenv("BMMGPU_UMMA_PROBE");
-    const uint64_t n_stages_l = kw * 64 / P_KBITS;
     const int flags = (accumulate ? 1 : 0) | (gf2 ? 2 : 0) | (n_stages_l >= 64 ? 4 : 0) |
                       (getenv("BMMGPU_UMMA_TRACE") ? 16 : 0) | (probe && *probe ? 32 * atoi(probe) : 0);
     // Epilogue warps poll acc_full with this sleep between tries: long tiles (K of tens of
@@ -1046,6 +1123,23 @@ extern "C" int bmmgpu_debug_wave_stats(uint64_t* aligned_launches, uint64_t* loa
         if (cudaMemcpyFromSymbol(&t, bmmgpu::g_wave_timeouts, sizeof(t)) != cudaSuccess) return 5;
         *loader_timeouts = t;
     }
+    return 0;
+}
+
+// Debug: SM cycles and nanoseconds of pair 0's MMA loop in the last K2 launch (effective
+// SM clock = cycles / ns).
+extern "C" int bmmgpu_debug_k2_clock(uint64_t* cycles, uint64_t* ns) {
+    unsigned long long v[2] = {0, 0};
+    if (cudaMemcpyFromSymbol(v, bmmgpu::g_clock_stat, sizeof(v)) != cudaSuccess) return 5;
+    if (cycles) *cycles = v[0];
+    if (ns) *ns = v[1];
+    return 0;
+}
+
+// Debug: K2 launches that kept operand A in tensor memory (kTs), since the library was loaded.
+extern "C" int bmmgpu_debug_ts_launches(uint64_t* launches) {
+    if (!launches) return 1;
+    *launches = bmmgpu::g_ts_launches.load();
     return 0;
 }
 

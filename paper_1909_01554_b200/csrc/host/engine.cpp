@@ -110,12 +110,9 @@ const Decomposition& decomposition_for(Algo algo) {
 }
 
 void kernel64(const std::uint64_t* a, const std::uint64_t* b_transposed, std::uint64_t* out, Semiring ring) {
-    // b_transposed holds B column-major; the engine takes B row-major.
-    BitMatrix b = BitMatrix::zeros(kBlockDim, kBlockDim);
-    std::copy(b_transposed, b_transposed + kBlockWords, b.words.begin());
-    transpose_blocks64(b);
-    check(bmmgpu_cubic(a, b.words.data(), out, kBlockDim, kBlockDim, kBlockDim,
-                       ring == Semiring::Gf2XorAnd ? BMMGPU_GF2_XOR_AND : BMMGPU_BOOLEAN_OR_AND, nullptr));
+    // one launch on page-locked mapped staging (K9, csrc/kernel64.cu); b_transposed is B
+    // column-major, exactly the reference's operand form
+    check(bmmgpu_kernel64(a, b_transposed, out, ring == Semiring::Gf2XorAnd ? BMMGPU_GF2_XOR_AND : BMMGPU_BOOLEAN_OR_AND));
 }
 
 BitMatrix multiply_cubic(const BitMatrix& a, const BitMatrix& b, Semiring ring, int workers, OpCounter* counter) {

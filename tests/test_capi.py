@@ -74,10 +74,10 @@ def test_kernels_are_sm100a_native():
     # STTM), the pair's TMEM allocator and commit barriers, 3-D tensor-map loads
     fns = sass.split("Function : ")
     k2 = [f for f in fns if "cubic_umma2_kernel" in f.splitlines()[0]]
-    assert len(k2) == 3, "the TMA, the cp.async-loader and the level-shifted (fold) instantiations"
+    assert len(k2) == 4, "the TMA, TMA + A-in-TMEM, cp.async-loader and level-shifted (fold) instantiations"
     for op in ("UTCOMMA.2CTA", "LDTM", "STTM", "UTCATOMSWS.2CTA", "UTCBAR.2CTA"):
         assert all(op in f for f in k2), op
-    assert sum("UTMALDG.3D" in f for f in k2) == 2  # TMA loaders: plain and fold
+    assert sum("UTMALDG.3D" in f for f in k2) == 3  # TMA loaders: plain, A-in-TMEM and fold
 
 
 @pytest.mark.skipif(HAS_GPU, reason="checks the no-device path")

@@ -28,6 +28,38 @@ def test_small_shapes_match_reference_words(engine, oracle, golden, kernel):
         assert [f"{int(x):016x}" for x in got.words] == c["words"], (c["m"], c["k"], c["n"], c["ring"])
 
 
+def test_kernel64_matches_reference_golden(engine, oracle, golden):
+    """bmmgpu_kernel64 (K9) on the reference's 64 x 64 golden block and its identities
+    (reference test_engine.cpp:86-112), and its per-call latency (one launch + sync)."""
+    import time
+    bmm = engine
+    g = golden["kernel64"]
+    a = oracle.random(64, 64, g["a_seed"])
+    bt = oracle.transpose_blocks64(64, 64, oracle.random(64, 64, g["b_seed"]))
+    assert [f"{int(x):016x}" for x in bmm.kernel64(a, bt, bmm.Semiring.Gf2XorAnd)] == g["gf2"]
+    assert [f"{int(x):016x}" for x in bmm.kernel64(a, bt, bmm.Semiring.BooleanOrAnd)] == g["bool"]
+    ident = np.array([1 << i for i in range(64)], dtype=np.uint64)
+    assert np.array_equal(bmm.kernel64(ident, bt, bmm.Semiring.Gf2XorAnd), oracle.random(64, 64, g["b_seed"]))
+    ones = np.full(64, ~np.uint64(0), dtype=np.uint64)
+    assert not bmm.kernel64(ones, ones, bmm.Semiring.Gf2XorAnd).any()
+    assert np.all(bmm.kernel64(ones, ones, bmm.Semiring.BooleanOrAnd) == ~np.uint64(0))
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        x = rng.integers(0, 2**63, 64, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, 64, dtype=np.uint64)
+        y = rng.integers(0, 2**63, 64, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, 64, dtype=np.uint64)
+        for ring in (GF2, BOOL):
+            assert np.array_equal(bmm.kernel64(x, y, bmm.Semiring(ring)), oracle.kernel64(x, y, ring))
+    lib = bmm.lib()
+    out = np.zeros(64, dtype=np.uint64)
+    reps = 2000
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        assert lib.bmmgpu_kernel64(a.ctypes.data, bt.ctypes.data, out.ctypes.data, GF2) == 0
+    us = (time.perf_counter() - t0) / reps * 1e6
+    print(f"bmmgpu_kernel64: {us:.1f} us per call")
+    assert us < 200, us
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_large_digests(engine, oracle, golden, kernel):
     bmm = engine
@@ -382,3 +414,46 @@ def test_wave_aligned_mode_matches_oracle(engine, oracle, ring):
     if ring == BOOL:
         frac = float(np.unpackbits(want.view(np.uint8)).mean())
         assert 0.3 < frac < 0.9, frac
+
+
+@pytest.mark.parametrize("ring", [GF2, BOOL])
+def test_tmem_operand_mode_matches_oracle(engine, oracle, ring):
+    """Long-K launches keep operand A in tensor memory (kTs: tcgen05.mma with A from TMEM,
+    one accumulator).  Through the device API, one launch each: 2560 x 32768 x 2048 (80 tiles
+    over 74 pairs, 128 K-stages) and 768 x 65536 x 512 (256 stages, fewer tiles than pairs),
+    the second also with the accumulate flag (the K-chunk fold); the debug counter proves the
+    mode ran; word for word against the oracle (Boolean on AND-of-7 inputs)."""
+    import torch
+    bmm = engine
+    lib = bmm.lib()
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for m, k, n, seed in ((2560, 32768, 2048, 701), (768, 65536, 512, 731)):
+        a = oracle.random(m, k, seed)
+        b = oracle.random(k, n, seed + 1)
+        if ring == BOOL:
+            for s in range(6):
+                a &= oracle.random(m, k, seed + 10 + s)
+                b &= oracle.random(k, n, seed + 20 + s)
+        kw, nw = k // 64, n // 64
+        dA = torch.from_numpy(a.view(np.int64).reshape(m, kw)).cuda()
+        dB = torch.from_numpy(b.view(np.int64).reshape(k, nw)).cuda()
+        dBt = torch.empty((n, kw), dtype=torch.int64, device="cuda")
+        dC = torch.empty((m, nw), dtype=torch.int64, device="cuda")
+        assert lib.bmmgpu_dev_transpose(dB.data_ptr(), nw, k, n, dBt.data_ptr(), n, kw, stream) == 0
+        before, after = ctypes.c_uint64(), ctypes.c_uint64()
+        assert lib.bmmgpu_debug_ts_launches(ctypes.byref(before)) == 0
+        assert lib.bmmgpu_dev_cubic(dA.data_ptr(), kw, dBt.data_ptr(), kw, dC.data_ptr(), nw, m, n, kw, ring, 2, 0,
+                                    stream) == 0
+        torch.cuda.synchronize()
+        assert lib.bmmgpu_debug_ts_launches(ctypes.byref(after)) == 0
+        assert after.value == before.value + 1, "the TMEM-operand mode did not run"
+        want = oracle.multiply_cubic(a, b, m, k, n, ring)
+        assert np.array_equal(dC.cpu().numpy().view(np.uint64).ravel(), want), (m, k, n)
+        if k == 65536:
+            c0 = oracle.random(m, n, seed + 5)
+            dC.copy_(torch.from_numpy(c0.view(np.int64).reshape(m, nw)).cuda())
+            assert lib.bmmgpu_dev_cubic(dA.data_ptr(), kw, dBt.data_ptr(), kw, dC.data_ptr(), nw, m, n, kw, ring, 2,
+                                        1, stream) == 0
+            torch.cuda.synchronize()
+            folded = (c0 ^ want) if ring == GF2 else (c0 | want)
+            assert np.array_equal(dC.cpu().numpy().view(np.uint64).ravel(), folded)
