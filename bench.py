@@ -194,6 +194,11 @@ class ClockSampler:
     def stop(self) -> dict | None:
         if self.proc is None:
             return None
+        # a timed region shorter than the poller's start-up and period (the n = 8192 lines) has no
+        # sample inside it: take the poller's next one, right after the region
+        t_end = time.time() + 1.0
+        while not self.lines and time.time() < t_end:
+            time.sleep(0.01)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -584,6 +589,7 @@ def run_ooc(args, dist: Dist) -> None:
     check(lib.bmmgpu_block_timer(1))
     times = [step() for _ in range(args.steps)]
     clocks = sampler.stop()
+    k2clk = read_k2_clock(lib)
     blk_ms, blk_launches = ctypes.c_double(0.0), ctypes.c_uint64(0)
     check(lib.bmmgpu_block_timer_read(ctypes.byref(blk_ms), ctypes.byref(blk_launches)))
     check(lib.bmmgpu_block_timer(0))
@@ -657,15 +663,24 @@ def run_ooc(args, dist: Dist) -> None:
         shared_b.close()
 
 
-def k2_clock(lib, launch_macs: float, kms: float) -> dict:
-    """Effective SM clock of the last K2 launch (clock64 / globaltimer of CTA pair 0's MMA loop,
-    bmmgpu_debug_k2_clock) and the MACs per SM clock it implies: nvidia-smi's clocks.sm does not
-    show the power cap's clock slowdown, this does."""
-    import torch
+def read_k2_clock(lib) -> tuple[int, int]:
+    """(cycles, ns) of CTA pair 0's MMA loop in the last K2 launch (bmmgpu_debug_k2_clock):
+    read right after the timed steps, before any other product runs."""
     cyc, ns = ctypes.c_uint64(0), ctypes.c_uint64(0)
-    if lib.bmmgpu_debug_k2_clock(ctypes.byref(cyc), ctypes.byref(ns)) != 0 or not ns.value:
+    if lib.bmmgpu_debug_k2_clock(ctypes.byref(cyc), ctypes.byref(ns)) != 0:
+        return 0, 0
+    return cyc.value, ns.value
+
+
+def k2_clock(clk: tuple[int, int], launch_macs: float, kms: float) -> dict:
+    """Effective SM clock of the last timed K2 launch (clock64 / globaltimer of CTA pair 0's MMA
+    loop) and the MACs per SM clock it implies: nvidia-smi's clocks.sm does not show the power
+    cap's clock slowdown, this does."""
+    import torch
+    cyc, ns = clk
+    if not ns:
         return {}
-    mhz = cyc.value / ns.value * 1e3
+    mhz = cyc / ns * 1e3
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     per_clk = launch_macs / (kms * 1e-3) / sms / (mhz * 1e6)
     return {"sm_clock_effective_mhz": round(mhz, 1), "mac_per_sm_clock": round(per_clk, 1),
@@ -895,6 +910,7 @@ def run_ours(args, dist: Dist) -> None:
     torch.cuda.synchronize()
     dist.barrier()
     clocks = sampler.stop()
+    k2clk = read_k2_clock(lib)
     blk_ms, blk_launches = ctypes.c_double(0.0), ctypes.c_uint64(0)
     check(lib.bmmgpu_block_timer_read(ctypes.byref(blk_ms), ctypes.byref(blk_launches)))
     check(lib.bmmgpu_block_timer(0))
@@ -990,7 +1006,7 @@ def run_ours(args, dist: Dist) -> None:
                                 "ubench_sustained.cu, 16,375 MAC/SM-clock at an effective 1845 MHz); "
                                 "MEASURED_PEAKS.json has no integer-ALU or fp4 figure")}
     if resolved != 1:
-        roofline.update(k2_clock(lib, launch_bops / 2.0, kms))
+        roofline.update(k2_clock(k2clk, launch_bops / 2.0, kms))
     mp = ROOT / "MEASURED_PEAKS.json"
     if mp.exists() and resolved != 1:
         # cross-check against the driver's bf16 GEMM figure: kind::mxf4 issues 4 MACs per
