@@ -106,12 +106,9 @@ constexpr size_t P_SMEM = size_t(P_STAGES) * P_STAGE + size_t(P_PACKED) + P_CONS
 constexpr uint32_t P_TMEM_COLS = 512;
 // Block scales (UE8M0, uniform): an M128 / N128-per-CTA operand's scales take 4 TMEM
 // columns (rows 32 q + i in lane i, replicated over the 4 lane quarters); 8 each.
-#ifndef BMMGPU_OVL16
-#define BMMGPU_OVL16 0  // 1: scales in [496, 512), accumulator Y at 240: the accumulators overlap in 16 columns
-#endif
-constexpr uint32_t P_SF_EVEN = BMMGPU_OVL16 ? 496 : 480;  // 1.0
-constexpr uint32_t P_SF_ODD = P_SF_EVEN + 8;               // 2.0
-constexpr uint32_t P_SF_BIAS = 496;  // 2^9 block scales of the bias MMA (BMMGPU_EPI_BIAS=0 only)
+constexpr uint32_t P_SF_EVEN = 480;  // 1.0
+constexpr uint32_t P_SF_ODD = 488;   // 2.0
+constexpr uint32_t P_SF_BIAS = 496;  // 2^9 block scales of the bias MMA
 constexpr uint32_t P_MAX_PAIRS = 74;  // 148 SMs
 // kTs (long-K launches): operand A of each stage lives in TMEM columns [P_TS_A + 32 s, + 32)
 // instead of shared memory, next to one accumulator at [0, 256).
@@ -286,38 +283,10 @@ __device__ __forceinline__ uint32_t pack_counts16(const uint32_t (&v)[16]) {
 #ifndef BMMGPU_ACC2
 #define BMMGPU_ACC2 1  // 0: one accumulator (the MMAs wait for the whole drain)
 #endif
-constexpr uint32_t P_ACC_Y = BMMGPU_ACC2 ? (BMMGPU_OVL16 ? 240 : 224) : 0;  // TMEM column of accumulator Y
-// first drain step: the columns the other accumulator overlaps (32, or 16 = half a group)
-constexpr int kOvlHalf = BMMGPU_OVL16 && BMMGPU_ACC2;
+constexpr uint32_t P_ACC_Y = BMMGPU_ACC2 ? 224 : 0;  // TMEM column of accumulator Y
 template <bool kRot>
 __device__ __forceinline__ constexpr int drain_group(int i) {
     return kRot ? (i + 7) & 7 : i;
-}
-// Epilogue-written bias (default): instead of a bias MMA at the head of every tile (one K = 64
-// MMA of constants, 1/65 of a 4096-bit leaf tile's tensor work, on the critical path after the
-// accumulator hand-over), the epilogue stores 2^23 (fp32 0x4B000000) into each 32-column group
-// right after reading it, so the accumulator comes back pre-biased and every MMA accumulates.
-// The kernel prologue biases both accumulators once.
-#ifndef BMMGPU_EPI_BIAS
-#define BMMGPU_EPI_BIAS 1
-#endif
-constexpr uint32_t kBiasBits = 0x4B000000u;  // 2^23 as fp32
-static_assert(!BMMGPU_OVL16 || BMMGPU_EPI_BIAS, "the 16-column overlap needs the bias MMA's scale columns");
-// 8-column stores: the value has to sit in as many consecutive registers as the store has
-// columns, and the drain's registers are already live (a 32-column store spilled)
-__device__ __forceinline__ void rebias_group(uint32_t taddr) {
-    if (BMMGPU_EPI_BIAS)
-#pragma unroll
-        for (int c = 0; c < 32; c += 8) umma::tmem_st8_fill(taddr + c, kBiasBits);
-}
-__device__ __forceinline__ void rebias_half(uint32_t taddr) {
-    if (BMMGPU_EPI_BIAS) {
-        umma::tmem_st8_fill(taddr, kBiasBits);
-        umma::tmem_st8_fill(taddr + 8, kBiasBits);
-    }
-}
-__device__ __forceinline__ void rebias_wait() {
-    if (BMMGPU_EPI_BIAS) umma::tmem_st_wait();
 }
 __device__ __forceinline__ void drain_signal(uint32_t bar_leader, uint32_t lane) {
     umma::fence_before_sync();
@@ -338,25 +307,10 @@ template <bool kGf2, bool kRot>
 __device__ __forceinline__ void drain_accumulator2(uint32_t tacc, uint32_t (&words)[8], uint32_t ovl_leader,
                                                    uint32_t empty_leader, uint32_t lane) {
     uint32_t va[32], vb[32];
-    const uint32_t g0 = tacc + 32 * drain_group<kRot>(0);
-    if (kOvlHalf) {
-        // X overlaps Y in its last 16 columns (upper half of group 7), Y in its first 16
-        constexpr int oh = kRot ? 1 : 0;
-        umma::tmem_ld16(g0 + 16 * oh, half16(va, oh));
-        umma::tmem_ld_wait_regs16(half16(va, oh));
-        rebias_half(g0 + 16 * oh);
-        rebias_wait();
-        drain_signal(ovl_leader, lane);
-        umma::tmem_ld16(g0 + 16 * (1 - oh), half16(va, 1 - oh));
-        umma::tmem_ld_wait_regs16(half16(va, 1 - oh));
-    } else {
-        umma::tmem_ld16(g0, half16(va, 0));
-        umma::tmem_ld16(g0 + 16, half16(va, 1));
-        umma::tmem_ld_wait_regs(va);
-        rebias_group(g0);
-        rebias_wait();
-        drain_signal(ovl_leader, lane);
-    }
+    umma::tmem_ld16(tacc + 32 * drain_group<kRot>(0), half16(va, 0));
+    umma::tmem_ld16(tacc + 32 * drain_group<kRot>(0) + 16, half16(va, 1));
+    umma::tmem_ld_wait_regs(va);
+    drain_signal(ovl_leader, lane);
 #pragma unroll
     for (int i = 0; i < 8; i += 2) {
         umma::tmem_ld16(tacc + 32 * drain_group<kRot>(i + 1), half16(vb, 0));
@@ -367,10 +321,6 @@ __device__ __forceinline__ void drain_accumulator2(uint32_t tacc, uint32_t (&wor
             umma::tmem_ld16(tacc + 32 * drain_group<kRot>(i + 2), half16(va, 0));
             umma::tmem_ld16(tacc + 32 * drain_group<kRot>(i + 2) + 16, half16(va, 1));
         } else {
-#pragma unroll
-            for (int g = 1; g < 8; ++g) rebias_group(tacc + 32 * drain_group<kRot>(g));
-            if (kOvlHalf) rebias_half(g0 + 16 * (kRot ? 0 : 1));
-            rebias_wait();
             drain_signal(empty_leader, lane);
         }
         words[drain_group<kRot>(i + 1)] = pack_counts32<kGf2>(vb);
@@ -405,37 +355,18 @@ template <bool kRot>
 __device__ __forceinline__ void drain_accumulator_gf2_pack16(uint32_t tacc, uint32_t (&words)[8], uint32_t ovl_leader,
                                                              uint32_t empty_leader, uint32_t lane) {
     uint32_t va[16], vb[16];
-    const uint32_t g0 = tacc + 32 * drain_group<kRot>(0);
-    if (kOvlHalf) {
-        constexpr int oh = kRot ? 1 : 0;  // registers 8 oh .. 8 oh + 7 hold columns 16 oh .. 16 oh + 15
-        umma::tmem_ld8_pack16(g0 + 16 * oh, va + 8 * oh);
-        umma::tmem_ld_wait_regs8(va + 8 * oh);
-        rebias_half(g0 + 16 * oh);
-        rebias_wait();
-        drain_signal(ovl_leader, lane);
-        umma::tmem_ld8_pack16(g0 + 16 * (1 - oh), va + 8 * (1 - oh));
-        umma::tmem_ld_wait_regs8(va + 8 * (1 - oh));
-    } else {
-        umma::tmem_ld16_pack16(g0, va);
-        umma::tmem_ld_wait_regs16(va);
-        rebias_group(g0);
-        rebias_wait();
-        drain_signal(ovl_leader, lane);
-    }
+    umma::tmem_ld16_pack16(tacc + 32 * drain_group<kRot>(0), va);
+    umma::tmem_ld_wait_regs16(va);
+    drain_signal(ovl_leader, lane);
 #pragma unroll
     for (int i = 0; i < 8; i += 2) {
         umma::tmem_ld16_pack16(tacc + 32 * drain_group<kRot>(i + 1), vb);
         words[drain_group<kRot>(i)] = pack_pairs16(va);
         umma::tmem_ld_wait_regs16(vb);
-        if (i + 2 < 8) {
+        if (i + 2 < 8)
             umma::tmem_ld16_pack16(tacc + 32 * drain_group<kRot>(i + 2), va);
-        } else {
-#pragma unroll
-            for (int g = 1; g < 8; ++g) rebias_group(tacc + 32 * drain_group<kRot>(g));
-            if (kOvlHalf) rebias_half(g0 + 16 * (kRot ? 0 : 1));
-            rebias_wait();
+        else
             drain_signal(empty_leader, lane);
-        }
         words[drain_group<kRot>(i + 1)] = pack_pairs16(vb);
         if (i + 2 < 8) umma::tmem_ld_wait_regs16(va);
     }
@@ -517,8 +448,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         umma::tmem_st8_fill(tmem + lane_base + P_SF_EVEN, 0x7F7F7F7Fu);
         umma::tmem_st8_fill(tmem + lane_base + P_SF_ODD, 0x80808080u);
         umma::tmem_st8_fill(tmem + lane_base + P_SF_BIAS, 0x88888888u);  // 2^9
-        if (BMMGPU_EPI_BIAS)  // both accumulators start biased (X = [0, 256), Y = [224, 480))
-            for (uint32_t c = 0; c < P_SF_EVEN; c += 16) umma::tmem_st16_fill(tmem + lane_base + c, kBiasBits);
         umma::tmem_st_wait();
     }
     {
@@ -724,7 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                 const uint32_t dacc = tmem + (buf ? P_ACC_Y : 0);
                 TRACE_AT(pair == 0 && lane == 0 && local < 512, 3072 + 4 * local + 3);
                 umma::fence_after_sync();
-                if (!BMMGPU_EPI_BIAS && umma::elect_one() && !PROBE(32))  // preset the accumulator to 2^23
+                if (umma::elect_one() && !PROBE(32))  // preset the accumulator to 2^23
                     umma::mma_mxf4_pair(dacc, desc_const, desc_const, idesc, tmem + P_SF_BIAS, tmem + P_SF_BIAS, 0u);
                 __syncwarp();
                 for (uint64_t k = 0; k < (PROBE(128) ? 0 : n_stages); ++k, ++it, s = (s + 1 == P_STAGES) ? (full_parity ^= 1, 0) : s + 1) {
