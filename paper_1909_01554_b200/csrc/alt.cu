@@ -646,16 +646,17 @@ int alt_serial_levels(uint64_t n, int e, uint64_t budget) {
     return e > 0 ? e - 1 : 0;
 }
 
-uint64_t free_budget() {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
-    return uint64_t(double(free_b) * 0.8);
-}
+uint64_t free_budget(bool refresh = false) { return uint64_t(double(device_free_bytes(refresh)) * 0.8); }
 
-// Depth-first level count for this device (BMMGPU_ALT_SERIAL forces it; tests use it).
+// Depth-first level count for this device (BMMGPU_ALT_SERIAL forces it; tests use it).  The
+// free-memory estimate is non-blocking (device_free_bytes); a plan whose breadth-first part
+// would take more than half of it is re-checked against a fresh query.
 int choose_serial_levels(uint64_t n, int e) {
     if (const char* env = getenv("BMMGPU_ALT_SERIAL")) return std::max(0, std::min(atoi(env), e - 1));
-    return alt_serial_levels(n, e, free_budget());
+    const uint64_t budget = free_budget();
+    const int es = alt_serial_levels(n, e, budget);
+    if (alt_serial_levels(n, e, budget / 2) != es) return alt_serial_levels(n, e, free_budget(true));
+    return es;
 }
 
 // Recursion levels run as passes: the leaf dimension is 2^leaf_log2

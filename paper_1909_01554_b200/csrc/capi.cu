@@ -82,6 +82,44 @@ void enable_pool_caching() {
     }
     done_mask |= 1u << dev;
 }
+// Free device memory without cudaMemGetInfo on every call: measured on the box, that call
+// blocked host threads for 9-68 ms now and then while the device was busy (microbench/
+// c2_steps.py, profiles/r02/c2_step_enqueue.txt), which stalled the enqueue of a whole
+// fast-product step.  One real query per device is kept as a snapshot together with the
+// stream-ordered pool's reserved bytes at that time; later estimates = snapshot free - what
+// the pool reserved since + the pool's idle (reserved, unused) bytes, which the library's
+// own stream-ordered allocations reuse.  Allocations by others after the snapshot are not
+// seen: callers that size a plan close to the estimate ask for a fresh query
+// (device_free_bytes(true)).
+uint64_t device_free_bytes(bool refresh) {
+    static std::mutex mu;
+    static bool have[32] = {};
+    static uint64_t free0[32] = {}, reserved0[32] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 32) return 0;
+    enable_pool_caching();
+    uint64_t reserved = 0, used = 0;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    if (refresh || !have[dev]) {
+        size_t f = 0, t = 0;
+        if (cudaMemGetInfo(&f, &t) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        have[dev] = true;
+        free0[dev] = f;
+        reserved0[dev] = reserved;
+    }
+    const int64_t est = int64_t(free0[dev]) - (int64_t(reserved) - int64_t(reserved0[dev])) +
+                        (int64_t(reserved) - int64_t(used));
+    return est > 0 ? uint64_t(est) : 0;
+}
+
 namespace {
 std::mutex g_stream_mu;
 std::vector<cudaStream_t> g_stream_pool[32];  // idle leased-out-and-returned streams per device
@@ -395,11 +433,15 @@ int run_cubic_slab(SlabJob& job, const uint64_t* A, const uint64_t* B, uint64_t*
             if (total && in_core * 32 <= total && k < 32768) {
                 limit = in_core;
             } else {
-                size_t free_b = 0, total_b = 0;
-                BMMGPU_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+                uint64_t free_b = device_free_bytes(false);
+                if (in_core * 2 > free_b) free_b = device_free_bytes(true);  // close call: a fresh query
                 limit = uint64_t(double(free_b) * 0.9);
-                std::lock_guard<std::mutex> lock(mu);
-                if (job.device < 32) total_mem[job.device] = total_b;
+                if (!total) {
+                    size_t f = 0, t = 0;
+                    BMMGPU_CUDA_TRY(cudaMemGetInfo(&f, &t));
+                    std::lock_guard<std::mutex> lock(mu);
+                    if (job.device < 32) total_mem[job.device] = t;
+                }
             }
         }
         // force_streaming 1: the out-of-core tile driver; 2: the K-outer pipeline.
@@ -800,10 +842,10 @@ int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t 
         // Operands beyond HBM (configs[4]): output tiles of alt-basis block products
         // streamed from host memory (alt_tiles.cu).  In core the recursion needs about six
         // n^2/8 arrays (A, B, Bt, C and the level buffers of the breadth-first part).
-        size_t free_b = 0, total_b = 0;
-        cudaMemGetInfo(&free_b, &total_b);
-        const uint64_t budget = o.device_budget ? o.device_budget : uint64_t(free_b);
         const double need = 6.0 * double(n) * double(n) / 8.0;
+        uint64_t free_b = o.device_budget ? 0 : device_free_bytes(false);
+        if (!o.device_budget && need * 2 > double(free_b)) free_b = device_free_bytes(true);
+        const uint64_t budget = o.device_budget ? o.device_budget : free_b;
         if (o.force_streaming == 1 || need > double(budget))
             return alt_multiply_tiles(A, B, C, n, algo, devs, o.kernel, o.leaf_log2, o.timing_ms, 0, 0, 0);
     }

@@ -45,6 +45,9 @@ inline cudaError_t memcpy_counted(void* dst, const void* src, size_t bytes, cuda
 // buffers of repeated calls are recycled instead of re-mapped, and freeing a
 // level's buffer needs no stream synchronisation.
 void enable_pool_caching();
+// Free bytes on the current device for planning (capi.cu): a cached cudaMemGetInfo snapshot
+// corrected by the memory pool's reservations; refresh = a fresh (possibly blocking) query.
+uint64_t device_free_bytes(bool refresh);
 
 // Non-blocking streams leased from a per-device pool: creating and destroying a
 // stream costs ~100 us of host time (measured, microbench/api_cost.py), three per call

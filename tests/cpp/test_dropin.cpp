@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <chrono>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -212,6 +213,118 @@ void pipeline_host_cases() {
             CHECK(throws<std::invalid_argument>(
                 [&] { pipeline::aggregate(c, SubInstanceIndex::from_flat(0, 1), q, d, plan, small); }));
         }
+    });
+}
+
+// The reference's acceptance criteria C3-C7 (tests/acceptance_main.cpp:167-344), case for case:
+// same plans, seeds, workers and expected counts (C1 is "acceptance C1" below; C2 checks the
+// coefficient-algebra toolkit, which is not part of this engine).
+BitVectorTensor acceptance_hat(int depth, std::uint64_t seed) {  // acceptance_main.cpp:43-51
+    std::vector<std::uint64_t> modes(depth, 4);
+    modes.push_back(kBlockBits);
+    return random_hat(modes, seed);
+}
+
+void acceptance_cases() {
+    run("acceptance C3: combine-phase word XORs at depths 1..3 across serial/parallel splits; program counts", [] {
+        const Decomposition& asi = builtin(Builtin::AltSelfInverse);
+        const Decomposition& ach = builtin(Builtin::AltChaining);
+        const Decomposition& sw = builtin(Builtin::StrassenWinograd);
+        for (int d = 1; d <= 3; ++d) {
+            const std::uint64_t want = 12 * (pow_u64(7, d) - pow_u64(4, d)) / 3 * kBlockWords;
+            for (int ds = 0; ds <= d; ++ds) {
+                const BitVectorTensor a = acceptance_hat(d, 301 + d), b = acceptance_hat(d, 302 + d);
+                OpCounter counter;
+                multiply_alt(a, b, asi, plan_for(ds, d - ds), &counter);
+                CHECK(counter.word_xors.load() == want);
+            }
+        }
+        for (const Decomposition* d : {&asi, &ach})
+            CHECK(d->adds_phi == 2 && d->adds_psi == 2 && d->adds_chi == 2 && d->adds_alpha == 3 &&
+                  d->adds_beta == 3 && d->adds_gamma == 6);
+        CHECK(sw.adds_alpha + sw.adds_beta + sw.adds_gamma == 15);
+    });
+    run("acceptance C4: 7^depth kernels per engine run; 49 sub-instances generated and aggregated once", [] {
+        const Decomposition& asi = builtin(Builtin::AltSelfInverse);
+        for (auto [ds, dp] : {std::pair{1, 0}, std::pair{0, 1}, std::pair{2, 1}, std::pair{1, 2}}) {
+            const int depth = ds + dp;
+            const BitVectorTensor a = acceptance_hat(depth, 401 + depth), b = acceptance_hat(depth, 402 + depth);
+            OpCounter counter;
+            multiply_alt(a, b, asi, plan_for(ds, dp), &counter);
+            CHECK(counter.kernel_invocations.load() == pow_u64(7, depth));
+        }
+        const BitVectorTensor a = acceptance_hat(3, 403), b = acceptance_hat(3, 404);
+        OpCounter counter;
+        pipeline::PipelineStats stats;
+        pipeline::coordinate(a, b, asi, plan_for(0, 1, 2), 4, &counter, &stats);
+        CHECK(counter.kernel_invocations.load() == 343);
+        bool once = stats.prepared_left.size() == 49;
+        for (std::uint64_t f = 0; once && f < stats.prepared_left.size(); ++f)
+            once = stats.prepared_left[f] == 1 && stats.prepared_right[f] == 1 && stats.aggregated[f] == 1;
+        CHECK(once);
+    });
+    run("acceptance C5: n=1024 host-level output bit-identical for workers {1,2,4,8} and 5 repeats", [] {
+        const auto t0 = std::chrono::steady_clock::now();
+        const Decomposition& asi = builtin(Builtin::AltSelfInverse);
+        const BitVectorTensor a = acceptance_hat(4, 501), b = acceptance_hat(4, 502);
+        const BitVectorTensor want = multiply_alt(a, b, asi, plan_for(2, 2));
+        std::uint64_t violations = 0;
+        for (int workers : {1, 2, 4, 8}) {
+            pipeline::PipelineStats stats;
+            CHECK(pipeline::coordinate(a, b, asi, plan_for(1, 1, 2), workers, nullptr, &stats) == want);
+            violations += stats.lock_violations;
+        }
+        for (int r = 0; r < 5; ++r) {
+            pipeline::PipelineStats stats;
+            CHECK(pipeline::coordinate(a, b, asi, plan_for(1, 1, 2), 4, nullptr, &stats) == want);
+            violations += stats.lock_violations;
+        }
+        const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        CHECK(violations == 0 && secs < 60.0);
+    });
+    run("acceptance C6 (soft, as in the reference): alt-si vs cubic crossover up to n = 16384", [] {
+        std::string report = "no crossover observed up to n=16384:";
+        for (std::uint64_t n : {512ull, 1024ull, 2048ull, 4096ull, 8192ull, 16384ull}) {
+            const BitMatrix a = BitMatrix::random(n, n, 601), b = BitMatrix::random(n, n, 602);
+            const LayerPlan plan = LayerPlan::auto_plan(n, 4);
+            std::vector<double> ct, at;
+            for (int r = 0; r < 3; ++r) {
+                auto t0 = std::chrono::steady_clock::now();
+                multiply_cubic(a, b, Semiring::Gf2XorAnd, 4);
+                ct.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+                t0 = std::chrono::steady_clock::now();
+                multiply(a, b, Algo::AltSelfInverse, plan, Semiring::Gf2XorAnd);
+                at.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+            }
+            std::sort(ct.begin(), ct.end());
+            std::sort(at.begin(), at.end());
+            char buf[120];
+            std::snprintf(buf, sizeof(buf), " n=%llu cubic %.4fs vs alt-si %.4fs", (unsigned long long)n, ct[1], at[1]);
+            if (at[1] < ct[1]) {
+                report = std::string("crossover at") + buf;
+                break;
+            }
+            report += buf;
+        }
+        std::printf("C6: %s\n", report.c_str());
+    });
+    run("acceptance C7: three-matrix chain with one final basis change equals the cubic triple product", [] {
+        const Decomposition& ach = builtin(Builtin::AltChaining);
+        const LayerPlan plan = LayerPlan::auto_plan(256, 1);
+        const BitMatrix m0 = BitMatrix::random(256, 256, 701), m1 = BitMatrix::random(256, 256, 702),
+                        m2 = BitMatrix::random(256, 256, 703);
+        const BitMatrix want = multiply_cubic(multiply_cubic(m0, m1, Semiring::Gf2XorAnd), m2, Semiring::Gf2XorAnd);
+        BitVectorTensor left = to_interleaved(m0, plan, Operand::Left);
+        basis_change(left, ach, BasisFactor::Phi, plan.depth());
+        std::vector<BitVectorTensor> operands = {std::move(left)};
+        for (const BitMatrix* m : {&m1, &m2}) {
+            BitVectorTensor hat = to_interleaved(*m, plan, Operand::Right);
+            basis_change(hat, ach, BasisFactor::Psi, plan.depth());
+            operands.push_back(std::move(hat));
+        }
+        BitVectorTensor c_hat = chain_multiply(operands, ach, plan);
+        basis_change(c_hat, ach, BasisFactor::Chi, plan.depth());
+        CHECK(from_interleaved(c_hat, plan, Operand::Result) == want);
     });
 }
 
@@ -636,6 +749,7 @@ void gpu_cases() {
         CHECK(from_interleaved(ch, p, Operand::Result) == want);
         CHECK(throws<std::invalid_argument>([&] { (void)chain_multiply(ops, builtin(Builtin::AltSelfInverse), p); }));
     });
+    acceptance_cases();
     pipeline_gpu_cases();
 }
 
