@@ -46,4 +46,7 @@ def test_dropin_products_on_gpu(dropin_binary, pipeline):
     host-thread pipeline with BMM_PIPELINE=host -- both against the reference's outputs
     and counters."""
     out = _run(dropin_binary, "gpu", {"BMM_PIPELINE": pipeline})
+    for line in out.splitlines():
+        if line.startswith("C6:"):  # the reference's soft crossover criterion, reported not asserted
+            print(line)
     assert "0 failures" in out
