@@ -47,13 +47,14 @@ struct K64State {
     uint64_t* dev = nullptr;   // device alias of host
     cudaStream_t stream = nullptr;
     ~K64State() {
-        if (host) {
-            int prev = 0;
-            if (cudaGetDevice(&prev) == cudaSuccess && prev != device) cudaSetDevice(device);
-            if (stream) cudaStreamDestroy(stream);
-            cudaFreeHost(host);
-            if (prev != device) cudaSetDevice(prev);
-        }
+        // thread exit; at process exit the runtime may already be unloading (then the OS
+        // reclaims the 1.5 KB and the stream)
+        int prev = 0;
+        if (!host || cudaGetDevice(&prev) != cudaSuccess) return;
+        if (prev != device) cudaSetDevice(device);
+        if (stream) cudaStreamDestroy(stream);
+        cudaFreeHost(host);
+        if (prev != device) cudaSetDevice(prev);
     }
 };
 thread_local K64State t_k64;

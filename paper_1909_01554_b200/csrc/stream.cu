@@ -100,7 +100,8 @@ int stream_cubic_slab(int device, uint64_t row_begin, uint64_t row_end, const ui
     const uint64_t gkw = gk / 64;
     const uint64_t ka = ceil_div(k, 64), nb = ceil_div(n, 64);
     const uint64_t kw = round_up(std::max<uint64_t>(ka, 1), gkw);
-    if (budget == 0) budget = uint64_t(double(device_free_bytes(false)) * 0.9);
+    // out-of-core calls run for seconds: a fresh (possibly blocking) query costs nothing here
+    if (budget == 0) budget = uint64_t(double(device_free_bytes(true)) * 0.9);
     const Plan P = plan_tiles(m, n, kw, gm, gn, gkw, budget);
     if (P.bytes > budget) {
         set_error("out-of-core driver: even the smallest tiles (" + std::to_string(P.bytes) +
