@@ -420,14 +420,15 @@ def test_wave_aligned_mode_matches_oracle(engine, oracle, ring):
 def test_tmem_operand_mode_matches_oracle(engine, oracle, ring):
     """Long-K launches keep operand A in tensor memory (kTs: tcgen05.mma with A from TMEM,
     one accumulator).  Through the device API, one launch each: 2560 x 32768 x 2048 (80 tiles
-    over 74 pairs, 128 K-stages) and 768 x 65536 x 512 (256 stages, fewer tiles than pairs),
-    the second also with the accumulate flag (the K-chunk fold); the debug counter proves the
+    over 74 pairs, 128 K-stages), 768 x 65536 x 512 (256 stages, fewer tiles than pairs) and
+    512 x 33024 x 768 (129 stages: a partial superstage at the end of K), the second also with
+    the accumulate flag (the K-chunk fold); the debug counter proves the
     mode ran; word for word against the oracle (Boolean on AND-of-7 inputs)."""
     import torch
     bmm = engine
     lib = bmm.lib()
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    for m, k, n, seed in ((2560, 32768, 2048, 701), (768, 65536, 512, 731)):
+    for m, k, n, seed in ((2560, 32768, 2048, 701), (768, 65536, 512, 731), (512, 33024, 768, 761)):
         a = oracle.random(m, k, seed)
         b = oracle.random(k, n, seed + 1)
         if ring == BOOL:
