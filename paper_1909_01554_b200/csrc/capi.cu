@@ -10,7 +10,9 @@
 // segment").
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -171,7 +173,9 @@ bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-// Two 64 MiB page-locked slots per device, allocated on first use and kept.
+// Two 64 MiB page-locked slots per device and direction, allocated on first use and kept:
+// uploads and downloads stage concurrently (the streamed fast path downloads finished C
+// quadrants while later operand quadrants go up).
 struct Stager {
     static constexpr size_t kSlot = size_t(64) << 20;
     std::mutex mu;
@@ -188,31 +192,95 @@ struct Stager {
         return true;
     }
 };
-Stager g_stagers[16];
+Stager g_stagers[16][2];  // [device][0: host -> device, 1: device -> host]
+
+// Persistent memcpy helpers for the staged copies: spawning threads per 64 MiB chunk cost
+// a large share of the chunk's time (staged uploads measured 10.8 GB/s against 63 GB/s for
+// an 8-thread memcpy on the box, microbench/staging.py, memcpy_bw.cu).  run(n, f) calls
+// f(0) .. f(n - 1), f(0) on the caller, the rest on the pool.
+class CopyPool {
+  public:
+    static CopyPool& get() {
+        static CopyPool* pool = new CopyPool();  // never destroyed: workers may outlive main
+        return *pool;
+    }
+    unsigned width() const { return unsigned(workers_.size()) + 1; }
+    void run(unsigned n, const std::function<void(unsigned)>& f) {
+        std::lock_guard<std::mutex> one(call_mu_);  // one staged copy at a time per pool
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_ = &f;
+            parts_ = n;
+            next_ = 1;
+            pending_ = n - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    CopyPool() {
+        const unsigned hc = std::thread::hardware_concurrency();
+        const unsigned n = std::max(1u, std::min(8u, hc ? hc / 2 : 4u));
+        for (unsigned i = 0; i + 1 < n; ++i) workers_.emplace_back([this] { loop(); });
+        for (auto& t : workers_) t.detach();
+    }
+    void loop() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return gen_ != seen && job_ && next_ < parts_; });
+            seen = gen_;
+            while (job_ && next_ < parts_) {
+                const unsigned i = next_++;
+                const std::function<void(unsigned)>* f = job_;
+                lk.unlock();
+                (*f)(i);
+                lk.lock();
+                if (--pending_ == 0) done_cv_.notify_one();
+            }
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(unsigned)>* job_ = nullptr;
+    unsigned parts_ = 0, next_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+};
 
 // `rows` rows of `width` bytes from src (pitch spitch) to dst (pitch dpitch), split
-// across host threads (8 MiB per thread, at most 4)
+// across the copy pool (8 MiB per part, at most the pool's width: one memcpy thread
+// moves ~8-10 GB/s, the link takes ~55 GB/s)
 void copy_rows(char* dst, size_t dpitch, const char* src, size_t spitch, size_t width, size_t rows) {
     const size_t bytes = rows * width;
-    const unsigned n_thr = unsigned(std::min<size_t>(4, std::max<size_t>(1, bytes >> 23)));
-    auto part = [&](size_t a, size_t b) {
-        for (size_t r = a; r < b; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, width);
+    CopyPool& pool = CopyPool::get();
+    const unsigned n = unsigned(std::min<size_t>(pool.width(), std::max<size_t>(1, bytes >> 23)));
+    const size_t step = (rows + n - 1) / n;
+    auto part = [&](unsigned i) {
+        const size_t a = std::min(rows, i * step), b = std::min(rows, (i + 1) * step);
+        if (width == spitch && width == dpitch)
+            std::memcpy(dst + a * dpitch, src + a * spitch, (b - a) * width);
+        else
+            for (size_t r = a; r < b; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, width);
     };
-    if (n_thr == 1) {
-        part(0, rows);
-        return;
-    }
-    std::vector<std::thread> thr;
-    const size_t step = (rows + n_thr - 1) / n_thr;
-    for (unsigned i = 0; i < n_thr; ++i) thr.emplace_back(part, std::min(rows, i * step), std::min(rows, (i + 1) * step));
-    for (auto& t : thr) t.join();
+    if (n == 1)
+        part(0);
+    else
+        pool.run(n, part);
 }
 
 }  // namespace
 
-cudaError_t memcpy2d_counted(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
-                             cudaMemcpyKind kind, cudaStream_t s) {
-    count_copy(kind, uint64_t(width) * height);
+namespace {
+// The staged copy proper (no byte counting): pageable host buffers go through the page-locked
+// slots, everything else straight to cudaMemcpy2DAsync.
+cudaError_t memcpy2d_staged(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                            cudaMemcpyKind kind, cudaStream_t s) {
     const bool h2d = kind == cudaMemcpyHostToDevice, d2h = kind == cudaMemcpyDeviceToHost;
     const void* host = h2d ? src : d2h ? static_cast<const void*>(dst) : nullptr;
     int dev = 0;
@@ -221,7 +289,7 @@ cudaError_t memcpy2d_counted(void* dst, size_t dpitch, const void* src, size_t s
     if (disabled || !host || width * height < (size_t(16) << 20) || width > Stager::kSlot || dev < 0 || dev >= 16 ||
         is_pinned(host))
         return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, s);
-    Stager& st = g_stagers[dev];
+    Stager& st = g_stagers[dev][h2d ? 0 : 1];
     std::lock_guard<std::mutex> lk(st.mu);
     if (!st.init()) return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, s);
     const size_t rows_per = std::max<size_t>(1, Stager::kSlot / width);
@@ -264,6 +332,26 @@ cudaError_t memcpy2d_counted(void* dst, size_t dpitch, const void* src, size_t s
                   width, width, pending_r1 - pending_r0);
     }
     return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t memcpy2d_counted(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                             cudaMemcpyKind kind, cudaStream_t s) {
+    count_copy(kind, uint64_t(width) * height);
+    // A contiguous region wider than a staging slot (memcpy_counted of a whole operand is one
+    // "row" of hundreds of MiB) is staged as rows of 1 MiB: it used to fall through to the
+    // runtime's own pageable copy, ~10 GB/s against ~50 staged (microbench/staging.py)
+    constexpr size_t kPiece = size_t(1) << 20;
+    if (width > (size_t(64) << 20) && (height == 1 || (spitch == width && dpitch == width))) {
+        const size_t total = width * height, main = total / kPiece * kPiece;
+        if (main) {
+            const cudaError_t e = memcpy2d_staged(dst, kPiece, src, kPiece, kPiece, main / kPiece, kind, s);
+            if (e != cudaSuccess || total == main) return e;
+        }
+        return cudaMemcpyAsync(static_cast<char*>(dst) + main, static_cast<const char*>(src) + main, total - main,
+                               kind, s);
+    }
+    return memcpy2d_staged(dst, dpitch, src, spitch, width, height, kind, s);
 }
 
 int resolve_kernel(int kernel) {
