@@ -283,13 +283,16 @@ def test_inner_dimension_beyond_fp32_exact_range(engine, kernel):
         assert np.array_equal(got.words, want), (kernel, ring)
 
 
-def test_pageable_host_buffers_are_staged(engine, oracle):
+@pytest.mark.parametrize("shape", [(2048, 8192, 131072), (1024, 8256, 66560)])
+def test_pageable_host_buffers_are_staged(engine, oracle, shape):
     """Large pageable operands (the reference API's std::vector storage) go through the
     library's pinned staging slots: same bits as the call on page-locked buffers, and
-    rows checked independently."""
+    rows checked independently.  First shape: B 128 MiB and C 32 MiB, both directions
+    staged; second: B is 65.5 MiB, a contiguous copy wider than a staging slot that is
+    not a whole number of the 1 MiB rows it is reshaped into (the remainder path)."""
     import torch
     bmm = engine
-    m, k, n = 2048, 8192, 131072  # B 128 MiB and C 32 MiB: both directions staged
+    m, k, n = shape
     a = oracle.random(m, k, 301)
     b = oracle.random(k, n, 302)
     for ring in (GF2, BOOL):
@@ -301,12 +304,12 @@ def test_pageable_host_buffers_are_staged(engine, oracle):
                                     bmm.BitMatrix(k, n, hb.numpy().view(np.uint64)), bmm.Semiring(ring),
                                     out=bmm.BitMatrix(m, n, hc.numpy().view(np.uint64)))
         assert np.array_equal(got.words, pinned.words), ring
-        B = b.reshape(k, n // 64)
+        B = b.reshape(k, -(-n // 64))
         for i in (0, 777, m - 1):
-            bits = np.unpackbits(a.reshape(m, k // 64)[i].view(np.uint8), bitorder="little")[:k]
+            bits = np.unpackbits(a.reshape(m, -(-k // 64))[i].view(np.uint8), bitorder="little")[:k]
             sel = B[np.flatnonzero(bits)]
             want = np.bitwise_xor.reduce(sel, axis=0) if ring == GF2 else np.bitwise_or.reduce(sel, axis=0)
-            assert np.array_equal(got.words.reshape(m, n // 64)[i], want), (ring, i)
+            assert np.array_equal(got.words.reshape(m, -(-n // 64))[i], want), (ring, i)
 
 
 def test_concurrent_long_k_products_on_one_device(engine, oracle):
