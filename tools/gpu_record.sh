@@ -8,7 +8,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 600 python bench.py > $O/bench_c3_bool.log 2>&1
 timeout 600 python bench.py --impl reference > $O/bench_reference_c3.log 2>&1
 timeout 600 python bench.py --workload c3-gf2-cubic-131072 --no-cpu-baseline > $O/bench_c3_gf2.log 2>&1
-timeout 600 python bench.py --workload c2-gf2-altsi-65536 > $O/bench_c2_altsi.log 2>&1
+timeout 600 python bench.py --workload c2-gf2-altsi-65536 --e2e-steps 20 > $O/bench_c2_altsi.log 2>&1
 timeout 600 python bench.py --workload c2-gf2-altsi-65536 --impl reference > $O/bench_reference_c2.log 2>&1
 timeout 600 python bench.py --workload c1-gf2-cubic-8192 > $O/bench_c1_gf2.log 2>&1
 timeout 600 python bench.py --workload c1-bool-cubic-8192 > $O/bench_c1_bool.log 2>&1
