@@ -84,16 +84,21 @@ __global__ void __launch_bounds__(256) transpose_kernel(const uint64_t* __restri
 // one 16-byte piece of 32 different rows per warp instruction, so its L1 wavefronts,
 // not DRAM, bound it (ncu: L1/TEX 77 %, DRAM 28 %).  Here the global side is
 // row-contiguous -- four lanes cover a row's 64 bytes, a warp instruction touches 8
-// rows -- and the 64 x 64 bit transposes work from shared memory (rows padded to 9 words:
-// conflict-free column reads and writes).  The tile is staged in, transposed in
-// registers, written back into the same buffer, and streamed out.
+// rows -- and the 64 x 64 bit transposes work from shared memory.  The tile is staged in,
+// transposed in registers, written back into the same buffer, and streamed out.
+// Shared layout: 8 words per row, word c of row r at c ^ ((r >> 1) & 7).  Both access
+// patterns are conflict-free per half-warp (16 lanes x 8 bytes): the row-contiguous ones
+// (4 lanes per row, rows r .. r + 3) see 4 distinct word groups per row pair, the column
+// ones (one word of rows r .. r + 15) 16 distinct (r & 1, word) pairs.  (Round 1 padded
+// rows to 9 words: conflict-free columns but 23 % of the row-side wavefronts conflicted,
+// profiles/r01/full_transpose_staged_c2.txt.)
 constexpr int TS_ROWS = TB * 64;  // 512 rows of B per tile
-constexpr int TS_PAD = TB + 1;    // words per padded smem row
+__device__ __forceinline__ int ts_at(int r, int c) { return r * TB + (c ^ ((r >> 1) & 7)); }
 
 __global__ void __launch_bounds__(256) transpose_staged_kernel(const uint64_t* __restrict__ B, uint64_t ldb,
                                                                uint64_t k, uint64_t n, uint64_t* __restrict__ Bt,
                                                                uint64_t n_pad, uint64_t kw, uint64_t ldbt) {
-    __shared__ uint64_t tile[TS_ROWS * TS_PAD];
+    __shared__ uint64_t tile[TS_ROWS * TB];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t nb_words = (n + 63) / 64;
     const uint64_t bj0 = blockIdx.x * uint64_t(TB);        // first word column (N direction)
@@ -119,9 +124,9 @@ __global__ void __launch_bounds__(256) transpose_staged_kernel(const uint64_t* _
                 if (c == nb_words - 1) v0 &= tail_mask;
                 if (c + 1 == nb_words - 1) v1 &= tail_mask;
             }
-            uint64_t* d = tile + (rr + 64 * i) * TS_PAD + 2 * q;
-            d[0] = v0;
-            d[1] = v1;
+            const int r = rr + 64 * i;
+            tile[ts_at(r, 2 * q)] = v0;
+            tile[ts_at(r, 2 * q + 1)] = v1;
         }
     }
     __syncthreads();
@@ -129,16 +134,16 @@ __global__ void __launch_bounds__(256) transpose_staged_kernel(const uint64_t* _
     uint64_t x0[TB], x1[TB];
 #pragma unroll
     for (int b = 0; b < TB; ++b) {
-        x0[b] = tile[(warp * 64 + lane) * TS_PAD + b];
-        x1[b] = tile[(warp * 64 + 32 + lane) * TS_PAD + b];
+        x0[b] = tile[ts_at(warp * 64 + lane, b)];
+        x1[b] = tile[ts_at(warp * 64 + 32 + lane, b)];
     }
     __syncthreads();
 #pragma unroll
     for (int b = 0; b < TB; ++b) {
         warp_transpose64(x0[b], x1[b], lane);
-        // Bt row (bj0 + b) * 64 + j, K word blockIdx.y * 8 + warp -> tile[(b * 64 + j) * TS_PAD + warp]
-        tile[(b * 64 + lane) * TS_PAD + warp] = x0[b];
-        tile[(b * 64 + 32 + lane) * TS_PAD + warp] = x1[b];
+        // Bt row (bj0 + b) * 64 + j, K word blockIdx.y * 8 + warp -> tile[ts_at(b * 64 + j, warp)]
+        tile[ts_at(b * 64 + lane, warp)] = x0[b];
+        tile[ts_at(b * 64 + 32 + lane, warp)] = x1[b];
     }
     __syncthreads();
     // 3. Bt rows (bj0 * 64) .. +511, K words blockIdx.y * 8 .. +7: four lanes per row
@@ -149,12 +154,13 @@ __global__ void __launch_bounds__(256) transpose_staged_kernel(const uint64_t* _
         for (int i = 0; i < TS_ROWS / 64; ++i) {
             const uint64_t trow = bj0 * 64 + rr + 64 * i;
             if (trow >= n_pad) continue;
-            const uint64_t* sp = tile + (rr + 64 * i) * TS_PAD + 2 * q;
+            const int r = rr + 64 * i;
+            const uint64_t w0 = tile[ts_at(r, 2 * q)], w1 = tile[ts_at(r, 2 * q + 1)];
             uint64_t* dst = Bt + trow * ldbt + kw0;
             if (kw0 + 1 < kw)
-                *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(sp[0], sp[1]);
+                *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(w0, w1);
             else if (kw0 < kw)
-                dst[0] = sp[0];
+                dst[0] = w0;
         }
     }
 }
