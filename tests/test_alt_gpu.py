@@ -308,3 +308,29 @@ def test_level_shifted_leaves_match_reference(engine, oracle, golden, monkeypatc
             got = bmm.multiply(bmm.BitMatrix(n, n, a), bmm.BitMatrix(n, n, b), algo, bmm.LayerPlan.auto_plan(n, 1),
                                bmm.Semiring.Gf2XorAnd, leaf_log2=leaf)
             assert np.array_equal(got.words, want), (algo, n, leaf)
+
+
+@pytest.mark.parametrize("algo", [1, 2, 3])
+def test_production_leaves_every_scheme_against_reference_digest(engine, oracle, golden, algo):
+    """The production leaf size (4096-bit leaves on the tcgen05 kernel) for sw, alt-si and
+    alt-chain: n = 8192 (one recursion level) must reproduce the reference's own n = 8192
+    GF(2) product digest (golden cubic_large, seeds 1 and 2); n = 16384 (one fused
+    two-level expand / compress pass around 49 leaves) must equal the cubic product of the
+    same operands and pass Freivalds-style row checks in numpy."""
+    bmm = engine
+    cub = next(x for x in golden["cubic_large"] if x["m"] == 8192 and x["ring"] == GF2)
+    a = bmm.BitMatrix(8192, 8192, oracle.random(8192, 8192, cub["a_seed"]))
+    b = bmm.BitMatrix(8192, 8192, oracle.random(8192, 8192, cub["b_seed"]))
+    plan = bmm.LayerPlan.auto_plan(8192, 1)
+    got = bmm.multiply(a, b, bmm.Algo(algo), plan, bmm.Semiring.Gf2XorAnd, leaf_log2=12)
+    assert f"{oracle.fnv1a64(got.words):016x}" == cub["fnv"], algo
+    n = 16384
+    a = bmm.BitMatrix(n, n, oracle.random(n, n, 41))
+    b = bmm.BitMatrix(n, n, oracle.random(n, n, 42))
+    got = bmm.multiply(a, b, bmm.Algo(algo), bmm.LayerPlan.auto_plan(n, 1), bmm.Semiring.Gf2XorAnd, leaf_log2=12)
+    want = bmm.multiply_cubic(a, b, bmm.Semiring.Gf2XorAnd)
+    assert np.array_equal(got.words, want.words), algo
+    B = b.words.reshape(n, n // 64)
+    for i in (0, 4097, n - 1):
+        bits = np.unpackbits(a.words.reshape(n, n // 64)[i].view(np.uint8), bitorder="little")
+        assert np.array_equal(got.words.reshape(n, n // 64)[i], np.bitwise_xor.reduce(B[np.flatnonzero(bits)], axis=0))
