@@ -53,10 +53,16 @@
 //     32-column TMEM loads (GF(2): .pack::16b, two columns per register), the group that
 //     overlaps the other accumulator first (then `ovl`), release the accumulator
 //     (acc_empty) as soon as the last load lands, pack the bits, store.
-// Measured (ncu, microbench/trace_tiles.py, time_leaf.py): the tensor pipe is 98-99%
-// active on long K, held at ~1.8 GHz by the board power cap; on 4096-bit leaves each
-// tile boundary costs ~0.5 us (drain, bias MMA, commit / restart latency) against a
-// ~4.56 us tile.
+// kTs (long-K launches, >= BMMGPU_TS_MIN_STAGES stages): operand A of each stage goes to
+//   the expander thread's own TMEM lane instead of shared memory (one tcgen05.st.32x32b.x32
+//   per row and stage, A ring at TMEM columns 256 + 32 s) and the MMAs read it from there;
+//   one accumulator at [0, 256).  Halving the operand stores is worth SM clock under the
+//   power cap (c3 1730 -> 1761 MHz effective, 8.34 -> 8.43 Pbop/s, profiles/r02).
+// Measured (ncu, clock64 / globaltimer, microbench/trace_tiles.py, time_leaf.py,
+// probe_leaf.py): on long K the kernel issues 0.99 of the tensor pipe's 16,384 MACs per SM
+// clock (tensor pipe 98.9 % active) at an effective ~1.76 GHz set by the board power cap;
+// on 4096-bit leaves each tile boundary costs ~0.45 us (commit -> epilogue -> overlap drain
+// -> ovl -> next tile's MMAs) against a ~4.56 us tile.
 #include <cuda.h>
 
 #include <atomic>
