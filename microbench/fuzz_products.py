@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import os
 import random
 import sys
 import time
@@ -71,10 +72,12 @@ def cubic_case(i: int) -> dict | None:
     ha, pa = host(a, pinned)
     hb, pb = host(b, pinned)
     hc, pc = host(c0.copy(), pinned)
-    opts = bmm._opts(kernel, accumulate=accumulate, device_budget=budget, force_streaming=mode)
+    mask = rng.choice([0, 0, 0, 3, 5, 15])  # several bits: logical devices on the one GPU
+    os.environ["BMMGPU_LOGICAL_DEVICES"] = "4"
+    opts = bmm._opts(kernel, accumulate=accumulate, device_budget=budget, force_streaming=mode, device_mask=mask)
     st = lib.bmmgpu_cubic(pa, pb, pc, m, k, n, ring, ctypes.byref(opts))
     case = {"kind": "cubic", "m": m, "k": k, "n": n, "ring": ring, "kernel": kernel, "mode": mode, "budget": budget,
-            "pinned": pinned, "accumulate": accumulate}
+            "pinned": pinned, "accumulate": accumulate, "device_mask": mask}
     if st != 0:
         msg = lib.bmmgpu_last_error().decode()
         # a budget below the smallest out-of-core plan is a legitimate refusal
@@ -103,10 +106,15 @@ def alt_case(i: int) -> dict | None:
     hb, pb = host(b, pinned)
     hc, pc = host(np.zeros(n * n // 64, dtype=np.uint64), pinned)
     ds = rng.randint(0, depth)
-    plan = bmm._Plan(0, ds, depth - ds, 1, 1)
-    opts = bmm._opts(0, leaf_log2=leaf)
+    mask = rng.choice([0, 0, 3, 15])  # several bits: sub-instances dealt over logical devices
+    dh = rng.randint(0, min(2, depth)) if mask else 0
+    ds = min(ds, depth - dh)
+    plan = bmm._Plan(dh, ds, depth - ds - dh, 1, 1)
+    os.environ["BMMGPU_LOGICAL_DEVICES"] = "4"
+    opts = bmm._opts(0, leaf_log2=leaf, device_mask=mask)
     st = lib.bmmgpu_multiply(pa, pb, pc, n, algo, ctypes.byref(plan), 1, ctypes.byref(opts))
-    case = {"kind": "alt", "n": n, "algo": algo, "leaf": leaf, "plan": [0, ds, depth - ds], "pinned": pinned}
+    case = {"kind": "alt", "n": n, "algo": algo, "leaf": leaf, "plan": [dh, ds, depth - ds - dh], "pinned": pinned,
+            "device_mask": mask}
     if st != 0:
         return {**case, "status": st, "error": lib.bmmgpu_last_error().decode()}
     if not np.array_equal(words_of(hc), want):
