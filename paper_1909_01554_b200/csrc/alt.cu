@@ -766,9 +766,11 @@ int alt_multiply_host_streamed(const uint64_t* A, const uint64_t* B, uint64_t* C
     // BMMGPU_ALT_STREAM_LEVELS forces: 1 quadrants, 2 all children split, 3 first / last.
     const char* lv_env = getenv("BMMGPU_ALT_STREAM_LEVELS");
     const int stream_mode = lv_env ? atoi(lv_env) : (n >= (1u << 17) ? 2 : 3);
+    // BMMGPU_ALT_SPLIT_MASK (dev): which child positions run as grandchildren (bit i = position i)
+    const char* sm_env = getenv("BMMGPU_ALT_SPLIT_MASK");
+    const uint32_t split_mask = sm_env ? uint32_t(strtoul(sm_env, nullptr, 0)) & 0x7Fu : stream_mode == 2 ? 0x7Fu : 0x41u;
     if (stream_mode >= 2 && e >= 3 && n >= 1024 && host_pinned(A) && host_pinned(B) && host_pinned(C))
-        return alt_multiply_host_streamed2(A, B, C, n, sc, e, kernel, order, stream_mode == 2 ? 0x7Fu : 0x41u,
-                                           timing_ms);
+        return alt_multiply_host_streamed2(A, B, C, n, sc, e, kernel, order, split_mask, timing_ms);
     int last_pos[4] = {-1, -1, -1, -1};  // position in `order` after which quadrant q of C is final
     for (int i = 0; i < 7; ++i)
         for (int q = 0; q < 4; ++q)
