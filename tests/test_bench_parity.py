@@ -36,3 +36,23 @@ def test_freivalds_and_numpy_rows_accept_truth_and_reject_flips(oracle, ring):
         if ring == 1:
             assert not bench.freivalds_gf2(T(a, m), T(b, k), T(bad, m), m, k, n)
         assert not bench.spot_check(a, b, bad, n, ring, [i], j, m)
+
+
+def test_reference_arm_without_the_reference_prints_unavailable(monkeypatch, capsys):
+    """`bench.py --impl reference` on a box where oracle/_ref is missing (and the reference
+    sources absent) must still print its one JSON line -- {"impl": "reference",
+    "unavailable": ...} -- and return normally, not crash the driver's run."""
+    import json
+    import sys
+    from pathlib import Path
+    import oracle
+    monkeypatch.setattr(oracle, "REF_SO", Path("/nonexistent/libbmmref.so"))
+    monkeypatch.setattr(oracle, "REF_SRC", Path("/nonexistent/proj"))
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0"])
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        monkeypatch.delenv(k, raising=False)
+    bench.main()
+    lines = [ln for ln in capsys.readouterr().out.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    rec = json.loads(lines[0])
+    assert rec["impl"] == "reference" and "unavailable" in rec
