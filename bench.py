@@ -564,6 +564,16 @@ def run_ooc(args, dist: Dist) -> None:
     budget = args.device_budget or OOC_BUDGET
     opts = bmm._opts(0 if args.kernel == "auto" else KERNEL_IDS[args.kernel], device_mask=1 << dev,
                      device_budget=budget, force_streaming=1)
+    # fast GF(2) on one rank: the sub-instance driver (BMMGPU_ALT_OOC=tiles or several ranks: output tiles)
+    subinst = algo != 0 and dist.world == 1 and os.environ.get("BMMGPU_ALT_OOC") != "tiles"
+    plan_c = bmm._Plan(0, (n // 64).bit_length() - 1, 0, 1, 1)
+    dh_sub = 0
+    if subinst:
+        depth = (n // 64).bit_length() - 1
+        e_all = max(0, min(depth, depth + 6 - (args.leaf_log2 or 12)))
+        # the library's choice (alt.cu subinst_levels): the two generated children and ~11 sub-instance arrays
+        dh_sub = next((d for d in range(1, 5) if d < e_all and (n >> d) >= 8192
+                       and 2 * (n // 2) ** 2 / 8 + 11 * (n >> d) ** 2 / 8 <= budget), min(max(1, e_all - 1), 4))
 
     def check(rc: int) -> None:
         if rc != 0:
@@ -574,6 +584,11 @@ def run_ooc(args, dist: Dist) -> None:
         s0 = time.perf_counter()
         if algo == 0:
             check(lib.bmmgpu_cubic(hA.data_ptr(), hB.data_ptr(), hC.data_ptr(), m, n, n, ring, ctypes.byref(opts)))
+        elif subinst:
+            # one rank: bmmgpu_multiply's out-of-core driver runs the recursion's own top-level
+            # sub-instances (7^dh of n >> dh, generated on the device from streamed sub-blocks)
+            check(lib.bmmgpu_multiply(hA.data_ptr(), hB.data_ptr(), hC.data_ptr(), n, algo, ctypes.byref(plan_c),
+                                      GF2, ctypes.byref(opts)))
         else:
             # the library addresses A and C as whole n x n matrices and touches only this
             # rank's panel rows: hand it base pointers r0 rows before the slab buffers
@@ -620,6 +635,14 @@ def run_ooc(args, dist: Dist) -> None:
     kms = blk_ms.value / args.steps
     if algo == 0:
         launch_bops, kname = eff_bops(m, n, n), "cubic_umma2_kernel (K-chunk products of the tile driver)"
+    elif subinst:
+        # leaf layers of the 7^dh sub-instances: 7^e products of L = n >> e in all
+        depth = (n // 64).bit_length() - 1
+        e_levels = max(0, min(depth, depth + 6 - (args.leaf_log2 or 12)))
+        leaf = n >> e_levels
+        launch_bops = 7**e_levels * eff_bops(leaf, leaf, leaf)
+        kname = (f"cubic_umma2_kernel (leaf layers of the 7^{dh_sub} sub-instances of {n >> dh_sub}: "
+                 f"7^{e_levels} products of {leaf}^3 in all)")
     else:
         # leaf layers of the (n/b)^2 (m/b) block products: 7^e products of L = b >> e each
         bt = 1 << tile_log2
@@ -639,8 +662,12 @@ def run_ooc(args, dist: Dist) -> None:
                            "algo": ["cubic", "sw", "alt-si", "alt-chain"][algo], "rows_per_rank": m,
                            "device_budget_bytes": budget if algo == 0 else None,
                            "driver": ("out-of-core tiles (force_streaming=1)" if algo == 0 else
+                                      f"out-of-core sub-instances (bmmgpu_multiply: 7^{dh_sub} = {7 ** dh_sub} of "
+                                      f"{n >> dh_sub}, generated on the device from streamed sub-blocks, "
+                                      f"Q folded into C by host threads)" if subinst else
                                       f"out-of-core alt tiles (bmmgpu_multiply_panels, b = 2^{tile_log2}, "
                                       f"panels [{p0}, {p1}) on rank 0)"),
+                           "device_budget_bytes_alt": budget if subinst else None,
                            "value_is": "end to end from pinned host buffers (the operands exceed the budget)",
                            "input_generation_s": t_gen,
                            "parallelism": f"output row slabs x{dist.world}, no exchange"},
@@ -653,9 +680,12 @@ def run_ooc(args, dist: Dist) -> None:
                 "cpu_baseline": None,
                 "e2e": {"value": value, "unit": UNIT, "ms_per_step": t * 1e3,
                         "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value),
-                        "h2d_note": "counted by the library (bmmgpu_last_copy_bytes): A once, B once per "
-                                    "resident row panel of the plan",
-                        "path": ("bmmgpu_cubic" if algo == 0 else "bmmgpu_multiply_panels") +
+                        "h2d_note": ("counted by the library (bmmgpu_last_copy_bytes): each source sub-block once per "
+                                     "sub-instance that selects it" if subinst else
+                                     "counted by the library (bmmgpu_last_copy_bytes): A once, B once per "
+                                     "resident row panel of the plan"),
+                        "path": ("bmmgpu_cubic" if algo == 0 else "bmmgpu_multiply" if subinst else
+                                 "bmmgpu_multiply_panels") +
                                 " (include/bmmgpu.h) from pinned host buffers, per rank"},
                 "spot_check": ok, "parity": parity, "clocks": clocks, "gpu_launches": int(launches * args.steps)}
         print(json.dumps(line), flush=True)

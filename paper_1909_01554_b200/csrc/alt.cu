@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdio>
 #include <cstring>
@@ -1533,6 +1534,350 @@ int dev_multiply_partial(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, 
             (st = launch_block_list(true, Q.u(), lw, dC, ldc, ls, lc, s)))
             return st;
     }
+    return kOk;
+}
+
+// ------------------------------------------------ out of core through the host levels
+// The paper's route for products beyond accelerator memory (reference
+// pipeline::coordinate, pipeline.cpp:198-369) with the generation moved onto the device:
+// the top dh levels are 7^dh sub-instances of n >> dh; for sub-instance h the source
+// sub-blocks its fused alpha.phi / beta.psi rows select are streamed from host memory one by
+// one and XOR-accumulated on the device into T_h / S_h (B's sub-blocks transposed on the
+// way), the product Q_h runs as the device-resident recursion of the remaining levels, and
+// Q_h goes home where host threads XOR it into every C sub-block its chi.gamma column
+// selects.  Against output tiles of full block products (alt_tiles.cu) this does the
+// recursion's own 7^dh products instead of 8^dh (49 against 64 at dh = 2), at the price of
+// more uploads (each source sub-block once per sub-instance that selects it) and a host
+// fold.  Per device buffers: T, S, Q twice (the next sub-instance is generated while the
+// current one multiplies), two upload slots per operand and one transpose buffer.
+namespace {
+
+struct BlockCoords {
+    uint32_t br[1 << (2 * kMaxHostLevels)], bc[1 << (2 * kMaxHostLevels)];
+    uint32_t count;
+};
+template <class Coef>
+BlockCoords block_coords(int dh, Coef coef) {
+    BlockCoords b{};
+    for (uint32_t q = 0; q < (1u << (2 * dh)); ++q) {
+        bool on = true;
+        uint32_t br = 0, bc = 0;
+        for (int l = 0; l < dh && on; ++l) {
+            const uint32_t ql = (q >> (2 * (dh - 1 - l))) & 3;
+            on = coef(l, ql);
+            br = 2 * br + (ql >> 1);
+            bc = 2 * bc + (ql & 1);
+        }
+        if (on) {
+            b.br[b.count] = br;
+            b.bc[b.count++] = bc;
+        }
+    }
+    return b;
+}
+
+// page-locked host buffers for the Q_h downloads, kept across calls (pinning GiBs costs ~0.1 s/GiB)
+constexpr int kQSlots = 4;  // downloaded Q's the host fold may lag behind by
+struct PinnedCache {
+    std::mutex mu;
+    void* p[kQSlots] = {};
+    size_t bytes = 0;
+    bool get(size_t need, void* (&out)[kQSlots]) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (bytes < need) {
+            for (auto& x : p)
+                if (x) cudaFreeHost(x), x = nullptr;
+            bytes = 0;
+            for (auto& x : p)
+                if (cudaHostAlloc(&x, need, cudaHostAllocPortable) != cudaSuccess) return false;
+            bytes = need;
+        }
+        for (int k = 0; k < kQSlots; ++k) out[k] = p[k];
+        return true;
+    }
+};
+PinnedCache g_q_pinned[32];
+
+}  // namespace
+
+// Host levels for the out-of-core sub-instance driver: the fewest (>= 1) whose per-device
+// working set -- the two generated top-level children (2 (n/2)^2/8) and ~11 sub-instance
+// arrays -- fits `budget`, with sub-instances of at least 2^13 and one level below them.
+int subinst_levels(uint64_t n, int e, uint64_t budget) {
+    for (int dh = 1; dh <= kMaxHostLevels && dh < e && (n >> dh) >= 8192; ++dh) {
+        const double ls = double(n >> dh), h = double(n / 2);
+        if (2.0 * h * h / 8.0 + 11.0 * ls * ls / 8.0 <= double(budget)) return dh;
+    }
+    return std::min(std::max(1, e - 1), kMaxHostLevels);
+}
+
+int alt_multiply_subinst(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, int dh,
+                         int kernel, int leaf_log2, uint64_t budget, double* timing_ms) {
+    const Scheme* sc = scheme_for(algo);
+    if (!sc) {
+        set_error("no bilinear scheme for this algorithm");
+        return kEinval;
+    }
+    kernel = resolve_kernel(kernel);
+    const int e = alt_levels(n, leaf_log2);
+    if (e < 2 || n < 512) {
+        set_error("out-of-core sub-instances need n >= 512 and at least two recursion levels");
+        return kEinval;
+    }
+    if (dh <= 0) dh = subinst_levels(n, e, budget);
+    dh = std::min({dh, kMaxHostLevels, e - 1});
+    while (dh > 1 && (n >> dh) < 256) --dh;  // sub-instances stay multiples of the kernel tile
+    const Masks7 ma = fused_expand(sc->alpha, sc->phi, sc->n_phi, false);
+    const Masks7 mb = fused_expand(sc->beta, sc->psi, sc->n_psi, true);
+    const Masks4 mg = fused_compress(sc);
+    const uint64_t w = n / 64, half = n / 2, hw = half / 64, ls = n >> dh, lw = ls / 64, blk = ls * lw * 8;
+    const uint64_t P = uint64_t(1) << (dh - 1);  // pieces per quadrant side (ls x ls each)
+    uint64_t subs = 1, per_top = 1;
+    for (int l = 0; l < dh; ++l) subs *= 7;
+    per_top = subs / 7;
+    const int e_sub = e - dh;
+    int dev = 0;
+    BMMGPU_CUDA_TRY(cudaGetDevice(&dev));
+    void* qh[kQSlots];
+    if (dev >= 32 || !g_q_pinned[dev].get(blk, qh)) {
+        set_error("out-of-core sub-instances: page-locked host buffers for Q");
+        return kEcuda;
+    }
+    StreamSet ss;  // 0 compute, 1 uploads, 2 generation, 3 downloads
+    if (int r = ss.acquire(4)) return r;
+    const cudaStream_t s = ss[0], h = ss[1], x = ss[2], d = ss[3];
+    struct Events {
+        cudaEvent_t e[16] = {};
+        ~Events() {
+            for (auto v : e)
+                if (v) cudaEventDestroy(v);
+        }
+    } ev;
+    for (int i = 0; i < 14; ++i) BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&ev.e[i], cudaEventDisableTiming));
+    BMMGPU_CUDA_TRY(cudaEventCreate(&ev.e[14]));
+    BMMGPU_CUDA_TRY(cudaEventCreate(&ev.e[15]));
+    cudaEvent_t* formed = ev.e + 0;    // [slot] on x: T / S of the slot's sub-instance ready
+    cudaEvent_t* consumed = ev.e + 2;  // [slot] on s: its product done (T, S read; Q written)
+    cudaEvent_t* hdown = ev.e + 4;     // [host slot] on d: Q copied home (kQSlots of them)
+    cudaEvent_t up = ev.e[8];          // on h: the upload slot filled
+    cudaEvent_t up_free = ev.e[9];     // on x: the upload slot read
+    cudaEvent_t top_free = ev.e[10];   // on x: the generated children TA / SB read for the last time
+    static_assert(kQSlots == 4, "event layout");
+    int rc;
+    // TA / SB: the top-level child h1 of A / Bt (n/2 x n/2), generated from uploaded pieces;
+    // the sub-instances of h1 gather their operands from it on the device
+    DevMem TA, SB, T[2], S[2], Q[2], st, bt;
+    StreamDrain drain{{s, h, x, d}};
+    if ((rc = TA.alloc(half * hw * 8, s)) || (rc = SB.alloc(half * hw * 8, s)) || (rc = st.alloc(blk, s)) ||
+        (rc = bt.alloc(blk, s)))
+        return rc;
+    for (int k = 0; k < 2; ++k)
+        if ((rc = T[k].alloc(blk, s)) || (rc = S[k].alloc(blk, s)) || (rc = Q[k].alloc(blk, s))) return rc;
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));  // the pool allocations, before the other streams use them
+    const uint64_t driver_bytes = 2 * half * hw * 8 + 8 * blk;
+    const int e_serial = budget > driver_bytes ? alt_serial_levels(ls, e_sub, uint64_t(0.8 * double(budget - driver_bytes)))
+                                               : std::max(0, e_sub - 1);
+    // host fold: one thread consumes the downloaded Q's in order
+    std::mutex mu;
+    std::condition_variable cv;
+    uint64_t queued = 0, folded = 0;
+    int fold_status = kOk;
+    std::vector<uint8_t> touched(size_t(1) << (2 * dh), 0);
+    std::vector<BlockCoords> lcs(static_cast<size_t>(subs));
+    const bool trace = getenv("BMMGPU_SUBINST_TRACE") != nullptr;  // dev: host-side waits on stderr
+    double fold_busy_s = 0, main_wait_s = 0;
+    const auto wall0 = std::chrono::steady_clock::now();
+    std::thread folder([&] {
+        for (uint64_t i = 0; i < subs; ++i) {
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return queued > i || fold_status != kOk; });
+                if (fold_status != kOk) return;
+            }
+            const int hslot = int(i % kQSlots);
+            if (cudaEventSynchronize(hdown[hslot]) != cudaSuccess) {
+                std::lock_guard<std::mutex> lk(mu);
+                fold_status = kEcuda;
+                cv.notify_all();
+                return;
+            }
+            const auto f0 = std::chrono::steady_clock::now();
+            const uint64_t* q = static_cast<const uint64_t*>(qh[hslot]);
+            const BlockCoords& lc = lcs[size_t(i)];
+            for (uint32_t t = 0; t < lc.count; ++t) {
+                const uint32_t id = (lc.br[t] << dh) | lc.bc[t];
+                const bool first = !touched[id];
+                touched[id] = 1;
+                uint64_t* c0 = C + uint64_t(lc.br[t]) * ls * w + uint64_t(lc.bc[t]) * lw;
+                const unsigned parts = std::max(1u, host_parallel_width());
+                const uint64_t step = (ls + parts - 1) / parts;
+                host_parallel(parts, [&](unsigned pi) {
+                    const uint64_t r0 = std::min<uint64_t>(ls, pi * step), r1 = std::min<uint64_t>(ls, r0 + step);
+                    for (uint64_t r = r0; r < r1; ++r) {
+                        uint64_t* dst = c0 + r * w;
+                        const uint64_t* src = q + r * lw;
+                        if (first)
+                            std::memcpy(dst, src, lw * 8);
+                        else
+                            for (uint64_t j = 0; j < lw; ++j) dst[j] ^= src[j];
+                    }
+                });
+            }
+            std::lock_guard<std::mutex> lk(mu);
+            fold_busy_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - f0).count();
+            ++folded;
+            cv.notify_all();
+        }
+    });
+    auto stop_folder = [&](int status) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (status != kOk && fold_status == kOk) fold_status = status;
+        }
+        cv.notify_all();
+        if (folder.joinable()) folder.join();
+    };
+    // every early return below (BMMGPU_CUDA_TRY) must still stop and join the fold thread
+    struct FolderGuard {
+        std::function<void()> f;
+        ~FolderGuard() { f(); }
+    } folder_guard{[&] { stop_folder(kEcuda); }};
+    // Order of the top-level children: consecutive children update TA / SB in place by the
+    // quadrants in which their alpha.phi (beta.psi) rows differ (XOR is its own inverse), so
+    // the order with the fewest such quadrants (the first child's full rows plus the
+    // symmetric differences) is searched over the 7! orders
+    int h1_order[7] = {0, 1, 2, 3, 4, 5, 6};
+    {
+        int perm[7] = {0, 1, 2, 3, 4, 5, 6}, best = 1 << 30;
+        do {
+            int cost = __builtin_popcount(ma.m[perm[0]]) + __builtin_popcount(mb.m[perm[0]]);
+            for (int k = 1; k < 7; ++k)
+                cost += __builtin_popcount(ma.m[perm[k]] ^ ma.m[perm[k - 1]]) +
+                        __builtin_popcount(mb.m[perm[k]] ^ mb.m[perm[k - 1]]);
+            if (cost < best) {
+                best = cost;
+                std::copy(perm, perm + 7, h1_order);
+            }
+        } while (std::next_permutation(perm, perm + 7));
+    }
+    BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[14], s));
+    uint64_t uploads = 0;
+    // one ls x ls piece from host memory into the upload slot (or straight into `direct`)
+    auto upload_piece = [&](const uint64_t* src, uint64_t* direct, uint64_t ld_direct) -> cudaError_t {
+        if (uploads++ > 0) {
+            cudaError_t e2 = cudaStreamWaitEvent(h, up_free, 0);
+            if (e2 != cudaSuccess) return e2;
+        }
+        cudaError_t e2 = memcpy2d_counted(direct ? static_cast<void*>(direct) : st.p, (direct ? ld_direct : lw) * 8,
+                                          src, w * 8, lw * 8, ls, cudaMemcpyHostToDevice, h);
+        if (e2 == cudaSuccess) e2 = cudaEventRecord(up, h);
+        if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(x, up, 0);
+        return e2;
+    };
+    rc = kOk;
+    for (uint64_t i = 0; i < subs && rc == kOk; ++i) {
+        const int slot = int(i & 1);
+        int hd[kMaxHostLevels];
+        uint64_t r = i;
+        for (int l = dh - 1; l >= 0; --l, r /= 7) hd[l] = int(r % 7);
+        hd[0] = h1_order[hd[0]];
+        const int prev_h1 = i >= per_top ? h1_order[(i / per_top) - 1] : -1;
+        lcs[size_t(i)] = block_coords(dh, [&](int l, uint32_t q) { return (mg.m[q] >> hd[l]) & 1; });
+        if (i % per_top == 0) {
+            // new top-level child h1: TA = XOR of the A quadrants alpha.phi row h1 selects, SB the
+            // same for Bt (beta.psi), generated piece by piece as the pieces land -- the first
+            // child from scratch, the next ones by XORing in the quadrants where their rows differ
+            if (i > 0) BMMGPU_CUDA_TRY(cudaStreamWaitEvent(h, top_free, 0));
+            for (int op = 0; op < 2 && rc == kOk; ++op) {
+                uint64_t* dst = op ? SB.u() : TA.u();
+                const Masks7& mm = op ? mb : ma;
+                const uint32_t mask = prev_h1 < 0 ? mm.m[hd[0]] : (mm.m[hd[0]] ^ mm.m[prev_h1]);
+                bool first = prev_h1 < 0;
+                for (uint32_t q = 0; q < 4 && rc == kOk; ++q) {
+                    if (!(mask >> q & 1)) continue;
+                    for (uint64_t pr = 0; pr < P && rc == kOk; ++pr)
+                        for (uint64_t pc = 0; pc < P && rc == kOk; ++pc) {
+                            uint64_t* piece = dst + pr * ls * hw + pc * lw;  // piece of the child
+                            const uint64_t gr = (q >> 1) * P + pr, gc = (q & 1) * P + pc;  // piece of A / Bt
+                            if (op == 0) {
+                                const uint64_t* src = A + gr * ls * w + gc * lw;
+                                BMMGPU_CUDA_TRY(upload_piece(src, first ? piece : nullptr, hw));
+                                if (!first) rc = bmmgpu_dev_fold(piece, hw, st.u(), lw, ls, lw, BMMGPU_GF2_XOR_AND, x);
+                            } else {
+                                // Bt piece (gr, gc) is B piece (gc, gr) transposed
+                                const uint64_t* src = B + gc * ls * w + gr * lw;
+                                BMMGPU_CUDA_TRY(upload_piece(src, nullptr, 0));
+                                if (first)
+                                    rc = launch_transpose_ld(st.u(), lw, ls, ls, piece, ls, lw, hw, x);
+                                else if (!(rc = launch_transpose_ld(st.u(), lw, ls, ls, bt.u(), ls, lw, lw, x)))
+                                    rc = bmmgpu_dev_fold(piece, hw, bt.u(), lw, ls, lw, BMMGPU_GF2_XOR_AND, x);
+                            }
+                            BMMGPU_CUDA_TRY(cudaEventRecord(up_free, x));
+                        }
+                    first = false;
+                }
+            }
+            if (rc) break;
+        }
+        // the sub-instance's operands from the children: levels 2 .. dh as device gathers
+        if (i >= 2) BMMGPU_CUDA_TRY(cudaStreamWaitEvent(x, consumed[slot], 0));
+        const BlockList la = block_list(dh - 1, half, hw, [&](int l, uint32_t q) { return (ma.m[hd[l + 1]] >> q) & 1; });
+        const BlockList lb = block_list(dh - 1, half, hw, [&](int l, uint32_t q) { return (mb.m[hd[l + 1]] >> q) & 1; });
+        if ((rc = launch_block_list(false, TA.u(), hw, T[slot].u(), lw, ls, la, x)) ||
+            (rc = launch_block_list(false, SB.u(), hw, S[slot].u(), lw, ls, lb, x)))
+            break;
+        BMMGPU_CUDA_TRY(cudaEventRecord(formed[slot], x));
+        if (i % per_top == per_top - 1) BMMGPU_CUDA_TRY(cudaEventRecord(top_free, x));
+        // Q_h on the compute stream (its Q slot free once the download two back is done)
+        if (i >= 2) BMMGPU_CUDA_TRY(cudaStreamWaitEvent(s, hdown[(i - 2) % kQSlots], 0));
+        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(s, formed[slot], 0));
+        if ((rc = alt_multiply_device(T[slot].u(), lw, S[slot].u(), lw, Q[slot].u(), lw, ls, algo, e_sub, e_serial,
+                                      kernel, s)))
+            break;
+        BMMGPU_CUDA_TRY(cudaEventRecord(consumed[slot], s));
+        // download into the slot's page-locked buffer once the host fold two back released it
+        {
+            const auto w0 = std::chrono::steady_clock::now();
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return folded + kQSlots > i || fold_status != kOk; });
+            main_wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+            if (fold_status != kOk) {
+                rc = fold_status;
+                break;
+            }
+        }
+        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(d, consumed[slot], 0));
+        BMMGPU_CUDA_TRY(memcpy_counted(qh[i % kQSlots], Q[slot].p, blk, cudaMemcpyDeviceToHost, d));
+        BMMGPU_CUDA_TRY(cudaEventRecord(hdown[i % kQSlots], d));
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            queued = i + 1;
+        }
+        cv.notify_all();
+    }
+    stop_folder(rc);
+    if (rc) return rc;
+    if (fold_status != kOk) {
+        set_error("out-of-core sub-instances: a download failed");
+        return fold_status;
+    }
+    BMMGPU_CUDA_TRY(cudaEventRecord(ev.e[15], s));
+    BMMGPU_CUDA_TRY(cudaStreamSynchronize(s));
+    // every C sub-block receives a contribution from some sub-instance; zero any that did not
+    for (size_t id = 0; id < touched.size(); ++id)
+        if (!touched[id]) {
+            const uint64_t br = id >> dh, bc = id & ((uint64_t(1) << dh) - 1);
+            for (uint64_t r = 0; r < ls; ++r) std::memset(C + (br * ls + r) * w + bc * lw, 0, lw * 8);
+        }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev.e[14], ev.e[15]);
+    if (trace)
+        fprintf(stderr, "subinst n=%llu dh=%d e_sub=%d e_serial=%d: wall %.3f s, device %.3f s, fold busy %.3f s, "
+                        "enqueue waited on the fold %.3f s\n",
+                (unsigned long long)n, dh, e_sub, e_serial,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count(), ms / 1e3,
+                fold_busy_s, main_wait_s);
+    if (timing_ms) *timing_ms = ms;
     return kOk;
 }
 

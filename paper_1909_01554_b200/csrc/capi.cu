@@ -42,6 +42,8 @@ int alt_multiply_multi(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64
                        const std::vector<int>& phys, int kernel, int leaf_log2, double* timing_ms);
 int host_levels_for(uint64_t n, uint32_t parts, int e);
 int alt_levels(uint64_t n, int leaf_log2);
+int alt_multiply_subinst(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo, int dh,
+                         int kernel, int leaf_log2, uint64_t budget, double* timing_ms);
 int alt_multiply_tiles(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int algo,
                        const std::vector<int>& devs, int kernel, int leaf_log2, double* timing_ms, uint64_t b,
                        uint64_t p0, uint64_t p1);
@@ -225,7 +227,7 @@ class CopyPool {
   private:
     CopyPool() {
         const unsigned hc = std::thread::hardware_concurrency();
-        const unsigned n = std::max(1u, std::min(8u, hc ? hc / 2 : 4u));
+        const unsigned n = std::max(1u, std::min(12u, hc ? hc * 3 / 4 : 4u));
         for (unsigned i = 0; i + 1 < n; ++i) workers_.emplace_back([this] { loop(); });
         for (auto& t : workers_) t.detach();
     }
@@ -252,6 +254,20 @@ class CopyPool {
     unsigned parts_ = 0, next_ = 0, pending_ = 0;
     uint64_t gen_ = 0;
 };
+
+}  // namespace
+
+// f(0) .. f(parts - 1) over the library's host helper threads (the staging copy pool).
+void host_parallel(unsigned parts, const std::function<void(unsigned)>& f) {
+    if (parts <= 1) {
+        if (parts == 1) f(0);
+        return;
+    }
+    CopyPool::get().run(parts, f);
+}
+unsigned host_parallel_width() { return CopyPool::get().width(); }
+
+namespace {
 
 // `rows` rows of `width` bytes from src (pitch spitch) to dst (pitch dpitch), split
 // across the copy pool (8 MiB per part, at most the pool's width: one memcpy thread
@@ -934,8 +950,17 @@ int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t 
         uint64_t free_b = o.device_budget ? 0 : device_free_bytes(false);
         if (!o.device_budget && need * 2 > double(free_b)) free_b = device_free_bytes(true);
         const uint64_t budget = o.device_budget ? o.device_budget : free_b;
-        if (o.force_streaming == 1 || need > double(budget))
+        if (o.force_streaming == 1 || need > double(budget)) {
+            // one device: the recursion's own top-level sub-instances, generated on the device
+            // from streamed source sub-blocks (alt.cu); several devices or BMMGPU_ALT_OOC=tiles:
+            // output tiles of block products dealt over the devices (alt_tiles.cu)
+            const char* ooc = getenv("BMMGPU_ALT_OOC");
+            const bool tiles = devs.size() > 1 || (ooc && !strcmp(ooc, "tiles"));
+            if (!tiles && alt_levels(n, o.leaf_log2) >= 2)
+                return alt_multiply_subinst(A, B, C, n, algo, plan->d_host, o.kernel, o.leaf_log2, budget,
+                                            o.timing_ms);
             return alt_multiply_tiles(A, B, C, n, algo, devs, o.kernel, o.leaf_log2, o.timing_ms, 0, 0, 0);
+        }
     }
     if (devs.size() > 1) {
         // several devices: the top host levels of the recursion are dealt across them

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <functional>
 #include <string>
 
 namespace bmmgpu {
@@ -48,6 +49,9 @@ void enable_pool_caching();
 // Free bytes on the current device for planning (capi.cu): a cached cudaMemGetInfo snapshot
 // corrected by the memory pool's reservations; refresh = a fresh (possibly blocking) query.
 uint64_t device_free_bytes(bool refresh);
+// f(0) .. f(parts - 1) over the library's host helper threads (capi.cu), and their number.
+void host_parallel(unsigned parts, const std::function<void(unsigned)>& f);
+unsigned host_parallel_width();
 
 // Non-blocking streams leased from a per-device pool: creating and destroying a
 // stream costs ~100 us of host time (measured, microbench/api_cost.py), three per call

@@ -251,14 +251,21 @@ def test_multiply_alt_hat_vectors_match_reference_digests(engine, oracle, golden
             assert oracle.popcount(ch) == c["pop"] and f"{int(ch[0]):016x}" == c["w0"]
 
 
+@pytest.mark.parametrize("driver", ["subinst", "tiles"])
 @pytest.mark.parametrize("n,tile,leaf", [(1024, 8, 6), (2048, 9, 7), (2048, 10, 8), (4096, 11, 9), (1024, 10, 7), (1024, 9, 12)])
-def test_out_of_core_tiles_equal_cubic(engine, oracle, monkeypatch, n, tile, leaf):
-    """The out-of-core fast product (alt_tiles.cu: C tiles = XOR over K of alt-basis block
-    products of tiles streamed from host memory), forced at small n with small tiles, from
-    pageable and page-locked buffers, for every scheme: the bits of the cubic product."""
+def test_out_of_core_tiles_equal_cubic(engine, oracle, monkeypatch, n, tile, leaf, driver):
+    """The out-of-core fast products, forced at small n, from pageable and page-locked
+    buffers, for every scheme: the bits of the cubic product.  subinst (the one-device
+    default, alt.cu): the recursion's top-level sub-instances generated on the device from
+    streamed source sub-blocks, Q folded into C by host threads; tiles (alt_tiles.cu): C
+    tiles = XOR over K of alt-basis block products of streamed tiles."""
     import torch
     bmm = engine
     monkeypatch.setenv("BMMGPU_ALT_TILE", str(tile))
+    if driver == "tiles":
+        monkeypatch.setenv("BMMGPU_ALT_OOC", "tiles")
+    else:
+        monkeypatch.delenv("BMMGPU_ALT_OOC", raising=False)
     a = oracle.random(n, n, 91)
     b = oracle.random(n, n, 92)
     want = oracle.multiply_cubic(a, b, n, n, n, GF2)
@@ -275,11 +282,16 @@ def test_out_of_core_tiles_equal_cubic(engine, oracle, monkeypatch, n, tile, lea
     assert np.array_equal(got.words, want)
 
 
-def test_out_of_core_tiles_by_budget(engine, oracle, monkeypatch):
+@pytest.mark.parametrize("driver", ["subinst", "tiles"])
+def test_out_of_core_tiles_by_budget(engine, oracle, monkeypatch, driver):
     """A device budget below six n^2/8 arrays selects the out-of-core driver without the
     force flag (golden n = 4096 alt-si product of the reference's seeds)."""
     bmm = engine
     monkeypatch.setenv("BMMGPU_ALT_TILE", "11")
+    if driver == "tiles":
+        monkeypatch.setenv("BMMGPU_ALT_OOC", "tiles")
+    else:
+        monkeypatch.delenv("BMMGPU_ALT_OOC", raising=False)
     n = 4096
     a = oracle.random(n, n, 1)
     b = oracle.random(n, n, 2)
@@ -334,3 +346,27 @@ def test_production_leaves_every_scheme_against_reference_digest(engine, oracle,
     for i in (0, 4097, n - 1):
         bits = np.unpackbits(a.words.reshape(n, n // 64)[i].view(np.uint8), bitorder="little")
         assert np.array_equal(got.words.reshape(n, n // 64)[i], np.bitwise_xor.reduce(B[np.flatnonzero(bits)], axis=0))
+
+
+
+@pytest.mark.parametrize("d_host", [1, 2, 3])
+def test_out_of_core_subinstances_with_host_levels(engine, oracle, d_host):
+    """The sub-instance driver with the caller's host levels (plan.d_host = 1..3: 7, 49, 343
+    sub-instances, several selecting up to 4^d_host source sub-blocks each), every scheme,
+    page-locked buffers: the bits of the cubic product."""
+    import torch
+    bmm = engine
+    n = 4096
+    depth = (n // 64).bit_length() - 1
+    a = oracle.random(n, n, 97)
+    b = oracle.random(n, n, 98)
+    want = oracle.multiply_cubic(a, b, n, n, n, GF2)
+    ha = torch.from_numpy(a.view(np.int64)).pin_memory()
+    hb = torch.from_numpy(b.view(np.int64)).pin_memory()
+    for algo in (1, 2, 3):
+        hc = torch.zeros(n * n // 64, dtype=torch.int64).pin_memory()
+        plan = bmm._Plan(d_host, depth - d_host, 0, 1, 1)
+        opts = bmm._opts(0, leaf_log2=8, force_streaming=True)
+        assert bmm.lib().bmmgpu_multiply(ha.data_ptr(), hb.data_ptr(), hc.data_ptr(), n, algo, ctypes.byref(plan), GF2,
+                                         ctypes.byref(opts)) == 0, bmm.lib().bmmgpu_last_error()
+        assert np.array_equal(hc.numpy().view(np.uint64), want), (algo, d_host)
