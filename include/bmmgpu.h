@@ -106,9 +106,13 @@ int bmmgpu_kernel64(const uint64_t* a, const uint64_t* bt, uint64_t* out, int32_
  * (plan.d_host, or an automatic choice when it is 0) are dealt across the devices,
  * one host thread each, and the partial products are XOR-folded slab by slab over
  * peer copies (bmmgpu_dev_multiply_partial).  Operands beyond the device budget (or
- * opts->force_streaming == 1) run out of core: b x b output tiles (b = 2^17, or n/2),
- * each the XOR of n/b alternative-basis block products of tiles streamed from host
- * memory, row panels of tiles dealt over the devices. */
+ * opts->force_streaming == 1) run out of core.  On one device: the recursion's top
+ * plan.d_host levels (0: the fewest that fit the budget) as 7^d_host sub-instances whose
+ * operands are generated on the device from pieces of A and B streamed from host memory,
+ * each product's Q folded into C by host threads (C must be writable host memory).  On
+ * several devices (or with the environment BMMGPU_ALT_OOC=tiles): b x b output tiles
+ * (b = 2^17, or n/2), each the XOR of n/b alternative-basis block products of tiles
+ * streamed from host memory, row panels of tiles dealt over the devices. */
 int bmmgpu_multiply(const uint64_t* A, const uint64_t* B, uint64_t* C, uint64_t n, int32_t algo,
                     const bmmgpu_plan* plan, int32_t semiring, const bmmgpu_opts* opts);
 
