@@ -1579,6 +1579,7 @@ BlockCoords block_coords(int dh, Coef coef) {
 // page-locked host buffers for the Q_h downloads, kept across calls (pinning GiBs costs ~0.1 s/GiB)
 constexpr int kQSlots = 4;  // downloaded Q's the host fold may lag behind by
 struct PinnedCache {
+    std::mutex call_mu;  // one out-of-core sub-instance call per device at a time (they share these)
     std::mutex mu;
     void* p[kQSlots] = {};
     size_t bytes = 0;
@@ -1639,7 +1640,12 @@ int alt_multiply_subinst(const uint64_t* A, const uint64_t* B, uint64_t* C, uint
     int dev = 0;
     BMMGPU_CUDA_TRY(cudaGetDevice(&dev));
     void* qh[kQSlots];
-    if (dev >= 32 || !g_q_pinned[dev].get(blk, qh)) {
+    if (dev >= 32) {
+        set_error("out-of-core sub-instances: device index");
+        return kEinval;
+    }
+    std::lock_guard<std::mutex> one_call(g_q_pinned[dev].call_mu);
+    if (!g_q_pinned[dev].get(blk, qh)) {
         set_error("out-of-core sub-instances: page-locked host buffers for Q");
         return kEcuda;
     }
