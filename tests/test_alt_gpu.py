@@ -370,3 +370,23 @@ def test_out_of_core_subinstances_with_host_levels(engine, oracle, d_host):
         assert bmm.lib().bmmgpu_multiply(ha.data_ptr(), hb.data_ptr(), hc.data_ptr(), n, algo, ctypes.byref(plan), GF2,
                                          ctypes.byref(opts)) == 0, bmm.lib().bmmgpu_last_error()
         assert np.array_equal(hc.numpy().view(np.uint64), want), (algo, d_host)
+
+
+def test_out_of_core_subinstances_staged_pieces_match_in_core(engine, oracle):
+    """n = 32768 out of core through the sub-instance driver from pageable buffers, where every
+    piece (16384 x 16384 bits, 32 MiB) goes through the page-locked staging slots: equal to the
+    in-core fast product of the same operands and to numpy rows of A.B."""
+    bmm = engine
+    n = 32768
+    a = oracle.random(n, n, 121)
+    b = oracle.random(n, n, 122)
+    plan = bmm.LayerPlan.auto_plan(n, 1)
+    want = bmm.multiply(bmm.BitMatrix(n, n, a), bmm.BitMatrix(n, n, b), bmm.Algo.AltSelfInverse, plan,
+                        bmm.Semiring.Gf2XorAnd)
+    got = bmm.multiply(bmm.BitMatrix(n, n, a), bmm.BitMatrix(n, n, b), bmm.Algo.AltSelfInverse, plan,
+                       bmm.Semiring.Gf2XorAnd, force_streaming=True)
+    assert np.array_equal(got.words, want.words)
+    B = b.reshape(n, n // 64)
+    for i in (0, 12345, n - 1):
+        bits = np.unpackbits(a.reshape(n, n // 64)[i].view(np.uint8), bitorder="little")
+        assert np.array_equal(got.words.reshape(n, n // 64)[i], np.bitwise_xor.reduce(B[np.flatnonzero(bits)], axis=0))
