@@ -1691,6 +1691,18 @@ int alt_multiply_subinst(const uint64_t* A, const uint64_t* B, uint64_t* C, uint
     std::vector<uint8_t> touched(size_t(1) << (2 * dh), 0);
     std::vector<BlockCoords> lcs(static_cast<size_t>(subs));
     const bool trace = getenv("BMMGPU_SUBINST_TRACE") != nullptr;  // dev: host-side waits on stderr
+    // dev trace: compute start / end of every sub-instance on s (timing events)
+    std::vector<cudaEvent_t> tr_ev;
+    struct TrEv {
+        std::vector<cudaEvent_t>& v;
+        ~TrEv() {
+            for (auto e2 : v) cudaEventDestroy(e2);
+        }
+    } tr_guard{tr_ev};
+    if (trace) {
+        tr_ev.resize(size_t(2 * subs));
+        for (auto& e2 : tr_ev) BMMGPU_CUDA_TRY(cudaEventCreate(&e2));
+    }
     double fold_busy_s = 0, main_wait_s = 0;
     const auto wall0 = std::chrono::steady_clock::now();
     std::thread folder([&] {
@@ -1837,9 +1849,11 @@ int alt_multiply_subinst(const uint64_t* A, const uint64_t* B, uint64_t* C, uint
         // Q_h on the compute stream (its Q slot free once the download two back is done)
         if (i >= 2) BMMGPU_CUDA_TRY(cudaStreamWaitEvent(s, hdown[(i - 2) % kQSlots], 0));
         BMMGPU_CUDA_TRY(cudaStreamWaitEvent(s, formed[slot], 0));
+        if (trace) BMMGPU_CUDA_TRY(cudaEventRecord(tr_ev[2 * i], s));
         if ((rc = alt_multiply_device(T[slot].u(), lw, S[slot].u(), lw, Q[slot].u(), lw, ls, algo, e_sub, e_serial,
                                       kernel, s)))
             break;
+        if (trace) BMMGPU_CUDA_TRY(cudaEventRecord(tr_ev[2 * i + 1], s));
         BMMGPU_CUDA_TRY(cudaEventRecord(consumed[slot], s));
         // download into the slot's page-locked buffer once the host fold two back released it
         {
@@ -1877,6 +1891,20 @@ int alt_multiply_subinst(const uint64_t* A, const uint64_t* B, uint64_t* C, uint
         }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev.e[14], ev.e[15]);
+    if (trace) {
+        double busy = 0, gap_top = 0, gap_other = 0;
+        float prev_end = 0.f;
+        for (uint64_t i = 0; i < subs; ++i) {
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, ev.e[14], tr_ev[2 * i]);
+            cudaEventElapsedTime(&b, ev.e[14], tr_ev[2 * i + 1]);
+            busy += (b - a) / 1e3;
+            (i % per_top == 0 ? gap_top : gap_other) += (a - prev_end) / 1e3;
+            prev_end = b;
+        }
+        fprintf(stderr, "subinst compute %.3f s, waits before top-level children %.3f s, other waits %.3f s, tail %.3f s\n",
+                busy, gap_top, gap_other, ms / 1e3 - prev_end / 1e3);
+    }
     if (trace)
         fprintf(stderr, "subinst n=%llu dh=%d e_sub=%d e_serial=%d: wall %.3f s, device %.3f s, fold busy %.3f s, "
                         "enqueue waited on the fold %.3f s\n",
