@@ -54,6 +54,7 @@ int launch_cubic(int kernel, const uint64_t* dA, uint64_t lda, const uint64_t* d
                  cudaStream_t stream, uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch);
 int granularity(int kernel, uint64_t* gm, uint64_t* gn, uint64_t* gk);
 int resolve_kernel(int kernel);
+void set_umma_pair_reserve(int pairs);
 
 namespace {
 
@@ -235,6 +236,13 @@ __global__ void __launch_bounds__(256, BMMGPU_COMPRESS_MINB) compress_pass_kerne
     }
 }
 
+#ifndef BMMGPU_ALT_OVERLAP
+#define BMMGPU_ALT_OVERLAP 1  // CTA pairs the overlapped leaf groups leave to their passes (0: off)
+#endif
+#ifndef BMMGPU_ALT_OVERLAP_MIN
+#define BMMGPU_ALT_OVERLAP_MIN 343  // fewest leaves per group (smaller groups: end to end lost ~1 %, profiles/r02/experiment_overlap_groups.txt)
+#endif
+
 unsigned grid_for(uint64_t total) {
     const uint64_t blocks = ceil_div(total, 256);
     return unsigned(std::min<uint64_t>(blocks, 148ull * 64));
@@ -400,10 +408,24 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
     const std::vector<int> lv = pass_levels(e);
     const std::vector<int> lv_expand = fold ? pass_levels(e - 1) : lv;
 
+    // Overlapped leaf groups (default for e >= 3): the last expand pass (level lg -> e) and
+    // the first compress pass (e -> lg) run per group of 1/7 of the level-lg parents on a
+    // second stream, next to the leaf launches of the neighbouring groups, which leave
+    // BMMGPU_ALT_OVERLAP CTA pairs (2 SMs each) idle for them; the leaf launches go on a
+    // high-priority stream so their CTAs take SMs ahead of pending pass blocks.  Level e
+    // is never whole in HBM: two group slots of T / S / Q (2/7 of the arrays).
+    const int lg = lv[lv.size() - 2];  // last materialised level above the leaves
+    const char* ov_env = getenv("BMMGPU_ALT_OVERLAP");
+    const int ov_pairs = ov_env ? atoi(ov_env) : BMMGPU_ALT_OVERLAP;
+    const char* ov_min_env = getenv("BMMGPU_ALT_OVERLAP_MIN");  // dev: fewest leaves per group
+    const uint64_t ov_min = ov_min_env ? strtoull(ov_min_env, nullptr, 10) : BMMGPU_ALT_OVERLAP_MIN;
+    const bool grouped = !fold && lg >= 1 && ov_pairs > 0 && pow7(e - 1) >= ov_min;
+    const size_t n_pre = grouped ? lv.size() - 2 : lv_expand.size() - 1;  // whole-array expand passes
+
     // Expand, one or two levels per pass, freeing each parent level once consumed.
     const uint64_t* tin = dA;
     const uint64_t* sin = dBt;
-    for (size_t i = 0; i + 1 < lv_expand.size(); ++i) {
+    for (size_t i = 0; i < n_pre; ++i) {
         const std::vector<int>& lv = lv_expand;
         const int l0 = lv[i], l1 = lv[i + 1];
         const uint64_t Pn = pow7(l1);
@@ -425,6 +447,120 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
         }
         tin = T[l1].u();
         sin = S[l1].u();
+    }
+
+    if (grouped) {
+        const int D = e - lg;
+        const uint64_t Pg = pow7(lg) / 7, per = Pg * pow7(D);  // parents / leaves per group
+        const uint64_t Lg = n >> lg, q_bs = t_rows * cwl;
+        const uint64_t out_ld = Lg / 64, out_bs = Lg * (Lg / 64);
+        DevMem N, Tg[2], Sg[2], Qg[2];  // level-lg products; two group slots
+        if ((st = N.alloc(size_t(pow7(lg) * out_bs * 8), s))) return st;
+        for (int k = 0; k < 2; ++k) {
+            if ((st = Tg[k].alloc(size_t(per * t_bs[e] * 8), s)) || (st = Sg[k].alloc(size_t(per * s_bs[e] * 8), s)) ||
+                (st = Qg[k].alloc(size_t(per * q_bs * 8), s)))
+                return st;
+            if (t_rows != L || s_rows != L || kwl != L / 64) {  // pads stay zero: the passes write interiors
+                BMMGPU_CUDA_TRY(cudaMemsetAsync(Tg[k].p, 0, size_t(per * t_bs[e] * 8), s));
+                BMMGPU_CUDA_TRY(cudaMemsetAsync(Sg[k].p, 0, size_t(per * s_bs[e] * 8), s));
+                count_launch(2);
+            }
+        }
+        StreamSet hi, lo;
+        const char* prio_env = getenv("BMMGPU_ALT_OVERLAP_PRIO");  // dev: 0 = leaves at default priority
+        if ((st = hi.acquire(1, prio_env && *prio_env == '0' ? 0 : 1)) || (st = lo.acquire(1, 0))) return st;
+        const cudaStream_t ks = hi[0], ps = lo[0];
+        struct Events {
+            cudaEvent_t e[16] = {};
+            ~Events() {
+                for (auto v : e)
+                    if (v) cudaEventDestroy(v);
+            }
+        } ev;
+        for (auto& v : ev.e) BMMGPU_CUDA_TRY(cudaEventCreateWithFlags(&v, cudaEventDisableTiming));
+        cudaEvent_t* expanded = ev.e;     // [g] on ps: group g's T / S written
+        cudaEvent_t* leaves = ev.e + 7;   // [g] on ks: group g's Q written (T / S slot free)
+        cudaEvent_t start = ev.e[14], done = ev.e[15];
+        // error returns: both streams idle before the buffers' frees (a normal return stays
+        // asynchronous: s waits for `done`, and the frees are ordered on s)
+        struct DrainOnError {
+            cudaStream_t a, b;
+            bool ok = false;
+            ~DrainOnError() {
+                if (!ok) {
+                    cudaStreamSynchronize(a);
+                    cudaStreamSynchronize(b);
+                }
+            }
+        } drain{ks, ps};
+        struct Reserve {
+            explicit Reserve(int p) { set_umma_pair_reserve(p); }
+            ~Reserve() { set_umma_pair_reserve(0); }
+        };
+        BMMGPU_CUDA_TRY(cudaEventRecord(start, s));
+        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(ks, start, 0));
+        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(ps, start, 0));
+        auto expand_group = [&](int g) -> int {
+            const int k = g & 1;
+            int r = launch_expand(D, tin + g * Pg * t_bs[lg], t_ld[lg], t_bs[lg], Pg, Lg, Tg[k].u(), t_ld[e], t_bs[e],
+                                  ma, ps);
+            if (!r)
+                r = launch_expand(D, sin + g * Pg * s_bs[lg], s_ld[lg], s_bs[lg], Pg, Lg, Sg[k].u(), s_ld[e], s_bs[e],
+                                  mb, ps);
+            if (!r && cudaEventRecord(expanded[g], ps) != cudaSuccess) r = kEcuda;
+            return r;
+        };
+        if ((st = expand_group(0)) || (st = expand_group(1))) return st;
+        {
+            Reserve reserve(ov_pairs);
+            for (int g = 0; g < 7; ++g) {
+                const int k = g & 1;
+                BMMGPU_CUDA_TRY(cudaStreamWaitEvent(ks, expanded[g], 0));
+                for (uint64_t b0 = 0; b0 < per; b0 += 65535) {
+                    const uint64_t nb = std::min<uint64_t>(65535, per - b0);
+                    if ((st = launch_cubic(kernel, Tg[k].u() + b0 * t_bs[e], kwl, Sg[k].u() + b0 * s_bs[e], kwl,
+                                           Qg[k].u() + b0 * q_bs, cwl, t_rows, s_rows, kwl, true, false, ks, nb,
+                                           t_bs[e], s_bs[e], q_bs)))
+                        return st;
+                }
+                BMMGPU_CUDA_TRY(cudaEventRecord(leaves[g], ks));
+                BMMGPU_CUDA_TRY(cudaStreamWaitEvent(ps, leaves[g], 0));
+                if ((st = launch_compress(D, Qg[k].u(), cwl, q_bs, Pg, Lg, N.u() + g * Pg * out_bs, out_ld, out_bs, mg,
+                                          ps)))
+                    return st;
+                // slot k's T / S were read by leaves g (ps waited for it); its Q by the compress above
+                if (g + 2 < 7 && (st = expand_group(g + 2))) return st;
+            }
+        }
+        BMMGPU_CUDA_TRY(cudaEventRecord(done, ps));
+        BMMGPU_CUDA_TRY(cudaStreamWaitEvent(s, done, 0));
+        drain.ok = true;
+        T[lg].release();
+        S[lg].release();
+        // the remaining compress passes, level lg up to dC, on s
+        DevMem cur = std::move(N), nxt;
+        uint64_t cur_ld = out_ld, cur_bs = out_bs;
+        for (size_t i = lv.size() - 2; i > 0; --i) {
+            const int l1 = lv[i], l0 = lv[i - 1];
+            const uint64_t Ll = n >> l0, Pp = pow7(l0);
+            uint64_t* out;
+            uint64_t o_ld, o_bs;
+            if (l0 == 0) {
+                out = dC;
+                o_ld = ldc;
+                o_bs = 0;
+            } else {
+                o_ld = Ll / 64;
+                o_bs = Ll * (Ll / 64);
+                if ((st = nxt.alloc(size_t(Pp * o_bs * 8), s))) return st;
+                out = nxt.u();
+            }
+            if ((st = launch_compress(l1 - l0, cur.u(), cur_ld, cur_bs, Pp, Ll, out, o_ld, o_bs, mg, s))) return st;
+            cur = std::move(nxt);
+            cur_ld = o_ld;
+            cur_bs = o_bs;
+        }
+        return kOk;
     }
 
     // Leaves: 7^e batched block products, Q row-major (t_rows x cwl words each).

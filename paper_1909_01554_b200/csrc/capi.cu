@@ -126,25 +126,29 @@ uint64_t device_free_bytes(bool refresh) {
 
 namespace {
 std::mutex g_stream_mu;
-std::vector<cudaStream_t> g_stream_pool[32];  // idle leased-out-and-returned streams per device
+std::vector<cudaStream_t> g_stream_pool[32][3];  // idle leased-and-returned streams per device and priority
 }  // namespace
 
-int StreamSet::acquire(int count) {
+int StreamSet::acquire(int count, int priority) {
     if (cudaGetDevice(&device) != cudaSuccess || device < 0 || device >= 32) return kEcuda;
     n = 0;
+    prio = priority > 0 ? 1 : priority < 0 ? 2 : 0;
     {
         std::lock_guard<std::mutex> lock(g_stream_mu);
-        auto& pool = g_stream_pool[device];
+        auto& pool = g_stream_pool[device][prio];
         while (n < count && !pool.empty()) {
             s[n++] = pool.back();
             pool.pop_back();
         }
     }
+    int least = 0, greatest = 0;
+    if (n < count && prio) cudaDeviceGetStreamPriorityRange(&least, &greatest);
     for (; n < count; ++n) {
-        const cudaError_t e = cudaStreamCreateWithFlags(&s[n], cudaStreamNonBlocking);
+        const cudaError_t e = cudaStreamCreateWithPriority(&s[n], cudaStreamNonBlocking,
+                                                           prio == 1 ? greatest : prio == 2 ? least : 0);
         if (e != cudaSuccess) {
             s[n] = nullptr;
-            set_error(std::string("cudaStreamCreateWithFlags: ") + cudaGetErrorString(e));
+            set_error(std::string("cudaStreamCreateWithPriority: ") + cudaGetErrorString(e));
             return kEcuda;
         }
     }
@@ -155,7 +159,7 @@ StreamSet::~StreamSet() {
     if (n == 0) return;
     std::lock_guard<std::mutex> lock(g_stream_mu);
     for (int i = 0; i < n; ++i)
-        if (s[i]) g_stream_pool[device].push_back(s[i]);
+        if (s[i]) g_stream_pool[device][prio].push_back(s[i]);
 }
 
 void count_launch(uint64_t n) { cur_stats().launches.fetch_add(n, std::memory_order_relaxed); }

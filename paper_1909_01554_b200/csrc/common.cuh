@@ -59,12 +59,14 @@ unsigned host_parallel_width();
 // streams; a lease goes back to the pool when the set is destroyed -- declare it
 // before the driver's buffers and StreamDrain, so the streams are idle by then.
 struct StreamSet {
-    int device = -1, n = 0;
+    int device = -1, n = 0, prio = 0;
     cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};
     StreamSet() = default;
     StreamSet(const StreamSet&) = delete;
     StreamSet& operator=(const StreamSet&) = delete;
-    int acquire(int count);  // on the current device; 0 or a CUDA status
+    // on the current device; 0 or a CUDA status.  priority: 0 default, 1 the device's
+    // greatest (its pending blocks are scheduled first), -1 its least
+    int acquire(int count, int priority = 0);
     ~StreamSet();
     cudaStream_t operator[](int i) const { return s[i]; }
 };

@@ -968,6 +968,11 @@ void umma_granularity(uint64_t* gm, uint64_t* gn, uint64_t* gk_bits) {
     *gk_bits = P_KBITS;
 }
 
+// CTA pairs this host thread's K2 launches leave idle (alt.cu's overlapped leaf groups run
+// their expand / compress passes on the freed SMs next to the leaves).
+thread_local int t_umma_pair_reserve = 0;
+void set_umma_pair_reserve(int pairs) { t_umma_pair_reserve = pairs < 0 ? 0 : pairs; }
+
 int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t ldbt, uint64_t* dC, uint64_t ldc,
                       uint64_t m_pad, uint64_t n_pad, uint64_t kw, bool gf2, bool accumulate, cudaStream_t stream,
                       uint64_t batch, uint64_t sA_batch, uint64_t sB_batch, uint64_t sC_batch) {
@@ -998,7 +1003,7 @@ int launch_cubic_umma(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uin
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t max_pairs = std::min<uint64_t>(P_MAX_PAIRS, std::max(1, sms / 2));
+    const uint64_t max_pairs = std::min<uint64_t>(P_MAX_PAIRS, std::max(1, sms / 2 - t_umma_pair_reserve));
     const uint64_t pairs = std::min<uint64_t>(total, max_pairs);
     TileMap map{uint32_t(m_tiles), uint32_t(n_tiles), uint32_t(per_prod), sA_batch, sB_batch, sC_batch};
     // TMA loads when the operands can be described by tensor maps (BMMGPU_UMMA_LOADER=cpasync
