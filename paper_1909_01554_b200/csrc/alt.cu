@@ -239,6 +239,9 @@ __global__ void __launch_bounds__(256, BMMGPU_COMPRESS_MINB) compress_pass_kerne
 #ifndef BMMGPU_ALT_OVERLAP
 #define BMMGPU_ALT_OVERLAP 1  // CTA pairs the overlapped leaf groups leave to their passes (0: off)
 #endif
+#ifndef BMMGPU_ALT_OVERLAP_ORDER
+#define BMMGPU_ALT_OVERLAP_ORDER 0  // pass stream order per group (alt_breadth)
+#endif
 #ifndef BMMGPU_ALT_OVERLAP_MIN
 #define BMMGPU_ALT_OVERLAP_MIN 343  // fewest leaves per group (smaller groups: end to end lost ~1 %, profiles/r02/experiment_overlap_groups.txt)
 #endif
@@ -454,11 +457,17 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
         const uint64_t Pg = pow7(lg) / 7, per = Pg * pow7(D);  // parents / leaves per group
         const uint64_t Lg = n >> lg, q_bs = t_rows * cwl;
         const uint64_t out_ld = Lg / 64, out_bs = Lg * (Lg / 64);
-        DevMem N, Tg[2], Sg[2], Qg[2];  // level-lg products; two group slots
+        // order 0: the pass stream compresses group g, then expands g + 2 (Q in two slots);
+        // order 1: expands g + 2 first, then compresses g (Q in three slots)
+        const char* ord_env = getenv("BMMGPU_ALT_OVERLAP_ORDER");
+        const int order = ord_env ? atoi(ord_env) : BMMGPU_ALT_OVERLAP_ORDER;
+        const int q_slots = order == 1 ? 3 : 2;
+        DevMem N, Tg[2], Sg[2], Qg[3];  // level-lg products; group slots
         if ((st = N.alloc(size_t(pow7(lg) * out_bs * 8), s))) return st;
+        for (int k = 0; k < q_slots; ++k)
+            if ((st = Qg[k].alloc(size_t(per * q_bs * 8), s))) return st;
         for (int k = 0; k < 2; ++k) {
-            if ((st = Tg[k].alloc(size_t(per * t_bs[e] * 8), s)) || (st = Sg[k].alloc(size_t(per * s_bs[e] * 8), s)) ||
-                (st = Qg[k].alloc(size_t(per * q_bs * 8), s)))
+            if ((st = Tg[k].alloc(size_t(per * t_bs[e] * 8), s)) || (st = Sg[k].alloc(size_t(per * s_bs[e] * 8), s)))
                 return st;
             if (t_rows != L || s_rows != L || kwl != L / 64) {  // pads stay zero: the passes write interiors
                 BMMGPU_CUDA_TRY(cudaMemsetAsync(Tg[k].p, 0, size_t(per * t_bs[e] * 8), s));
@@ -471,7 +480,7 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
         if ((st = hi.acquire(1, prio_env && *prio_env == '0' ? 0 : 1)) || (st = lo.acquire(1, 0))) return st;
         const cudaStream_t ks = hi[0], ps = lo[0];
         struct Events {
-            cudaEvent_t e[16] = {};
+            cudaEvent_t e[23] = {};
             ~Events() {
                 for (auto v : e)
                     if (v) cudaEventDestroy(v);
@@ -481,6 +490,7 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
         cudaEvent_t* expanded = ev.e;     // [g] on ps: group g's T / S written
         cudaEvent_t* leaves = ev.e + 7;   // [g] on ks: group g's Q written (T / S slot free)
         cudaEvent_t start = ev.e[14], done = ev.e[15];
+        cudaEvent_t* compressed = ev.e + 16;  // [g] on ps: group g's Q slot read
         // error returns: both streams idle before the buffers' frees (a normal return stays
         // asynchronous: s waits for `done`, and the frees are ordered on s)
         struct DrainOnError {
@@ -510,31 +520,80 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
             if (!r && cudaEventRecord(expanded[g], ps) != cudaSuccess) r = kEcuda;
             return r;
         };
-        if ((st = expand_group(0)) || (st = expand_group(1))) return st;
+        // dev trace (BMMGPU_GROUP_TRACE): per group, when its expand / leaves / compress end
+        const bool gtrace = getenv("BMMGPU_GROUP_TRACE") != nullptr;
+        struct TraceEv {
+            std::vector<cudaEvent_t> v;
+            ~TraceEv() {
+                for (auto x : v) cudaEventDestroy(x);
+            }
+        } tev;
+        auto mark = [&](cudaStream_t on) {
+            if (!gtrace) return;
+            cudaEvent_t x;
+            if (cudaEventCreate(&x) == cudaSuccess) {
+                cudaEventRecord(x, on);
+                tev.v.push_back(x);
+            }
+        };
+        std::vector<char> tag;
+        auto tmark = [&](char c, cudaStream_t on) {
+            if (gtrace) tag.push_back(c);
+            mark(on);
+        };
+        tmark('s', ps);
+        if ((st = expand_group(0))) return st;
+        tmark('x', ps);
+        if ((st = expand_group(1))) return st;
+        tmark('x', ps);
         {
             Reserve reserve(ov_pairs);
             for (int g = 0; g < 7; ++g) {
-                const int k = g & 1;
+                const int k = g & 1, kq = g % q_slots;
                 BMMGPU_CUDA_TRY(cudaStreamWaitEvent(ks, expanded[g], 0));
+                if (g >= q_slots) BMMGPU_CUDA_TRY(cudaStreamWaitEvent(ks, compressed[g - q_slots], 0));
+                tmark('k', ks);
                 for (uint64_t b0 = 0; b0 < per; b0 += 65535) {
                     const uint64_t nb = std::min<uint64_t>(65535, per - b0);
                     if ((st = launch_cubic(kernel, Tg[k].u() + b0 * t_bs[e], kwl, Sg[k].u() + b0 * s_bs[e], kwl,
-                                           Qg[k].u() + b0 * q_bs, cwl, t_rows, s_rows, kwl, true, false, ks, nb,
+                                           Qg[kq].u() + b0 * q_bs, cwl, t_rows, s_rows, kwl, true, false, ks, nb,
                                            t_bs[e], s_bs[e], q_bs)))
                         return st;
                 }
+                tmark('K', ks);
                 BMMGPU_CUDA_TRY(cudaEventRecord(leaves[g], ks));
                 BMMGPU_CUDA_TRY(cudaStreamWaitEvent(ps, leaves[g], 0));
-                if ((st = launch_compress(D, Qg[k].u(), cwl, q_bs, Pg, Lg, N.u() + g * Pg * out_bs, out_ld, out_bs, mg,
-                                          ps)))
+                // T / S slot k is free once leaves g are done (ps waited for it)
+                if (order == 1 && g + 2 < 7) {
+                    if ((st = expand_group(g + 2))) return st;
+                    tmark('x', ps);
+                }
+                tmark('c', ps);
+                if ((st = launch_compress(D, Qg[kq].u(), cwl, q_bs, Pg, Lg, N.u() + g * Pg * out_bs, out_ld, out_bs,
+                                          mg, ps)))
                     return st;
-                // slot k's T / S were read by leaves g (ps waited for it); its Q by the compress above
-                if (g + 2 < 7 && (st = expand_group(g + 2))) return st;
+                BMMGPU_CUDA_TRY(cudaEventRecord(compressed[g], ps));
+                tmark('C', ps);
+                if (order != 1 && g + 2 < 7) {
+                    if ((st = expand_group(g + 2))) return st;
+                    tmark('x', ps);
+                }
             }
         }
         BMMGPU_CUDA_TRY(cudaEventRecord(done, ps));
         BMMGPU_CUDA_TRY(cudaStreamWaitEvent(s, done, 0));
         drain.ok = true;
+        if (gtrace && !tev.v.empty()) {
+            // s = start, x = an expand ended, k / K = leaves began / ended, c / C = compress began / ended (ms)
+            cudaEventSynchronize(tev.v.back());
+            fprintf(stderr, "groups n=%llu e=%d lg=%d:", (unsigned long long)n, e, lg);
+            for (size_t i = 0; i < tev.v.size(); ++i) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, tev.v[0], tev.v[i]);
+                fprintf(stderr, " %c%.2f", tag[i], ms);
+            }
+            fprintf(stderr, "\n");
+        }
         T[lg].release();
         S[lg].release();
         // the remaining compress passes, level lg up to dC, on s
