@@ -390,3 +390,30 @@ def test_out_of_core_subinstances_staged_pieces_match_in_core(engine, oracle):
     for i in (0, 12345, n - 1):
         bits = np.unpackbits(a.reshape(n, n // 64)[i].view(np.uint8), bitorder="little")
         assert np.array_equal(got.words.reshape(n, n // 64)[i], np.bitwise_xor.reduce(B[np.flatnonzero(bits)], axis=0))
+
+
+@pytest.mark.parametrize("leaf", [7, 8, 9, 10])
+@pytest.mark.parametrize("setting", [
+    {"BMMGPU_ALT_NO_STREAM": "1", "BMMGPU_ALT_OVERLAP": "0"},
+    {"BMMGPU_ALT_NO_STREAM": "1", "BMMGPU_ALT_OVERLAP": "1"},
+    {"BMMGPU_ALT_NO_STREAM": "1", "BMMGPU_ALT_OVERLAP": "1", "BMMGPU_ALT_OVERLAP_ORDER": "1"},
+    {"BMMGPU_ALT_NO_STREAM": "1", "BMMGPU_ALT_OVERLAP": "3", "BMMGPU_ALT_OVERLAP_MIN": "1"},
+    {"BMMGPU_ALT_OVERLAP": "1", "BMMGPU_ALT_OVERLAP_MIN": "1"},  # streamed host path, grouped children
+])
+def test_overlapped_leaf_groups_match_reference(engine, oracle, golden, monkeypatch, leaf, setting):
+    """The overlapped leaf groups (alt.cu alt_breadth: the last expand / first compress pass
+    per group of leaves on a second stream beside the leaf launches, some CTA pairs left
+    idle) against the plain breadth-first order: n = 8192 with leaves 2^7..2^10 (e = 6, 5,
+    4, 3 levels: two-level and single-level passes above the groups, padded leaf panels at
+    2^7) must reproduce the reference's own n = 8192 GF(2) digest for every scheme, in both
+    pass orders, with groups as small as 49 leaves, in core and inside the streamed host
+    path's children."""
+    for k, v in setting.items():
+        monkeypatch.setenv(k, v)
+    bmm = engine
+    cub = next(x for x in golden["cubic_large"] if x["m"] == 8192 and x["ring"] == GF2)
+    a = bmm.BitMatrix(8192, 8192, oracle.random(8192, 8192, cub["a_seed"]))
+    b = bmm.BitMatrix(8192, 8192, oracle.random(8192, 8192, cub["b_seed"]))
+    for algo in (bmm.Algo.StrassenWinograd, bmm.Algo.AltSelfInverse, bmm.Algo.AltChaining):
+        got = bmm.multiply(a, b, algo, bmm.LayerPlan.auto_plan(8192, 1), bmm.Semiring.Gf2XorAnd, leaf_log2=leaf)
+        assert f"{oracle.fnv1a64(got.words):016x}" == cub["fnv"], (algo, leaf, setting)

@@ -26,5 +26,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:cubi
     python bench.py --workload c2-gf2-altsi-65536 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-check > $O/full_c2.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:expand_pass -s 2 -c 1 -o $O/full_expand_c2 \
     python bench.py --workload c2-gf2-altsi-65536 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-check > $O/full_expand.log 2>&1
+[ -x microbench/pipeline_bench ] || g++ -std=c++20 -O2 -I include microbench/pipeline_bench.cpp -o microbench/pipeline_bench -L paper_1909_01554_b200 -lbmm_b200 -lbmmgpu -Wl,-rpath,'$ORIGIN/../paper_1909_01554_b200' -lpthread
 timeout 600 microbench/pipeline_bench 65536 2 2 > $O/pipeline.log 2>&1
 tail -n 2 $O/*.log
