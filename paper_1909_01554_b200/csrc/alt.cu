@@ -411,9 +411,10 @@ int alt_breadth(const uint64_t* dA, uint64_t lda, const uint64_t* dBt, uint64_t 
     const std::vector<int> lv = pass_levels(e);
     const std::vector<int> lv_expand = fold ? pass_levels(e - 1) : lv;
 
-    // Overlapped leaf groups (default for e >= 3): the last expand pass (level lg -> e) and
-    // the first compress pass (e -> lg) run per group of 1/7 of the level-lg parents on a
-    // second stream, next to the leaf launches of the neighbouring groups, which leave
+    // Overlapped leaf groups (default when a group holds >= 343 leaves, i.e. e >= 4): the
+    // last expand pass (level lg -> e) and the first compress pass (e -> lg) run per group of
+    // 1/7 of the level-lg parents on a second stream, next to the leaf launches of the
+    // neighbouring groups (in practice the compresses: profiles/r02/experiment_overlap_*), which leave
     // BMMGPU_ALT_OVERLAP CTA pairs (2 SMs each) idle for them; the leaf launches go on a
     // high-priority stream so their CTAs take SMs ahead of pending pass blocks.  Level e
     // is never whole in HBM: two group slots of T / S / Q (2/7 of the arrays).
