@@ -107,8 +107,11 @@ struct PassGeom {
 // q_1 .. q_D of prod_i M[h_i][q_i] times the sub-block (q_1 .. q_D) of the parent
 // (reference yates::mode_step with the alpha / beta programs, yates.cpp:112-141,
 // engine.cpp:284-285, applied D times).
+#ifndef BMMGPU_EXPAND_MINB
+#define BMMGPU_EXPAND_MINB 2  // resident CTAs per SM the expand pass is compiled for (1 at 140 registers)
+#endif
 template <int D, int V>
-__global__ void __launch_bounds__(256) expand_pass_kernel(const uint64_t* __restrict__ in, uint64_t ld_in,
+__global__ void __launch_bounds__(256, BMMGPU_EXPAND_MINB) expand_pass_kernel(const uint64_t* __restrict__ in, uint64_t ld_in,
                                                           uint64_t bs_in, uint64_t total, PassGeom g,
                                                           uint64_t* __restrict__ out, uint64_t ld_out,
                                                           uint64_t bs_out, Masks7 m) {
