@@ -111,12 +111,15 @@ def alt_case(i: int) -> dict | None:
     ds = min(ds, depth - dh)
     plan = bmm._Plan(dh, ds, depth - ds - dh, 1, 1)
     os.environ["BMMGPU_LOGICAL_DEVICES"] = "4"
+    # overlapped leaf groups: off / 1-2 reserved pairs, both pass orders, groups down to 1 leaf
+    ov, order, gmin = rng.choice(["0", "1", "1", "2"]), rng.choice(["0", "1"]), rng.choice(["1", "49", "343"])
+    os.environ.update({"BMMGPU_ALT_OVERLAP": ov, "BMMGPU_ALT_OVERLAP_ORDER": order, "BMMGPU_ALT_OVERLAP_MIN": gmin})
     # out of core (force_streaming): one device -> the sub-instance driver, several -> tiles
     ooc = rng.random() < 0.3 and n >= 512
     opts = bmm._opts(0, leaf_log2=leaf, device_mask=mask, force_streaming=ooc)
     st = lib.bmmgpu_multiply(pa, pb, pc, n, algo, ctypes.byref(plan), 1, ctypes.byref(opts))
     case = {"kind": "alt", "n": n, "algo": algo, "leaf": leaf, "plan": [dh, ds, depth - ds - dh], "pinned": pinned,
-            "device_mask": mask, "ooc": ooc}
+            "device_mask": mask, "ooc": ooc, "overlap": [ov, order, gmin]}
     if st != 0:
         return {**case, "status": st, "error": lib.bmmgpu_last_error().decode()}
     if not np.array_equal(words_of(hc), want):
